@@ -1,0 +1,224 @@
+/*
+ * phj.h -- C ABI of libphj.so, the B200 (sm_100a) patchy semi-Lagrangian
+ * HJB engine.  Plain C types only: every array is a raw DEVICE pointer owned
+ * by the caller (the Python host package keeps them in torch tensors), every
+ * call takes the CUDA stream to run on and returns PHJ_OK or an error code
+ * (phj_last_error() gives the message; no C++ exception crosses the ABI).
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/patchyhjb/):
+ *   phj_solve            _kernels.sweep_batch       _kernels.py:18-106, driven by
+ *                        solver.solve               solver.py:201-279 (whole loop
+ *                        on device: sweeps, convergence, per-patch stop) and by
+ *                        patchy.solve_patches       patchy.py:304-389 (all patches
+ *                        in one launch)
+ *   phj_feedback         _kernels.feedback_batch    _kernels.py:109-167,
+ *                        solver.extract_feedback    solver.py:413-443
+ *   phj_transport        _kernels.transport_batch   _kernels.py:170-204,
+ *                        patchy.transport_color     patchy.py:183-219
+ *   phj_lift             grid.interpolate_many      grid.py:446-465 (patchy.py:146-148)
+ *   phj_argmax_update,   patchy.assemble_patches    patchy.py:236-301
+ *   phj_assemble_*
+ *   phj_classify         solver.classify_nodes      solver.py:101-108
+ *   phj_error_partials   analysis.error_report      analysis.py:50-63
+ *
+ * Layout: fields are ghost-padded C-order arrays (grid.py:69-85), one ghost
+ * layer, last internal axis fastest.  The host may permute user axes so that
+ * a stencil "class" axis (Dubins heading) is internal axis 0; periodic axes
+ * keep ghost layers as copies of the opposite interior layer.
+ */
+#ifndef PHJ_H
+#define PHJ_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PHJ_OK 0
+#define PHJ_ERR_ARG 1
+#define PHJ_ERR_CUDA 2
+#define PHJ_ERR_UNSUPPORTED 3
+
+#define PHJ_F64 0
+#define PHJ_F32 1
+
+#define PHJ_RULE_REF 0     /* u <- min_a I[u](x + h f) + h      (reference)   */
+#define PHJ_RULE_KRUZKOV 1 /* v <- min_a beta I[v](x + h f) + 1 - beta        */
+
+#define PHJ_COST_NODE 0 /* step cost per node (f = c(x) a, |a| = 1): hoisted  */
+#define PHJ_COST_CTRL 1 /* step cost per stencil entry (translation/Dubins)   */
+
+/* patch labels in the ext label array (int16) */
+#define PHJ_LAB_FIXED (-1)  /* not swept, readable (frozen / inactive data)    */
+#define PHJ_LAB_TARGET (-2) /* target: value 0, readable by every patch       */
+#define PHJ_LAB_HARD (-3)   /* ghost / obstacle / unreachable: never readable */
+
+/* patch-map codes (patchy.py:40-43) */
+#define PHJ_UNREACHABLE (-1)
+#define PHJ_TARGET (-2)
+#define PHJ_OBSTACLE (-3)
+#define PHJ_UNCOVERED (-4)
+
+typedef struct phj_grid {
+  int32_t dim;         /* 2 or 3 */
+  int32_t periodic[3]; /* per internal axis */
+  int64_t shape[3];    /* interior nodes per internal axis */
+  int64_t ext[3];      /* shape + 2 */
+  int64_t strides[3];  /* ext strides in nodes */
+  double lo[3];
+  double spacing[3];
+  double ext_lo[3];
+  double k; /* step length |h f| = k (grid.py:67) */
+} phj_grid;
+
+/* Node-independent interpolation stencils, one set per class (class index =
+ * interior index along internal axis 0 when n_classes > 1).  Entries of a
+ * class are sorted by foot octant; octant bit ax = foot on the + side of
+ * internal axis ax, corner bit ax = upper face of that octant cell.  All
+ * pointers are device pointers. */
+typedef struct phj_stencil {
+  int32_t dim;
+  int32_t n_classes;
+  int32_t n_controls; /* entries per class */
+  int32_t cost_mode;  /* PHJ_COST_NODE or PHJ_COST_CTRL */
+  const int32_t* oct_start; /* [n_classes][2^dim + 1] */
+  const int32_t* ctrl;      /* [n_classes][nc] original control index */
+  const uint32_t* nzmask;   /* [n_classes][nc] nonzero-weight 3^dim positions */
+  const double* weights;    /* [n_classes][nc][2^dim] */
+  const double* cost;       /* [n_classes][nc] step cost (COST_CTRL); < 0 skips */
+} phj_stencil;
+
+typedef struct phj_solve_args {
+  phj_grid grid;
+  phj_stencil st;
+  int32_t dtype; /* PHJ_F64 / PHJ_F32 */
+  int32_t rule;  /* PHJ_RULE_* */
+  void* v0;      /* ext field, ping */
+  void* v1;      /* ext field, pong; both hold the start field on entry */
+  const int16_t* lab;     /* ext labels: >= 0 patch id (swept), PHJ_LAB_* */
+  const uint32_t* fmask;  /* ext foreign-position masks (phj_fmask_*) */
+  const void* coef;       /* per ext node: h (REF) or beta (KRUZKOV) in dtype,
+                             < 0 = no admissible control; NULL => coef0 */
+  double coef0;
+  int32_t n_patches;
+  int32_t max_sweeps;
+  const uint8_t* mine; /* [n_patches] patches this device sweeps; NULL = all */
+  double tol;
+  void* workspace;            /* phj_solve_workspace_bytes() bytes */
+  int32_t* patch_sweeps;      /* out [n_patches]: sweeps to converge, -(cap) if not */
+  double* maxch_hist;         /* out [max_sweeps * n_patches], may be NULL */
+  unsigned long long* evals;  /* out [1]: candidate evaluations performed */
+  int32_t* info;              /* out [4]: total sweeps, index of result buffer,
+                                 tiles processed, launches */
+  void* stream;               /* cudaStream_t */
+} phj_solve_args;
+
+int64_t phj_solve_workspace_bytes(const phj_grid* g, int32_t n_patches, int32_t max_sweeps);
+int phj_solve(const phj_solve_args* a);
+
+/* foreign-position masks: bit p set when 3^dim neighbour p of the node is not
+ * readable by it.  From patch labels (corner label not in {own, TARGET,
+ * FIXED}) or from a caller hard mask (uint8 per ext node, non-zero = hard). */
+int phj_fmask_from_labels(const phj_grid* g, const int16_t* lab, uint32_t* fmask, void* stream);
+int phj_fmask_from_hard(const phj_grid* g, const uint8_t* hard, uint32_t* fmask, void* stream);
+
+/* Argmin control per interior serial (out is indexed by internal serial).
+ * unreach: own-value threshold (0.5*sentinel REF, 1.0 KRUZKOV); reads reject
+ * only where `fmask` (built from the ghost/obstacle hard mask) says so.
+ * The rule is applied per candidate and ties go to the lowest ORIGINAL
+ * control index (strict <, _kernels.py:162-165). */
+int phj_feedback(const phj_grid* g, const phj_stencil* st, int32_t dtype, int32_t rule,
+                 const void* v, const int8_t* kind, const uint32_t* fmask, const void* coef,
+                 double coef0, double unreach, int32_t* out, unsigned long long* evals,
+                 void* stream);
+
+/* Colour transport of one target part to max|change| <= tol (Jacobi, whole
+ * loop on device).  phi0/phi1 hold the start field; movers have fb >= 0 and
+ * kind == 0.  Result buffer index and sweeps go to info[0..1]. */
+typedef struct phj_transport_args {
+  phj_grid grid;
+  phj_stencil st;
+  double* phi0;
+  double* phi1;
+  const int32_t* fb;    /* per internal serial, original control index or -1 */
+  const int8_t* kind;   /* per internal serial */
+  double tol;
+  int32_t max_sweeps;
+  void* workspace;      /* phj_solve_workspace_bytes(g, 1, max_sweeps) */
+  int32_t* info;        /* out [4]: sweeps, result buffer, converged, tiles */
+  unsigned long long* updates; /* out [1] */
+  void* stream;
+} phj_transport_args;
+int phj_transport(const phj_transport_args* a);
+
+/* Saturating multilinear lift of a coarse ext field to fine ext interior. */
+int phj_lift(const phj_grid* gc, const phj_grid* gf, int32_t dtype, const void* vc, void* vf,
+             double sat_threshold, double sat_value, int32_t saturate, void* stream);
+
+/* running argmax over colour fields (strict >, patchy.py:251-256) */
+int phj_argmax_update(const phj_grid* g, const double* phi, int32_t j, double* best_val,
+                      int32_t* best_idx, void* stream);
+/* codes (patchy.py:258-262) */
+int phj_assemble_codes(const phj_grid* g, const double* best_val, const int32_t* best_idx,
+                       const uint8_t* mask, const int8_t* kind, int32_t* color, void* stream);
+/* one order-free majority-repair pass (patchy.py:264-282); n_filled/n_open out */
+int phj_assemble_repair(const phj_grid* g, const int32_t* color_in, int32_t* color_out,
+                        int32_t n_colors, int32_t* counters, void* stream);
+/* leftovers -> 0, boundary flags, patch labels for the solve (patchy.py:284-300) */
+int phj_assemble_finish(const phj_grid* g, int32_t* color, uint8_t* boundary, int16_t* lab,
+                        int32_t* counters, void* stream);
+
+/* node classification for analytic targets/obstacles: kind per serial */
+typedef struct phj_shapes {
+  int32_t n_balls;
+  const double* balls; /* host: [n][5] centre[3], radius, ncomp (leading coords) */
+  int32_t n_planes;
+  const double* planes; /* host: [n][3] axis, offset, tol */
+  int32_t n_obst_circles;
+  const double* obst_circles; /* host: [n][5] cx, cy, cz, r, ncomp */
+  int32_t n_obst_boxes;
+  const double* obst_boxes; /* host: [n][7] ncomp, lo[3], hi[3] */
+} phj_shapes;
+int phj_classify(const phj_grid* g, const phj_shapes* shapes, const int32_t* user_axis,
+                 int8_t* kind, void* stream);
+
+/* per-node coefficient: h = k / speed (REF) or beta = exp(-h) (KRUZKOV);
+ * speed from an analytic model or a per-serial array; < eps => -1. */
+typedef struct phj_speed_model {
+  int32_t kind;     /* 0 constant, 1 array, 2 sin-product: c0 + amp * prod sin(w x_ax) */
+  double c0;
+  double amp;
+  double omega[3];  /* per user axis, 0 => factor omitted */
+  double ctrl_norm; /* |a| of the (unit) control set */
+  double eps;       /* degeneracy threshold on |f| */
+  const double* speed; /* kind 1: per internal serial, device */
+} phj_speed_model;
+int phj_node_coef(const phj_grid* g, const phj_speed_model* m, const int32_t* user_axis,
+                  int32_t dtype, int32_t rule, void* coef, void* stream);
+
+/* field init/merge: v = target ? 0 : unreached everywhere (ghosts included) */
+int phj_init_field(const phj_grid* g, int32_t dtype, const int8_t* kind, double unreached,
+                   void* v, void* stream);
+/* T <-> Kruzkov v conversions over a whole ext array (n entries) */
+int phj_to_kruzkov(int64_t n, int32_t dtype, const double* T, void* v, double half_sentinel,
+                   void* stream);
+int phj_from_kruzkov(int64_t n, int32_t dtype, const void* v, double* T, double sentinel,
+                     void* stream);
+/* copy interior ghost layers for periodic axes */
+int phj_sync_periodic(const phj_grid* g, int32_t elem_bytes, void* v, void* stream);
+
+/* E1/Einf partial sums: out[0]=sum|a-b|, out[1]=max, out[2]=compared count */
+int phj_error_partials(int64_t n, const double* a, const double* b, double half_a,
+                       double half_b, double* out, void* stream);
+
+/* FP64/FP32 pipe peak microbenchmark: flops executed into out[0] */
+int phj_peak_flops(int32_t dtype, int32_t iters, double* sink, void* stream);
+
+const char* phj_last_error(void);
+int phj_num_sms(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PHJ_H */

@@ -1,0 +1,151 @@
+// phj_common.cuh -- shared device helpers for the sm_100a patchy SL engine.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/phj.h"
+
+namespace phj {
+
+constexpr int kThreads = 256;
+constexpr int kMaxPatches = 1024;
+constexpr int kSmemPatchReduce = 64;  // per-CTA patch max reduction when R <= 64
+
+// Tile geometry: each warp owns one row segment of 32*NB consecutive nodes
+// along the fastest internal axis (so a warp's class index -- internal axis
+// 0 -- is uniform); a CTA owns TY (x TZ) such rows.
+template <int D> struct Tile;
+template <> struct Tile<2> {
+  static constexpr int NB = 4, TX = 128, TY = 8, TZ = 1;
+};
+template <> struct Tile<3> {
+  static constexpr int NB = 2, TX = 64, TY = 4, TZ = 2;
+};
+
+struct TileGrid {
+  int n[3];      // tiles per internal axis (axis 0 slowest)
+  int total;
+};
+
+template <int D>
+__host__ __device__ inline TileGrid make_tile_grid(const phj_grid& g) {
+  TileGrid t;
+  if (D == 2) {
+    t.n[0] = (int)((g.shape[0] + Tile<2>::TY - 1) / Tile<2>::TY);
+    t.n[1] = (int)((g.shape[1] + Tile<2>::TX - 1) / Tile<2>::TX);
+    t.n[2] = 1;
+    t.total = t.n[0] * t.n[1];
+  } else {
+    t.n[0] = (int)((g.shape[0] + Tile<3>::TZ - 1) / Tile<3>::TZ);
+    t.n[1] = (int)((g.shape[1] + Tile<3>::TY - 1) / Tile<3>::TY);
+    t.n[2] = (int)((g.shape[2] + Tile<3>::TX - 1) / Tile<3>::TX);
+    t.total = t.n[0] * t.n[1] * t.n[2];
+  }
+  return t;
+}
+
+// Node-space origin of tile `t` (interior indices along each internal axis).
+template <int D>
+__device__ inline void tile_origin(const TileGrid& tg, int t, int o[3]) {
+  if (D == 2) {
+    int tx = t % tg.n[1], ty = t / tg.n[1];
+    o[0] = ty * Tile<2>::TY;
+    o[1] = tx * Tile<2>::TX;
+    o[2] = 0;
+  } else {
+    int tx = t % tg.n[2];
+    int r = t / tg.n[2];
+    int ty = r % tg.n[1], tz = r / tg.n[1];
+    o[0] = tz * Tile<3>::TZ;
+    o[1] = ty * Tile<3>::TY;
+    o[2] = tx * Tile<3>::TX;
+  }
+}
+
+// Mark the 3^D neighbour tiles of tile `t` active for the next sweep
+// (called by threads 0..3^D-1 of a CTA whose tile changed).
+template <int D>
+__device__ inline void mark_neighbour(const TileGrid& tg, const phj_grid& g, int t, int nid,
+                                      int* next_flags, int* next_list, int* next_count) {
+  int c[3], n[3] = {tg.n[0], tg.n[1], tg.n[2]};
+  if (D == 2) {
+    c[1] = t % n[1];
+    c[0] = t / n[1];
+    int d0 = nid / 3 - 1, d1 = nid % 3 - 1;
+    int a = c[0] + d0, b = c[1] + d1;
+    if (g.periodic[0]) a = (a + n[0]) % n[0];
+    if (g.periodic[1]) b = (b + n[1]) % n[1];
+    if (a < 0 || a >= n[0] || b < 0 || b >= n[1]) return;
+    int nt = a * n[1] + b;
+    if (atomicExch(&next_flags[nt], 1) == 0) next_list[atomicAdd(next_count, 1)] = nt;
+  } else {
+    c[2] = t % n[2];
+    int r = t / n[2];
+    c[1] = r % n[1];
+    c[0] = r / n[1];
+    int d0 = nid / 9 - 1, d1 = (nid / 3) % 3 - 1, d2 = nid % 3 - 1;
+    int a = c[0] + d0, b = c[1] + d1, e = c[2] + d2;
+    if (g.periodic[0]) a = (a + n[0]) % n[0];
+    if (g.periodic[1]) b = (b + n[1]) % n[1];
+    if (g.periodic[2]) e = (e + n[2]) % n[2];
+    if (a < 0 || a >= n[0] || b < 0 || b >= n[1] || e < 0 || e >= n[2]) return;
+    int nt = (a * n[1] + b) * n[2] + e;
+    if (atomicExch(&next_flags[nt], 1) == 0) next_list[atomicAdd(next_count, 1)] = nt;
+  }
+}
+
+// Workspace carve-up shared by solve/transport.
+struct Workspace {
+  int* list[2];
+  int* flags[2];
+  int* counts;  // [max_sweeps + 1]
+};
+
+inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+template <int D>
+inline int64_t workspace_bytes(const phj_grid& g, int max_sweeps) {
+  TileGrid tg = make_tile_grid<D>(g);
+  int64_t b = 0;
+  b += 4 * align_up((int64_t)tg.total * 4, 256);
+  b += align_up((int64_t)(max_sweeps + 2) * 4, 256);
+  return b;  // transport appends max_sweeps doubles after align_up(b, 256)
+}
+
+template <int D>
+inline Workspace carve(const phj_grid& g, void* base) {
+  TileGrid tg = make_tile_grid<D>(g);
+  char* p = (char*)base;
+  Workspace w;
+  int64_t tb = align_up((int64_t)tg.total * 4, 256);
+  w.list[0] = (int*)p; p += tb;
+  w.list[1] = (int*)p; p += tb;
+  w.flags[0] = (int*)p; p += tb;
+  w.flags[1] = (int*)p; p += tb;
+  w.counts = (int*)p;
+  return w;
+}
+
+__device__ inline unsigned long long dbits(double x) {
+  return (unsigned long long)__double_as_longlong(x);
+}
+
+template <typename T> __device__ __host__ constexpr T big_value();
+template <> __device__ __host__ constexpr double big_value<double>() { return 1.0e300; }
+template <> __device__ __host__ constexpr float big_value<float>() { return 1.0e30f; }
+
+__device__ inline double ld_cg(const double* p) { return __ldcg(p); }
+__device__ inline unsigned long long ld_cg(const unsigned long long* p) { return __ldcg(p); }
+__device__ inline int ld_cg(const int* p) { return __ldcg(p); }
+
+}  // namespace phj
+
+// error plumbing shared by the .cu translation units
+void phj_set_error(const char* fmt, ...);
+int phj_check_cuda(cudaError_t e, const char* what);
+#define PHJ_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) return phj_check_cuda(_e, #call); \
+  } while (0)

@@ -1,0 +1,686 @@
+// phj_ops.cu -- lift, labelling (argmax / majority repair / boundary),
+// classification, per-node coefficients, conversions, error metrics and the
+// FP pipe peak probe.  All are HBM-bound elementwise/stencil kernels sized
+// as grid-stride loops over a multiple of the SM count.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "phj_common.cuh"
+
+static thread_local char g_err[512] = "";
+
+void phj_set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int phj_check_cuda(cudaError_t e, const char* what) {
+  phj_set_error("CUDA error %s (%d) in %s", cudaGetErrorString(e), (int)e, what);
+  return PHJ_ERR_CUDA;
+}
+
+extern "C" const char* phj_last_error(void) { return g_err; }
+extern "C" int phj_num_sms(void);
+
+namespace phj {
+
+__host__ __device__ inline int64_t n_interior(const phj_grid& g) {
+  return g.shape[0] * g.shape[1] * (g.dim == 3 ? g.shape[2] : 1);
+}
+
+__device__ inline void unravel(const phj_grid& g, int64_t s, int c[3]) {
+  c[0] = c[1] = c[2] = 0;
+  for (int ax = g.dim - 1; ax >= 0; --ax) {
+    c[ax] = (int)(s % g.shape[ax]);
+    s /= g.shape[ax];
+  }
+}
+
+__device__ inline int64_t iflat(const phj_grid& g, const int c[3]) {
+  int64_t f = 0;
+  for (int ax = 0; ax < g.dim; ++ax) f += (int64_t)(c[ax] + 1) * g.strides[ax];
+  return f;
+}
+
+// node coordinate lo + i*spacing with no FMA contraction (grid.py:293-295)
+__device__ inline double coord(const phj_grid& g, int ax, int i) {
+  return __dadd_rn(g.lo[ax], __dmul_rn((double)i, g.spacing[ax]));
+}
+
+inline int grid_blocks(int64_t n, int per = 256) {
+  int64_t b = (n + per - 1) / per;
+  int64_t cap = 32LL * (phj_num_sms() > 0 ? phj_num_sms() : 148);
+  if (b > cap) b = cap;
+  return (int)(b < 1 ? 1 : b);
+}
+
+// ---------------------------------------------------------------------------
+// lift: saturating multilinear interpolation of the coarse field at fine
+// nodes (grid.py:446-465).  Locate/weights/sum orders reproduce numpy's
+// (sequential 4-term sum, pairwise 8-term tree) with explicit _rn intrinsics.
+template <typename T>
+__device__ inline T t_mul(T a, T b);
+template <> __device__ inline double t_mul<double>(double a, double b) { return __dmul_rn(a, b); }
+template <> __device__ inline float t_mul<float>(float a, float b) { return __fmul_rn(a, b); }
+template <typename T>
+__device__ inline T t_add(T a, T b);
+template <> __device__ inline double t_add<double>(double a, double b) { return __dadd_rn(a, b); }
+template <> __device__ inline float t_add<float>(float a, float b) { return __fadd_rn(a, b); }
+
+template <typename T>
+__global__ void lift_kernel(phj_grid gc, phj_grid gf, const T* __restrict__ vc, T* __restrict__ vf,
+                            double thr, double sat, int saturate) {
+  const int64_t N = n_interior(gf);
+  const int d = gf.dim;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < N;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    int c[3];
+    unravel(gf, s, c);
+    int64_t cell[3];
+    double loc[3];
+    for (int ax = 0; ax < d; ++ax) {
+      const double x = coord(gf, ax, c[ax]);
+      const double t = __ddiv_rn(__dsub_rn(x, gc.ext_lo[ax]), gc.spacing[ax]);
+      int64_t ce = (int64_t)floor(t);
+      const int64_t nmax = gc.ext[ax] - 1;
+      if (ce < 0) ce = 0;
+      if (ce > nmax - 1) ce = nmax - 1;
+      double l = __dsub_rn(t, (double)ce);
+      if (l < 1.0e-12) l = 0.0;
+      if (l > 1.0 - 1.0e-12) l = 1.0;
+      cell[ax] = ce;
+      loc[ax] = l;
+    }
+    T terms[8];
+    bool bad = false;
+    const int ncor = 1 << d;
+    for (int k = 0; k < ncor; ++k) {
+      double w = 1.0;
+      int64_t f = 0;
+      for (int ax = 0; ax < d; ++ax) {
+        const int up = (k >> ax) & 1;
+        w = __dmul_rn(w, up ? loc[ax] : __dsub_rn(1.0, loc[ax]));
+        int64_t e = cell[ax] + up;
+        if (gc.periodic[ax]) {
+          if (e == 0) e = gc.shape[ax];
+          else if (e == gc.shape[ax] + 1) e = 1;
+        }
+        f += e * gc.strides[ax];
+      }
+      const T cv = vc[f];
+      terms[k] = t_mul<T>((T)w, cv);
+      if (w > 0.0 && (double)cv >= thr) bad = true;
+    }
+    T v;
+    if (ncor == 4) {
+      v = t_add<T>(t_add<T>(t_add<T>(terms[0], terms[1]), terms[2]), terms[3]);
+    } else {
+      v = t_add<T>(t_add<T>(t_add<T>(terms[0], terms[1]), t_add<T>(terms[2], terms[3])),
+                   t_add<T>(t_add<T>(terms[4], terms[5]), t_add<T>(terms[6], terms[7])));
+    }
+    vf[iflat(gf, c)] = (saturate && bad) ? (T)sat : v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// labelling (patchy.py:236-301)
+
+__global__ void argmax_kernel(phj_grid g, const double* __restrict__ phi, int j,
+                              double* __restrict__ best_val, int32_t* __restrict__ best_idx) {
+  const int64_t N = n_interior(g);
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < N;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    int c[3];
+    unravel(g, s, c);
+    const double v = phi[iflat(g, c)];
+    if (v > best_val[s]) {
+      best_val[s] = v;
+      best_idx[s] = j;
+    }
+  }
+}
+
+__global__ void codes_kernel(phj_grid g, const double* __restrict__ best_val,
+                             const int32_t* __restrict__ best_idx, const uint8_t* __restrict__ mask,
+                             const int8_t* __restrict__ kind, int32_t* __restrict__ color) {
+  const int64_t N = n_interior(g);
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < N;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    int32_t col = best_val[s] > 0.0 ? best_idx[s] : PHJ_UNCOVERED;
+    if (mask && mask[s]) col = PHJ_UNREACHABLE;
+    if (kind[s] == 2) col = PHJ_OBSTACLE;
+    if (kind[s] == 1) col = PHJ_TARGET;
+    color[s] = col;
+  }
+}
+
+// face neighbour colour of serial s along axis ax, step +-1 (edge => -9;
+// periodic axes wrap, an extension for the Dubins heading)
+__device__ inline int32_t face_nb(const phj_grid& g, const int32_t* col, const int c[3], int ax,
+                                  int step) {
+  int cc[3] = {c[0], c[1], c[2]};
+  cc[ax] += step;
+  if (cc[ax] < 0 || cc[ax] >= g.shape[ax]) {
+    if (!g.periodic[ax]) return -9;
+    cc[ax] = (cc[ax] + (int)g.shape[ax]) % (int)g.shape[ax];
+  }
+  int64_t s = 0;
+  for (int a = 0; a < g.dim; ++a) s = s * g.shape[a] + cc[a];
+  return col[s];
+}
+
+__global__ void repair_kernel(phj_grid g, const int32_t* __restrict__ cin, int32_t* __restrict__ cout,
+                              int n_colors, int32_t* counters) {
+  const int64_t N = n_interior(g);
+  int filled = 0, open = 0;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < N;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t own = cin[s];
+    if (own != PHJ_UNCOVERED) {
+      cout[s] = own;
+      continue;
+    }
+    ++open;
+    int c[3];
+    unravel(g, s, c);
+    int32_t nbc[6];
+    int nn = 0;
+    for (int ax = 0; ax < g.dim; ++ax) {
+      nbc[nn++] = face_nb(g, cin, c, ax, -1);
+      nbc[nn++] = face_nb(g, cin, c, ax, +1);
+    }
+    // max count, lowest colour on count ties (patchy.py:272-278)
+    int best_count = 0, best_color = PHJ_UNCOVERED;
+    for (int i = 0; i < nn; ++i) {
+      const int32_t cc = nbc[i];
+      if (cc < 0 || cc >= n_colors) continue;
+      int cnt = 0;
+      for (int k = 0; k < nn; ++k) cnt += nbc[k] == cc;
+      if (cnt > best_count || (cnt == best_count && cc < best_color)) {
+        best_count = cnt;
+        best_color = cc;
+      }
+    }
+    if (best_count > 0) {
+      cout[s] = best_color;
+      ++filled;
+    } else {
+      cout[s] = PHJ_UNCOVERED;
+    }
+  }
+  if (filled) atomicAdd(&counters[0], filled);
+  if (open) atomicAdd(&counters[1], open);
+}
+
+__global__ void finish_kernel(phj_grid g, int32_t* __restrict__ color, uint8_t* __restrict__ boundary,
+                              int16_t* __restrict__ lab, int32_t* counters) {
+  const int64_t N = n_interior(g);
+  int unc = 0;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < N;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    int32_t own = color[s];
+    if (own == PHJ_UNCOVERED) ++unc;
+  }
+  if (unc) atomicAdd(&counters[2], unc);
+}
+
+__global__ void finish2_kernel(phj_grid g, int32_t* __restrict__ color) {
+  const int64_t N = n_interior(g);
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < N;
+       s += (int64_t)gridDim.x * blockDim.x)
+    if (color[s] == PHJ_UNCOVERED) color[s] = 0;
+}
+
+__global__ void finish3_kernel(phj_grid g, const int32_t* __restrict__ color,
+                               uint8_t* __restrict__ boundary, int16_t* __restrict__ lab) {
+  const int64_t N = n_interior(g);
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < N;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    int c[3];
+    unravel(g, s, c);
+    const int32_t own = color[s];
+    bool b = false;
+    if (own >= 0) {
+      for (int ax = 0; ax < g.dim; ++ax)
+        for (int st = -1; st <= 1; st += 2) {
+          const int32_t nb = face_nb(g, color, c, ax, st);
+          b |= nb >= 0 && nb != own;
+        }
+    }
+    if (boundary) boundary[s] = b;
+    if (lab) {
+      const int16_t l = own >= 0 ? (int16_t)own : (own == PHJ_TARGET ? PHJ_LAB_TARGET : PHJ_LAB_HARD);
+      lab[iflat(g, c)] = l;
+    }
+  }
+}
+
+// ghost planes of periodic axes <- opposite interior planes (all ext entries)
+template <typename E>
+__global__ void periodic_kernel(phj_grid g, E* v, int ax) {
+  // iterate over the ext array restricted to plane index 0 and M+1 of axis ax
+  int64_t plane = 1;
+  for (int a = 0; a < g.dim; ++a)
+    if (a != ax) plane *= g.ext[a];
+  const int64_t M = g.shape[ax];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < plane;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    // decode i over the other axes (C order, skipping ax)
+    int64_t rem = i, f = 0;
+    for (int a = g.dim - 1; a >= 0; --a) {
+      if (a == ax) continue;
+      const int64_t ca = rem % g.ext[a];
+      rem /= g.ext[a];
+      f += ca * g.strides[a];
+    }
+    v[f + 0 * g.strides[ax]] = v[f + M * g.strides[ax]];
+    v[f + (M + 1) * g.strides[ax]] = v[f + 1 * g.strides[ax]];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// classification (solver.py:101-108 with problems.py:136-144, :206-219)
+
+struct Shapes {
+  int n_balls, n_planes, n_circ, n_box;
+  double balls[16][5];  // centre[3], radius, number of leading coordinates used
+  double planes[8][3];
+  double circ[8][5];
+  double box[8][7];
+};
+
+__global__ void classify_kernel(phj_grid g, Shapes sh, int ua0, int ua1, int ua2,
+                                int8_t* __restrict__ kind) {
+  const int64_t N = n_interior(g);
+  const int d = g.dim;
+  const int ua[3] = {ua0, ua1, ua2};
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < N;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    int c[3];
+    unravel(g, s, c);
+    double X[3] = {0, 0, 0};  // user-axis coordinates
+    for (int ax = 0; ax < d; ++ax) X[ua[ax]] = coord(g, ax, c[ax]);
+    bool tgt = false;
+    for (int b = 0; b < sh.n_balls; ++b) {
+      double ss = 0.0;
+      const int nco = (int)sh.balls[b][4];
+      for (int a = 0; a < nco; ++a) {
+        const double q = __dsub_rn(X[a], sh.balls[b][a]);
+        ss = (a == 0) ? __dmul_rn(q, q) : __dadd_rn(ss, __dmul_rn(q, q));
+      }
+      tgt |= __dsqrt_rn(ss) <= sh.balls[b][3];
+    }
+    for (int pl = 0; pl < sh.n_planes; ++pl) {
+      const int a = (int)sh.planes[pl][0];
+      tgt |= fabs(__dsub_rn(X[a], sh.planes[pl][1])) <= sh.planes[pl][2];
+    }
+    bool obs = false;
+    for (int o = 0; o < sh.n_circ; ++o) {
+      const int nco = (int)sh.circ[o][4];
+      double ss = 0.0;
+      for (int a = 0; a < nco; ++a) {
+        const double q = __dsub_rn(X[a], sh.circ[o][a]);
+        ss = (a == 0) ? __dmul_rn(q, q) : __dadd_rn(ss, __dmul_rn(q, q));
+      }
+      obs |= __dsqrt_rn(ss) <= sh.circ[o][3];
+    }
+    for (int o = 0; o < sh.n_box; ++o) {
+      const int nco = (int)sh.box[o][0];
+      bool in = true;
+      for (int a = 0; a < nco; ++a) in &= X[a] >= sh.box[o][1 + a] && X[a] <= sh.box[o][4 + a];
+      obs |= in;
+    }
+    kind[s] = obs ? 2 : (tgt ? 1 : 0);
+  }
+}
+
+// per-node h (REF) or beta (KRUZKOV): speed from an analytic model or array
+template <typename T>
+__global__ void coef_kernel(phj_grid g, phj_speed_model m, int ua0, int ua1, int ua2, int rule,
+                            T* __restrict__ coef) {
+  const int64_t N = n_interior(g);
+  const int d = g.dim;
+  const int ua[3] = {ua0, ua1, ua2};
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < N;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    int c[3];
+    unravel(g, s, c);
+    double sp;
+    if (m.kind == 0) {
+      sp = m.c0;
+    } else if (m.kind == 1) {
+      sp = m.speed[s];
+    } else {
+      double X[3] = {0, 0, 0};
+      for (int ax = 0; ax < d; ++ax) X[ua[ax]] = coord(g, ax, c[ax]);
+      double prod = 1.0;
+      for (int a = 0; a < d; ++a)
+        if (m.omega[a] != 0.0) prod *= sin(m.omega[a] * X[a]);
+      sp = m.c0 + m.amp * prod;
+    }
+    const double fnorm = fabs(sp) * m.ctrl_norm;
+    double out;
+    if (!(fnorm >= m.eps)) {
+      out = -1.0;
+    } else {
+      const double h = g.k / fnorm;
+      out = (rule == PHJ_RULE_KRUZKOV) ? exp(-h) : h;
+    }
+    coef[iflat(g, c)] = (T)out;
+  }
+}
+
+template <typename T>
+__global__ void init_field_kernel(phj_grid g, const int8_t* __restrict__ kind, double unreached,
+                                  T* __restrict__ v) {
+  const int64_t NE = g.ext[0] * g.ext[1] * (g.dim == 3 ? g.ext[2] : 1);
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < NE;
+       f += (int64_t)gridDim.x * blockDim.x) {
+    int64_t rem = f;
+    int c[3];
+    bool interior = true;
+    int64_t s = 0;
+    for (int ax = g.dim - 1; ax >= 0; --ax) {
+      c[ax] = (int)(rem % g.ext[ax]) - 1;
+      rem /= g.ext[ax];
+    }
+    for (int ax = 0; ax < g.dim; ++ax) {
+      interior &= c[ax] >= 0 && c[ax] < g.shape[ax];
+      s = s * g.shape[ax] + c[ax];
+    }
+    v[f] = (interior && kind && kind[s] == 1) ? (T)0 : (T)unreached;
+  }
+}
+
+template <typename T>
+__global__ void to_kruzkov_kernel(int64_t n, const double* __restrict__ Tv, T* __restrict__ v,
+                                  double half) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double t = Tv[i];
+    v[i] = (T)((t >= half) ? 1.0 : -expm1(-t));
+  }
+}
+
+template <typename T>
+__global__ void from_kruzkov_kernel(int64_t n, const T* __restrict__ v, double* __restrict__ Tv,
+                                    double sentinel) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double x = (double)v[i];
+    Tv[i] = (x >= 1.0) ? sentinel : -log1p(-x);
+  }
+}
+
+__global__ void error_kernel(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                             double ha, double hb, double* out) {
+  double sum = 0.0, mx = 0.0;
+  double cnt = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double x = a[i], y = b[i];
+    if (x < ha && y < hb) {
+      const double dlt = fabs(x - y);
+      sum += dlt;
+      mx = fmax(mx, dlt);
+      cnt += 1.0;
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    sum += __shfl_xor_sync(0xffffffffu, sum, off);
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&out[0], sum);
+    atomicMax((unsigned long long*)&out[1], dbits(mx));
+    atomicAdd(&out[2], cnt);
+  }
+}
+
+// FP64 / FP32 pipe peak probe: 8 independent FMA chains per thread
+template <typename T>
+__global__ void __launch_bounds__(256) peak_kernel(int iters, T* sink) {
+  T a[8];
+  const T m = (T)0.999999, c = (T)1e-7;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = (T)(threadIdx.x + i);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = fma(a[i], m, c);
+    }
+  }
+  T s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += a[i];
+  if (s == (T)12345.678) sink[0] = s;
+}
+
+}  // namespace phj
+
+using namespace phj;
+
+extern "C" int phj_lift(const phj_grid* gc, const phj_grid* gf, int32_t dtype, const void* vc,
+                        void* vf, double sat_threshold, double sat_value, int32_t saturate,
+                        void* stream) {
+  if (!gc || !gf || !vc || !vf || gc->dim != gf->dim) {
+    phj_set_error("phj_lift: bad arguments");
+    return PHJ_ERR_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nb = grid_blocks(n_interior(*gf));
+  if (dtype == PHJ_F32)
+    lift_kernel<float><<<nb, 256, 0, s>>>(*gc, *gf, (const float*)vc, (float*)vf, sat_threshold,
+                                          sat_value, saturate);
+  else
+    lift_kernel<double><<<nb, 256, 0, s>>>(*gc, *gf, (const double*)vc, (double*)vf,
+                                           sat_threshold, sat_value, saturate);
+  PHJ_CUDA(cudaGetLastError());
+  return PHJ_OK;
+}
+
+extern "C" int phj_argmax_update(const phj_grid* g, const double* phi, int32_t j, double* best_val,
+                                 int32_t* best_idx, void* stream) {
+  if (!g || !phi || !best_val || !best_idx) {
+    phj_set_error("phj_argmax_update: missing argument");
+    return PHJ_ERR_ARG;
+  }
+  argmax_kernel<<<grid_blocks(n_interior(*g)), 256, 0, (cudaStream_t)stream>>>(*g, phi, j, best_val,
+                                                                               best_idx);
+  PHJ_CUDA(cudaGetLastError());
+  return PHJ_OK;
+}
+
+extern "C" int phj_assemble_codes(const phj_grid* g, const double* best_val,
+                                  const int32_t* best_idx, const uint8_t* mask, const int8_t* kind,
+                                  int32_t* color, void* stream) {
+  if (!g || !best_val || !best_idx || !kind || !color) {
+    phj_set_error("phj_assemble_codes: missing argument");
+    return PHJ_ERR_ARG;
+  }
+  codes_kernel<<<grid_blocks(n_interior(*g)), 256, 0, (cudaStream_t)stream>>>(*g, best_val, best_idx,
+                                                                              mask, kind, color);
+  PHJ_CUDA(cudaGetLastError());
+  return PHJ_OK;
+}
+
+extern "C" int phj_assemble_repair(const phj_grid* g, const int32_t* color_in, int32_t* color_out,
+                                   int32_t n_colors, int32_t* counters, void* stream) {
+  if (!g || !color_in || !color_out || !counters) {
+    phj_set_error("phj_assemble_repair: missing argument");
+    return PHJ_ERR_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  PHJ_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(int32_t), s));
+  repair_kernel<<<grid_blocks(n_interior(*g)), 256, 0, s>>>(*g, color_in, color_out, n_colors,
+                                                            counters);
+  PHJ_CUDA(cudaGetLastError());
+  return PHJ_OK;
+}
+
+extern "C" int phj_assemble_finish(const phj_grid* g, int32_t* color, uint8_t* boundary,
+                                   int16_t* lab, int32_t* counters, void* stream) {
+  if (!g || !color || !counters) {
+    phj_set_error("phj_assemble_finish: missing argument");
+    return PHJ_ERR_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nb = grid_blocks(n_interior(*g));
+  PHJ_CUDA(cudaMemsetAsync(counters + 2, 0, sizeof(int32_t), s));
+  finish_kernel<<<nb, 256, 0, s>>>(*g, color, boundary, lab, counters);
+  finish2_kernel<<<nb, 256, 0, s>>>(*g, color);
+  finish3_kernel<<<nb, 256, 0, s>>>(*g, color, boundary, lab);
+  PHJ_CUDA(cudaGetLastError());
+  return PHJ_OK;
+}
+
+extern "C" int phj_classify(const phj_grid* g, const phj_shapes* sh, const int32_t* user_axis,
+                            int8_t* kind, void* stream) {
+  if (!g || !sh || !kind) {
+    phj_set_error("phj_classify: missing argument");
+    return PHJ_ERR_ARG;
+  }
+  Shapes S;
+  memset(&S, 0, sizeof(S));
+  const int d = g->dim;
+  if (sh->n_balls > 16 || sh->n_planes > 8 || sh->n_obst_circles > 8 || sh->n_obst_boxes > 8) {
+    phj_set_error("phj_classify: too many shapes");
+    return PHJ_ERR_UNSUPPORTED;
+  }
+  S.n_balls = sh->n_balls;
+  (void)d;
+  for (int b = 0; b < S.n_balls; ++b)
+    for (int i = 0; i < 5; ++i) S.balls[b][i] = sh->balls[b * 5 + i];
+  S.n_planes = sh->n_planes;
+  for (int p = 0; p < S.n_planes; ++p)
+    for (int i = 0; i < 3; ++i) S.planes[p][i] = sh->planes[p * 3 + i];
+  S.n_circ = sh->n_obst_circles;
+  for (int o = 0; o < S.n_circ; ++o)
+    for (int i = 0; i < 5; ++i) S.circ[o][i] = sh->obst_circles[o * 5 + i];
+  S.n_box = sh->n_obst_boxes;
+  for (int o = 0; o < S.n_box; ++o)
+    for (int i = 0; i < 7; ++i) S.box[o][i] = sh->obst_boxes[o * 7 + i];
+  int ua[3] = {0, 1, 2};
+  if (user_axis)
+    for (int i = 0; i < d; ++i) ua[i] = user_axis[i];
+  classify_kernel<<<grid_blocks(n_interior(*g)), 256, 0, (cudaStream_t)stream>>>(
+      *g, S, ua[0], ua[1], ua[2], kind);
+  PHJ_CUDA(cudaGetLastError());
+  return PHJ_OK;
+}
+
+extern "C" int phj_node_coef(const phj_grid* g, const phj_speed_model* m, const int32_t* user_axis,
+                             int32_t dtype, int32_t rule, void* coef, void* stream) {
+  if (!g || !m || !coef || (m->kind == 1 && !m->speed)) {
+    phj_set_error("phj_node_coef: missing argument");
+    return PHJ_ERR_ARG;
+  }
+  int ua[3] = {0, 1, 2};
+  if (user_axis)
+    for (int i = 0; i < g->dim; ++i) ua[i] = user_axis[i];
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nb = grid_blocks(n_interior(*g));
+  if (dtype == PHJ_F32)
+    coef_kernel<float><<<nb, 256, 0, s>>>(*g, *m, ua[0], ua[1], ua[2], rule, (float*)coef);
+  else
+    coef_kernel<double><<<nb, 256, 0, s>>>(*g, *m, ua[0], ua[1], ua[2], rule, (double*)coef);
+  PHJ_CUDA(cudaGetLastError());
+  return PHJ_OK;
+}
+
+extern "C" int phj_init_field(const phj_grid* g, int32_t dtype, const int8_t* kind,
+                              double unreached, void* v, void* stream) {
+  if (!g || !v) {
+    phj_set_error("phj_init_field: missing argument");
+    return PHJ_ERR_ARG;
+  }
+  const int64_t NE = g->ext[0] * g->ext[1] * (g->dim == 3 ? g->ext[2] : 1);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == PHJ_F32)
+    init_field_kernel<float><<<grid_blocks(NE), 256, 0, s>>>(*g, kind, unreached, (float*)v);
+  else
+    init_field_kernel<double><<<grid_blocks(NE), 256, 0, s>>>(*g, kind, unreached, (double*)v);
+  PHJ_CUDA(cudaGetLastError());
+  return PHJ_OK;
+}
+
+extern "C" int phj_to_kruzkov(int64_t n, int32_t dtype, const double* T, void* v,
+                              double half_sentinel, void* stream) {
+  if (!T || !v || n < 0) {
+    phj_set_error("phj_to_kruzkov: bad arguments");
+    return PHJ_ERR_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == PHJ_F32)
+    to_kruzkov_kernel<float><<<grid_blocks(n), 256, 0, s>>>(n, T, (float*)v, half_sentinel);
+  else
+    to_kruzkov_kernel<double><<<grid_blocks(n), 256, 0, s>>>(n, T, (double*)v, half_sentinel);
+  PHJ_CUDA(cudaGetLastError());
+  return PHJ_OK;
+}
+
+extern "C" int phj_from_kruzkov(int64_t n, int32_t dtype, const void* v, double* T,
+                                double sentinel, void* stream) {
+  if (!T || !v || n < 0) {
+    phj_set_error("phj_from_kruzkov: bad arguments");
+    return PHJ_ERR_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == PHJ_F32)
+    from_kruzkov_kernel<float><<<grid_blocks(n), 256, 0, s>>>(n, (const float*)v, T, sentinel);
+  else
+    from_kruzkov_kernel<double><<<grid_blocks(n), 256, 0, s>>>(n, (const double*)v, T, sentinel);
+  PHJ_CUDA(cudaGetLastError());
+  return PHJ_OK;
+}
+
+extern "C" int phj_sync_periodic(const phj_grid* g, int32_t elem_bytes, void* v, void* stream) {
+  if (!g || !v) {
+    phj_set_error("phj_sync_periodic: missing argument");
+    return PHJ_ERR_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int ax = 0; ax < g->dim; ++ax) {
+    if (!g->periodic[ax]) continue;
+    int64_t plane = 1;
+    for (int a = 0; a < g->dim; ++a)
+      if (a != ax) plane *= g->ext[a];
+    const int nb = grid_blocks(plane);
+    switch (elem_bytes) {
+      case 1: periodic_kernel<uint8_t><<<nb, 256, 0, s>>>(*g, (uint8_t*)v, ax); break;
+      case 2: periodic_kernel<int16_t><<<nb, 256, 0, s>>>(*g, (int16_t*)v, ax); break;
+      case 4: periodic_kernel<int32_t><<<nb, 256, 0, s>>>(*g, (int32_t*)v, ax); break;
+      case 8: periodic_kernel<int64_t><<<nb, 256, 0, s>>>(*g, (int64_t*)v, ax); break;
+      default: phj_set_error("phj_sync_periodic: elem_bytes"); return PHJ_ERR_ARG;
+    }
+  }
+  PHJ_CUDA(cudaGetLastError());
+  return PHJ_OK;
+}
+
+extern "C" int phj_error_partials(int64_t n, const double* a, const double* b, double half_a,
+                                  double half_b, double* out, void* stream) {
+  if (!a || !b || !out) {
+    phj_set_error("phj_error_partials: missing argument");
+    return PHJ_ERR_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  PHJ_CUDA(cudaMemsetAsync(out, 0, 3 * sizeof(double), s));
+  error_kernel<<<grid_blocks(n), 256, 0, s>>>(n, a, b, half_a, half_b, out);
+  PHJ_CUDA(cudaGetLastError());
+  return PHJ_OK;
+}
+
+extern "C" int phj_peak_flops(int32_t dtype, int32_t iters, double* sink, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  const int blocks = 8 * (phj_num_sms() > 0 ? phj_num_sms() : 148);
+  if (dtype == PHJ_F32) peak_kernel<float><<<blocks, 256, 0, s>>>(iters, (float*)sink);
+  else peak_kernel<double><<<blocks, 256, 0, s>>>(iters, sink);
+  PHJ_CUDA(cudaGetLastError());
+  return PHJ_OK;
+}

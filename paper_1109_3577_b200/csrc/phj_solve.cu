@@ -1,0 +1,1098 @@
+// phj_solve.cu -- the semi-Lagrangian value sweep, colour transport and
+// feedback extraction for sm_100a.
+//
+// Design:
+//  * Jacobi iteration with two ext buffers; the whole fixed-point loop runs
+//    inside ONE cooperative persistent launch (grid.sync between sweeps), so
+//    there is no host round trip per sweep (reference loop: solver.py:256-273).
+//  * Work is tiled; a tile is re-swept only if a tile in its 3^D neighbourhood
+//    changed in the previous sweep.  This is exact: a node whose stencil
+//    inputs did not change reproduces its previous value (monotone min).
+//  * Each warp owns 32*NB consecutive nodes of one row, so the stencil class
+//    (Dubins heading = internal axis 0) is warp-uniform; each thread keeps its
+//    NB nodes' 3^D neighbourhood in registers and the per-control corner
+//    weights come from shared memory as warp broadcasts.  Controls are grouped
+//    by foot octant on the host, which makes every register index compile-time.
+//  * State constraints (patch solves) are per-node 3^D "foreign" bitmasks; a
+//    warp with no foreign neighbour at all takes the rejection-free path.
+//  * Per-patch convergence: patch p stops at the first sweep whose max change
+//    over p is <= tol, exactly like one reference solve() per patch
+//    (patchy.py:362-377); later sweeps copy its nodes through unchanged.
+#include <cooperative_groups.h>
+#include <cstdio>
+
+#include "phj_common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace phj {
+
+struct SolveParams {
+  phj_grid g;
+  TileGrid tg;
+  int n_classes, nc;
+  const int32_t* oct_start;
+  const uint32_t* nzmask;
+  const double* weights;
+  const double* cost;
+  void* v[2];
+  const int16_t* lab;
+  const uint32_t* fmask;
+  const void* coef;
+  double coef0;
+  int R;
+  int max_sweeps;
+  const uint8_t* mine;
+  double tol;
+  Workspace ws;
+  unsigned long long* maxch;  // [max_sweeps * R], double bits
+  int32_t* patch_sweeps;
+  unsigned long long* evals;
+  int32_t* info;
+};
+
+template <int D, typename T>
+struct StencilSmem {
+  T* w;          // [nent][2^D]
+  T* a;          // [nent] beta (KRUZKOV) or cost (REF), COST_CTRL only
+  T* b;          // [nent] 1 - beta
+  uint32_t* nz;  // [nent]
+  int* oct;      // [ncls][2^D + 1]
+  static __host__ __device__ int64_t bytes(int ncls, int nc) {
+    int64_t nent = (int64_t)ncls * nc;
+    int64_t b = nent * (1 << D) * sizeof(T) + 2 * nent * sizeof(T);
+    b = (b + 15) / 16 * 16;
+    b += nent * 4 + (int64_t)ncls * ((1 << D) + 1) * 4;
+    return (b + 15) / 16 * 16;
+  }
+};
+
+template <int D, typename T>
+__device__ inline StencilSmem<D, T> carve_stencil(unsigned char* base, int ncls, int nc) {
+  StencilSmem<D, T> s;
+  int64_t nent = (int64_t)ncls * nc;
+  s.w = (T*)base;
+  s.a = s.w + nent * (1 << D);
+  s.b = s.a + nent;
+  unsigned char* p = (unsigned char*)(s.b + nent);
+  p = base + ((p - base + 15) / 16 * 16);
+  s.nz = (uint32_t*)p;
+  s.oct = (int*)(s.nz + nent);
+  return s;
+}
+
+template <int D, typename T, int RULE>
+__device__ inline void stage_stencil(const StencilSmem<D, T>& s, int ncls, int nc,
+                                     const int32_t* oct_start, const uint32_t* nzmask,
+                                     const double* weights, const double* cost) {
+  const int nent = ncls * nc;
+  for (int i = threadIdx.x; i < nent * (1 << D); i += blockDim.x) s.w[i] = (T)weights[i];
+  for (int i = threadIdx.x; i < nent; i += blockDim.x) {
+    s.nz[i] = nzmask[i];
+    double c = cost ? cost[i] : 0.0;
+    if (RULE == PHJ_RULE_KRUZKOV) {
+      double beta = exp(-c);
+      s.a[i] = (T)beta;
+      s.b[i] = (T)(1.0 - beta);
+    } else {
+      s.a[i] = (T)c;
+      s.b[i] = (T)0;
+    }
+  }
+  for (int i = threadIdx.x; i < ncls * ((1 << D) + 1); i += blockDim.x) s.oct[i] = oct_start[i];
+}
+
+// Neighbourhood register block: NR rows (3^(D-1)) x (NB + 2) columns.
+template <int D, typename T, int NB>
+struct Nbhd {
+  static constexpr int NR = (D == 2) ? 3 : 9;
+  T v[NR][NB + 2];
+};
+
+// value of corner k of octant o for node r (all compile-time after unrolling)
+template <int D, int NB, int O, int K, typename T>
+__device__ __forceinline__ T corner_val(const Nbhd<D, T, NB>& nb, int r) {
+  // internal axis ax: offset = (octant bit ? 0 : -1) + corner bit
+  constexpr int off0 = (((O >> 0) & 1) ? 0 : -1) + ((K >> 0) & 1);
+  constexpr int off1 = (((O >> 1) & 1) ? 0 : -1) + ((K >> 1) & 1);
+  if constexpr (D == 2) {
+    return nb.v[off0 + 1][r + off1 + 1];
+  } else {
+    constexpr int off2 = (((O >> 2) & 1) ? 0 : -1) + ((K >> 2) & 1);
+    return nb.v[(off0 + 1) * 3 + (off1 + 1)][r + off2 + 1];
+  }
+}
+
+template <int D, typename T, int NB, int O, int K>
+struct CornerSum {
+  __device__ __forceinline__ static T run(const Nbhd<D, T, NB>& nb, const T* w, int r, T acc) {
+    acc = fma(w[K], corner_val<D, NB, O, K>(nb, r), acc);
+    return CornerSum<D, T, NB, O, K + 1>::run(nb, w, r, acc);
+  }
+};
+template <int D, typename T, int NB, int O>
+struct CornerSum<D, T, NB, O, (1 << D)> {
+  __device__ __forceinline__ static T run(const Nbhd<D, T, NB>&, const T*, int, T acc) {
+    return acc;
+  }
+};
+
+template <typename T, int N>
+__device__ __forceinline__ void load_weights(const T* src, T* w) {
+  if constexpr (sizeof(T) == 8 && N % 2 == 0) {
+#pragma unroll
+    for (int i = 0; i < N / 2; ++i) {
+      double2 q = reinterpret_cast<const double2*>(src)[i];
+      w[2 * i] = q.x;
+      w[2 * i + 1] = q.y;
+    }
+  } else if constexpr (sizeof(T) == 4 && N % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < N / 4; ++i) {
+      float4 q = reinterpret_cast<const float4*>(src)[i];
+      w[4 * i] = q.x;
+      w[4 * i + 1] = q.y;
+      w[4 * i + 2] = q.z;
+      w[4 * i + 3] = q.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) w[i] = src[i];
+  }
+}
+
+// Evaluate all controls of octant O for the NB nodes of this thread.
+// MODE 0: min of the candidate values (sweep); MODE 1: argmin with lowest
+// original index on ties (feedback).
+template <int D, typename T, int NB, int RULE, int COST, bool SLOW, int MODE, int O>
+__device__ __forceinline__ void eval_octant(const Nbhd<D, T, NB>& nb, const StencilSmem<D, T>& s,
+                                            const int* os, const uint32_t (&fm)[NB],
+                                            const T (&ncoef)[NB], const int32_t* ctrl_map,
+                                            T (&best)[NB], int (&bidx)[NB]) {
+  constexpr int NC = 1 << D;
+  const int e0 = os[O], e1 = os[O + 1];
+  for (int e = e0; e < e1; ++e) {
+    T w[NC];
+    load_weights<T, NC>(s.w + (int64_t)e * NC, w);
+    T ca = T(0), cb = T(0);
+    if constexpr (COST == PHJ_COST_CTRL) {
+      ca = s.a[e];
+      cb = s.b[e];
+    }
+    uint32_t nz = 0;
+    if constexpr (SLOW) nz = s.nz[e];
+    int cidx = 0;
+    if constexpr (MODE == 1) cidx = ctrl_map[e];
+#pragma unroll
+    for (int r = 0; r < NB; ++r) {
+      T acc = w[0] * corner_val<D, NB, O, 0>(nb, r);
+      acc = CornerSum<D, T, NB, O, 1>::run(nb, w, r, acc);
+      if constexpr (COST == PHJ_COST_CTRL) {
+        acc = (RULE == PHJ_RULE_KRUZKOV) ? fma(ca, acc, cb) : acc + ca;
+      } else if constexpr (MODE == 1) {
+        // feedback applies the rule per candidate (Appendix A hoisting caveat)
+        acc = (RULE == PHJ_RULE_KRUZKOV) ? fma(ncoef[r], acc, T(1) - ncoef[r]) : acc + ncoef[r];
+      }
+      if constexpr (SLOW) {
+        if (fm[r] & nz) acc = big_value<T>();
+      }
+      if constexpr (MODE == 0) {
+        best[r] = acc < best[r] ? acc : best[r];
+      } else {
+        if (acc < best[r] || (acc == best[r] && cidx < bidx[r] && acc < big_value<T>())) {
+          best[r] = acc;
+          bidx[r] = cidx;
+        }
+      }
+    }
+  }
+}
+
+template <int D, typename T, int NB, int RULE, int COST, bool SLOW, int MODE, int O = 0>
+struct EvalAll {
+  __device__ __forceinline__ static void run(const Nbhd<D, T, NB>& nb, const StencilSmem<D, T>& s,
+                                             const int* os, const uint32_t (&fm)[NB],
+                                             const T (&ncoef)[NB], const int32_t* ctrl_map,
+                                             T (&best)[NB], int (&bidx)[NB]) {
+    eval_octant<D, T, NB, RULE, COST, SLOW, MODE, O>(nb, s, os, fm, ncoef, ctrl_map, best, bidx);
+    EvalAll<D, T, NB, RULE, COST, SLOW, MODE, O + 1>::run(nb, s, os, fm, ncoef, ctrl_map, best,
+                                                         bidx);
+  }
+};
+template <int D, typename T, int NB, int RULE, int COST, bool SLOW, int MODE>
+struct EvalAll<D, T, NB, RULE, COST, SLOW, MODE, (1 << D)> {
+  __device__ __forceinline__ static void run(const Nbhd<D, T, NB>&, const StencilSmem<D, T>&,
+                                             const int*, const uint32_t (&)[NB], const T (&)[NB],
+                                             const int32_t*, T (&)[NB], int (&)[NB]) {}
+};
+
+// Thread -> row mapping inside a tile.  Returns false if the row is outside
+// the grid.  c[] receives the interior index of the thread's first node.
+template <int D>
+__device__ inline bool thread_row(const phj_grid& g, const int o[3], int c[3]) {
+  using TL = Tile<D>;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if constexpr (D == 2) {
+    c[0] = o[0] + warp;
+    c[1] = o[1] + lane * TL::NB;
+    c[2] = 0;
+    return c[0] < g.shape[0] && c[1] < g.shape[1];
+  } else {
+    c[0] = o[0] + warp / TL::TY;
+    c[1] = o[1] + warp % TL::TY;
+    c[2] = o[2] + lane * TL::NB;
+    return c[0] < g.shape[0] && c[1] < g.shape[1] && c[2] < g.shape[2];
+  }
+}
+
+template <int D>
+__device__ inline int64_t ext_flat(const phj_grid& g, const int c[3]) {
+  if constexpr (D == 2) return (int64_t)(c[0] + 1) * g.strides[0] + (c[1] + 1);
+  else return (int64_t)(c[0] + 1) * g.strides[0] + (int64_t)(c[1] + 1) * g.strides[1] + (c[2] + 1);
+}
+
+template <int D>
+__device__ inline int64_t serial_of(const phj_grid& g, const int c[3]) {
+  if constexpr (D == 2) return (int64_t)c[0] * g.shape[1] + c[1];
+  else return ((int64_t)c[0] * g.shape[1] + c[1]) * g.shape[2] + c[2];
+}
+
+// Load the 3^D neighbourhood (clamped to the ext array) of NB nodes.
+template <int D, typename T, int NB>
+__device__ __forceinline__ void load_nbhd(const phj_grid& g, const T* __restrict__ v, const int c[3],
+                                          Nbhd<D, T, NB>& nb) {
+  constexpr int last = D - 1;
+  const int64_t xmax = g.ext[last] - 1;
+  const int64_t x0 = c[last];  // ext index of the column left of node 0 = c + 1 - 1
+  if constexpr (D == 2) {
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy) {
+      int64_t row = (int64_t)min((int64_t)(c[0] + dy), (int64_t)(g.ext[0] - 1)) * g.strides[0];
+#pragma unroll
+      for (int dx = 0; dx < NB + 2; ++dx) nb.v[dy][dx] = v[row + min(x0 + dx, xmax)];
+    }
+  } else {
+#pragma unroll
+    for (int dz = 0; dz < 3; ++dz) {
+#pragma unroll
+      for (int dy = 0; dy < 3; ++dy) {
+        int64_t row = (int64_t)min((int64_t)(c[0] + dz), (int64_t)(g.ext[0] - 1)) * g.strides[0] +
+                      (int64_t)min((int64_t)(c[1] + dy), (int64_t)(g.ext[1] - 1)) * g.strides[1];
+#pragma unroll
+        for (int dx = 0; dx < NB + 2; ++dx) nb.v[dz * 3 + dy][dx] = v[row + min(x0 + dx, xmax)];
+      }
+    }
+  }
+}
+
+template <typename T>
+__device__ inline void atomic_max_change(unsigned long long* addr, T ch) {
+  atomicMax(addr, dbits((double)ch));
+}
+
+// One tile of the value sweep.  Returns true if any node changed.
+template <int D, typename T, int RULE, int COST>
+__device__ bool sweep_tile(const SolveParams& p, const StencilSmem<D, T>& s, int tile,
+                           const T* __restrict__ vin, T* __restrict__ vout, const int* s_done,
+                           unsigned long long* s_max, unsigned long long* gmax_row,
+                           unsigned long long& evals) {
+  using TL = Tile<D>;
+  constexpr int NB = TL::NB;
+  constexpr int last = D - 1;
+  const phj_grid& g = p.g;
+  int o[3], c[3];
+  tile_origin<D>(p.tg, tile, o);
+  if (!thread_row<D>(g, o, c)) return false;  // whole row outside (warp-uniform)
+  const int64_t f0 = ext_flat<D>(g, c);
+  const int cls = p.n_classes > 1 ? c[0] : 0;
+  const int* os = s.oct + cls * ((1 << D) + 1);
+  const int nadm = os[1 << D] - os[0];
+
+  // per-node classification
+  int labv[NB];
+  bool comp[NB], copy[NB];
+  uint32_t fm[NB];
+  T ncoef[NB];
+  bool any_comp = false;
+#pragma unroll
+  for (int r = 0; r < NB; ++r) {
+    const bool in = c[last] + r < g.shape[last];
+    labv[r] = in ? (int)p.lab[f0 + r] : -1;
+    comp[r] = false;
+    copy[r] = false;
+    fm[r] = 0;
+    ncoef[r] = (T)p.coef0;
+    if (labv[r] >= 0) {
+      if (s_done[labv[r]] != 0x7fffffff) {
+        copy[r] = true;
+      } else {
+        if (COST == PHJ_COST_NODE && p.coef) ncoef[r] = ((const T*)p.coef)[f0 + r];
+        if (ncoef[r] < T(0) && COST == PHJ_COST_NODE) {
+          copy[r] = true;
+        } else {
+          comp[r] = true;
+          fm[r] = p.fmask[f0 + r];
+          any_comp = true;
+        }
+      }
+    }
+  }
+  const unsigned FULL = 0xffffffffu;
+  const bool warp_comp = __any_sync(FULL, any_comp);
+  bool changed = false;
+  T mych[NB];
+#pragma unroll
+  for (int r = 0; r < NB; ++r) mych[r] = T(0);
+
+  const int64_t M0 = g.shape[0];
+  const bool per0 = g.periodic[0] != 0;
+  const int64_t ghost_shift = M0 * g.strides[0];
+
+  if (warp_comp) {
+    Nbhd<D, T, NB> nb;
+    load_nbhd<D, T, NB>(g, vin, c, nb);
+    T best[NB];
+    int bidx[NB];
+#pragma unroll
+    for (int r = 0; r < NB; ++r) {
+      best[r] = big_value<T>();
+      bidx[r] = 0;
+    }
+    uint32_t fmo = 0;
+#pragma unroll
+    for (int r = 0; r < NB; ++r) fmo |= fm[r];
+    if (__any_sync(FULL, fmo != 0))
+      EvalAll<D, T, NB, RULE, COST, true, 0>::run(nb, s, os, fm, ncoef, nullptr, best, bidx);
+    else
+      EvalAll<D, T, NB, RULE, COST, false, 0>::run(nb, s, os, fm, ncoef, nullptr, best, bidx);
+    constexpr int CR = (D == 2) ? 1 : 4;  // centre row of the register block
+#pragma unroll
+    for (int r = 0; r < NB; ++r) {
+      if (!(comp[r] || copy[r])) continue;
+      const T old = nb.v[CR][r + 1];
+      T nv = old;
+      if (comp[r]) {
+        evals += (unsigned long long)nadm;
+        T cand = best[r];
+        if constexpr (COST == PHJ_COST_NODE) {
+          cand = (RULE == PHJ_RULE_KRUZKOV) ? fma(ncoef[r], best[r], T(1) - ncoef[r])
+                                            : best[r] + ncoef[r];
+        }
+        if (cand < old) {
+          nv = cand;
+          mych[r] = old - cand;
+          changed = true;
+        }
+      }
+      vout[f0 + r] = nv;
+      if (per0) {
+        if (c[0] == 0) vout[f0 + r + ghost_shift] = nv;
+        else if (c[0] == M0 - 1) vout[f0 + r - ghost_shift] = nv;
+      }
+    }
+  } else {
+    // copy-through only (done patches / degenerate nodes)
+#pragma unroll
+    for (int r = 0; r < NB; ++r) {
+      if (!copy[r]) continue;
+      const T old = vin[f0 + r];
+      vout[f0 + r] = old;
+      if (per0) {
+        if (c[0] == 0) vout[f0 + r + ghost_shift] = old;
+        else if (c[0] == M0 - 1) vout[f0 + r - ghost_shift] = old;
+      }
+    }
+  }
+
+  // per-patch max change
+  if (__any_sync(FULL, changed)) {
+    const int lane = threadIdx.x & 31;
+    int l0 = __shfl_sync(FULL, labv[0], 0);
+    bool uni = true;
+#pragma unroll
+    for (int r = 0; r < NB; ++r) uni &= (mych[r] == T(0)) || (labv[r] == l0);
+    if (__all_sync(FULL, uni)) {
+      T m = T(0);
+#pragma unroll
+      for (int r = 0; r < NB; ++r) m = max(m, mych[r]);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) m = max(m, __shfl_xor_sync(FULL, m, off));
+      if (lane == 0 && m > T(0)) {
+        if (p.R <= kSmemPatchReduce) atomic_max_change(&s_max[l0], m);
+        else atomic_max_change(&gmax_row[l0], m);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < NB; ++r) {
+        if (mych[r] > T(0)) {
+          if (p.R <= kSmemPatchReduce) atomic_max_change(&s_max[labv[r]], mych[r]);
+          else atomic_max_change(&gmax_row[labv[r]], mych[r]);
+        }
+      }
+    }
+  }
+  return changed;
+}
+
+template <int D, typename T, int RULE, int COST>
+__global__ void __launch_bounds__(kThreads, 1) solve_kernel(const __grid_constant__ SolveParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  cg::grid_group grid = cg::this_grid();
+  StencilSmem<D, T> s = carve_stencil<D, T>(smem, p.n_classes, p.nc);
+  int* s_done = (int*)(smem + StencilSmem<D, T>::bytes(p.n_classes, p.nc));
+  unsigned long long* s_max = (unsigned long long*)(s_done + ((p.R + 1) / 2 * 2));
+  stage_stencil<D, T, RULE>(s, p.n_classes, p.nc, p.oct_start, p.nzmask, p.weights, p.cost);
+  for (int i = threadIdx.x; i < p.R; i += blockDim.x)
+    s_done[i] = (p.mine == nullptr || p.mine[i]) ? 0x7fffffff : 0;
+  __syncthreads();
+
+  unsigned long long evals = 0;
+  int tiles = 0;
+  int sw = 0, buf = 0;
+  const int nshared = min(p.R, kSmemPatchReduce);
+  for (;;) {
+    const T* vin = (const T*)p.v[buf];
+    T* vout = (T*)p.v[buf ^ 1];
+    const int cnt = ld_cg(&p.ws.counts[sw]);
+    const int* list = p.ws.list[sw & 1];
+    int* cur_flags = p.ws.flags[sw & 1];
+    int* nxt_flags = p.ws.flags[(sw + 1) & 1];
+    int* nxt_list = p.ws.list[(sw + 1) & 1];
+    int* nxt_cnt = &p.ws.counts[sw + 1];
+    unsigned long long* gmax_row = p.maxch + (int64_t)sw * p.R;
+    for (int i = threadIdx.x; i < nshared; i += blockDim.x) s_max[i] = 0ull;
+    __syncthreads();
+    for (int li = blockIdx.x; li < cnt; li += gridDim.x) {
+      const int t = __ldcg(&list[li]);
+      if (threadIdx.x == 0) cur_flags[t] = 0;
+      bool ch = sweep_tile<D, T, RULE, COST>(p, s, t, vin, vout, s_done, s_max, gmax_row, evals);
+      const int any = __syncthreads_or(ch);
+      ++tiles;
+      if (any && threadIdx.x < (D == 2 ? 9 : 27))
+        mark_neighbour<D>(p.tg, p.g, t, threadIdx.x, nxt_flags, nxt_list, nxt_cnt);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nshared; i += blockDim.x)
+      if (s_max[i]) atomicMax(&gmax_row[i], s_max[i]);
+    grid.sync();
+    ++sw;
+    buf ^= 1;
+    int pending = 0;
+    for (int i = threadIdx.x; i < p.R; i += blockDim.x) {
+      if (s_done[i] == 0x7fffffff) {
+        const double mc = __longlong_as_double((long long)ld_cg(&gmax_row[i]));
+        if (mc <= p.tol) s_done[i] = sw;
+        else pending = 1;
+      }
+    }
+    const int any_pending = __syncthreads_or(pending);
+    if (!any_pending || sw >= p.max_sweeps) break;
+  }
+  // results
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i < p.R; i += blockDim.x) {
+      const int d = s_done[i];
+      p.patch_sweeps[i] = (d == 0x7fffffff) ? -sw : d;
+    }
+    if (threadIdx.x == 0) {
+      p.info[0] = sw;
+      p.info[1] = buf;
+    }
+  }
+  // block-reduce evals / tiles
+  __shared__ unsigned long long s_ev;
+  __shared__ int s_tiles;
+  if (threadIdx.x == 0) {
+    s_ev = 0;
+    s_tiles = 0;
+  }
+  __syncthreads();
+  atomicAdd(&s_ev, evals);
+  if (threadIdx.x == 0) s_tiles = tiles;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicAdd(p.evals, s_ev);
+    atomicAdd(&p.info[2], s_tiles);
+  }
+}
+
+// Initial active tile list: every tile holding a node of a patch to sweep.
+template <int D>
+__global__ void build_list_kernel(phj_grid g, TileGrid tg, const int16_t* __restrict__ lab,
+                                  const uint8_t* __restrict__ mine, int* flags, int* list,
+                                  int* count, int want_movers, const int32_t* __restrict__ fb,
+                                  const int8_t* __restrict__ kind) {
+  using TL = Tile<D>;
+  const int t = blockIdx.x;
+  int o[3], c[3];
+  tile_origin<D>(tg, t, o);
+  bool any = false;
+  if (thread_row<D>(g, o, c)) {
+    const int64_t f0 = ext_flat<D>(g, c);
+    const int64_t s0 = serial_of<D>(g, c);
+    for (int r = 0; r < TL::NB; ++r) {
+      if (c[D - 1] + r >= g.shape[D - 1]) break;
+      if (want_movers) {
+        any |= fb[s0 + r] >= 0 && kind[s0 + r] == 0;
+      } else {
+        const int l = lab[f0 + r];
+        any |= l >= 0 && (mine == nullptr || mine[l]);
+      }
+    }
+  }
+  if (__syncthreads_or(any) && threadIdx.x == 0) {
+    flags[t] = 1;
+    list[atomicAdd(count, 1)] = t;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// colour transport (patchy.py:183-219): phi_i <- I[phi](x_i + h f(x_i, a*_i))
+
+struct TransportParams {
+  phj_grid g;
+  TileGrid tg;
+  int n_classes, nc;
+  const int32_t* oct_start;
+  const int32_t* ctrl;
+  const double* weights;
+  double* phi[2];
+  const int32_t* fb;
+  const int8_t* kind;
+  double tol;
+  int max_sweeps;
+  Workspace ws;
+  unsigned long long* maxch;  // [max_sweeps]
+  int32_t* info;
+  unsigned long long* updates;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1) transport_kernel(const __grid_constant__ TransportParams p) {
+  using TL = Tile<D>;
+  constexpr int NC = 1 << D;
+  constexpr int NB = TL::NB;
+  constexpr int last = D - 1;
+  extern __shared__ __align__(16) unsigned char smem[];
+  cg::grid_group grid = cg::this_grid();
+  const int nent = p.n_classes * p.nc;
+  double* s_w = (double*)smem;                  // [nent][NC]
+  int* s_inv = (int*)(s_w + (int64_t)nent * NC);  // [ncls][nc] ctrl -> entry
+  signed char* s_oct = (signed char*)(s_inv + nent);  // [nent]
+  for (int i = threadIdx.x; i < nent * NC; i += blockDim.x) s_w[i] = p.weights[i];
+  for (int i = threadIdx.x; i < nent; i += blockDim.x) s_inv[i] = -1;
+  __syncthreads();
+  for (int cls = 0; cls < p.n_classes; ++cls) {
+    const int32_t* os = p.oct_start + cls * (NC + 1);
+    for (int e = os[0] + threadIdx.x; e < os[NC]; e += blockDim.x) {
+      int oc = 0;
+      while (oc < NC - 1 && e >= os[oc + 1]) ++oc;
+      s_oct[e] = (signed char)oc;
+      s_inv[cls * p.nc + p.ctrl[e]] = e;
+    }
+  }
+  __syncthreads();
+  const phj_grid& g = p.g;
+  const int64_t M0 = g.shape[0];
+  const bool per0 = g.periodic[0] != 0;
+  const int64_t ghost_shift = M0 * g.strides[0];
+  __shared__ unsigned long long s_mx;
+  unsigned long long upd = 0;
+  int sw = 0, buf = 0;
+  for (;;) {
+    const double* pin = p.phi[buf];
+    double* pout = p.phi[buf ^ 1];
+    const int cnt = ld_cg(&p.ws.counts[sw]);
+    const int* list = p.ws.list[sw & 1];
+    int* cur_flags = p.ws.flags[sw & 1];
+    if (threadIdx.x == 0) s_mx = 0ull;
+    __syncthreads();
+    for (int li = blockIdx.x; li < cnt; li += gridDim.x) {
+      const int t = __ldcg(&list[li]);
+      if (threadIdx.x == 0) cur_flags[t] = 0;
+      int o[3], c[3];
+      tile_origin<D>(p.tg, t, o);
+      bool changed = false;
+      double m = 0.0;
+      if (thread_row<D>(g, o, c)) {
+        const int64_t f0 = ext_flat<D>(g, c);
+        const int64_t s0 = serial_of<D>(g, c);
+        const int cls = p.n_classes > 1 ? c[0] : 0;
+        for (int r = 0; r < NB; ++r) {
+          if (c[last] + r >= g.shape[last]) break;
+          const int a = p.fb[s0 + r];
+          if (a < 0 || p.kind[s0 + r] != 0) continue;
+          const int e = s_inv[cls * p.nc + a];
+          if (e < 0) continue;
+          const int oc = s_oct[e];
+          const int64_t f = f0 + r;
+          double v = 0.0;
+#pragma unroll
+          for (int k = 0; k < NC; ++k) {
+            const double w = s_w[(int64_t)e * NC + k];
+            if (w != 0.0) {
+              int64_t off = 0;
+#pragma unroll
+              for (int ax = 0; ax < D; ++ax) {
+                const int oa = (((oc >> ax) & 1) ? 0 : -1) + ((k >> ax) & 1);
+                off += (int64_t)oa * g.strides[ax];
+              }
+              v = fma(w, pin[f + off], v);
+            }
+          }
+          const double ch = fabs(pin[f] - v);
+          pout[f] = v;
+          if (per0) {
+            if (c[0] == 0) pout[f + ghost_shift] = v;
+            else if (c[0] == M0 - 1) pout[f - ghost_shift] = v;
+          }
+          ++upd;
+          if (ch > 0.0) {
+            changed = true;
+            m = fmax(m, ch);
+          }
+        }
+      }
+      if (m > 0.0) atomicMax(&s_mx, dbits(m));
+      const int any = __syncthreads_or(changed);
+      if (any && threadIdx.x < (D == 2 ? 9 : 27))
+        mark_neighbour<D>(p.tg, g, t, threadIdx.x, p.ws.flags[(sw + 1) & 1],
+                          p.ws.list[(sw + 1) & 1], &p.ws.counts[sw + 1]);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && s_mx) atomicMax(&p.maxch[sw], s_mx);
+    grid.sync();
+    const double mc = __longlong_as_double((long long)ld_cg(&p.maxch[sw]));
+    ++sw;
+    buf ^= 1;
+    if (mc <= p.tol) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) p.info[2] = 1;
+      break;
+    }
+    if (sw >= p.max_sweeps) break;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    p.info[0] = sw;
+    p.info[1] = buf;
+  }
+  __shared__ unsigned long long s_up;
+  if (threadIdx.x == 0) s_up = 0;
+  __syncthreads();
+  atomicAdd(&s_up, upd);
+  __syncthreads();
+  if (threadIdx.x == 0) atomicAdd(p.updates, s_up);
+}
+
+// ---------------------------------------------------------------------------
+// feedback (extract_feedback, solver.py:413-443; feedback_batch _kernels.py:109-167)
+
+struct FeedbackParams {
+  phj_grid g;
+  TileGrid tg;
+  int n_classes, nc;
+  const int32_t* oct_start;
+  const int32_t* ctrl;
+  const uint32_t* nzmask;
+  const double* weights;
+  const double* cost;
+  const void* v;
+  const int8_t* kind;
+  const uint32_t* fmask;
+  const void* coef;
+  double coef0;
+  double unreach;
+  int32_t* out;
+  unsigned long long* evals;
+};
+
+template <int D, typename T, int RULE, int COST>
+__global__ void __launch_bounds__(kThreads) feedback_kernel(const __grid_constant__ FeedbackParams p) {
+  using TL = Tile<D>;
+  constexpr int NB = TL::NB;
+  constexpr int last = D - 1;
+  extern __shared__ __align__(16) unsigned char smem[];
+  StencilSmem<D, T> s = carve_stencil<D, T>(smem, p.n_classes, p.nc);
+  int* s_ctrl = (int*)(smem + StencilSmem<D, T>::bytes(p.n_classes, p.nc));
+  stage_stencil<D, T, RULE>(s, p.n_classes, p.nc, p.oct_start, p.nzmask, p.weights, p.cost);
+  for (int i = threadIdx.x; i < p.n_classes * p.nc; i += blockDim.x) s_ctrl[i] = p.ctrl[i];
+  __syncthreads();
+  const phj_grid& g = p.g;
+  unsigned long long ev = 0;
+  for (int t = blockIdx.x; t < p.tg.total; t += gridDim.x) {
+    int o[3], c[3];
+    tile_origin<D>(p.tg, t, o);
+    if (!thread_row<D>(g, o, c)) continue;
+    const int64_t f0 = ext_flat<D>(g, c);
+    const int64_t s0 = serial_of<D>(g, c);
+    const int cls = p.n_classes > 1 ? c[0] : 0;
+    const int* os = s.oct + cls * ((1 << D) + 1);
+    const int nadm = os[1 << D] - os[0];
+    bool comp[NB];
+    uint32_t fm[NB];
+    T ncoef[NB];
+    bool any = false;
+    const T* v = (const T*)p.v;
+#pragma unroll
+    for (int r = 0; r < NB; ++r) {
+      const bool in = c[last] + r < g.shape[last];
+      comp[r] = false;
+      fm[r] = 0;
+      ncoef[r] = (T)p.coef0;
+      if (in) {
+        p.out[s0 + r] = -1;
+        if (COST == PHJ_COST_NODE && p.coef) ncoef[r] = ((const T*)p.coef)[f0 + r];
+        const bool adm = !(COST == PHJ_COST_NODE && ncoef[r] < T(0));
+        if (p.kind[s0 + r] == 0 && (double)v[f0 + r] < p.unreach && adm) {
+          comp[r] = true;
+          fm[r] = p.fmask[f0 + r];
+          any = true;
+        }
+      }
+    }
+    if (!__any_sync(0xffffffffu, any)) continue;
+    Nbhd<D, T, NB> nb;
+    load_nbhd<D, T, NB>(g, v, c, nb);
+    T best[NB];
+    int bidx[NB];
+#pragma unroll
+    for (int r = 0; r < NB; ++r) {
+      best[r] = big_value<T>();
+      bidx[r] = 0x7fffffff;
+    }
+    EvalAll<D, T, NB, RULE, COST, true, 1>::run(nb, s, os, fm, ncoef, s_ctrl, best, bidx);
+#pragma unroll
+    for (int r = 0; r < NB; ++r) {
+      if (!comp[r]) continue;
+      ev += nadm;
+      p.out[s0 + r] = (best[r] < big_value<T>()) ? bidx[r] : -1;
+    }
+  }
+  __shared__ unsigned long long s_ev;
+  if (threadIdx.x == 0) s_ev = 0;
+  __syncthreads();
+  atomicAdd(&s_ev, ev);
+  __syncthreads();
+  if (threadIdx.x == 0 && p.evals) atomicAdd(p.evals, s_ev);
+}
+
+// ---------------------------------------------------------------------------
+// foreign masks
+
+template <int D>
+__global__ void fmask_kernel(phj_grid g, const int16_t* __restrict__ lab,
+                             const uint8_t* __restrict__ hard, uint32_t* __restrict__ fmask) {
+  const int64_t N = g.shape[0] * g.shape[1] * (D == 3 ? g.shape[2] : 1);
+  for (int64_t sidx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sidx < N;
+       sidx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t rem = sidx;
+    int c[3] = {0, 0, 0};
+    for (int ax = D - 1; ax >= 0; --ax) {
+      c[ax] = (int)(rem % g.shape[ax]);
+      rem /= g.shape[ax];
+    }
+    const int64_t f = ext_flat<D>(g, c);
+    uint32_t m = 0;
+    const int own = lab ? lab[f] : 0;
+    if (!lab || own >= 0) {
+      constexpr int NP = (D == 2) ? 9 : 27;
+      for (int q = 0; q < NP; ++q) {
+        int64_t off = 0;
+        if (D == 2) {
+          off = (int64_t)(q / 3 - 1) * g.strides[0] + (q % 3 - 1);
+        } else {
+          off = (int64_t)(q / 9 - 1) * g.strides[0] + (int64_t)((q / 3) % 3 - 1) * g.strides[1] +
+                (q % 3 - 1);
+        }
+        bool foreign;
+        if (lab) {
+          const int l = lab[f + off];
+          foreign = !(l == own || l == PHJ_LAB_TARGET || l == PHJ_LAB_FIXED);
+        } else {
+          foreign = hard[f + off] != 0;
+        }
+        if (foreign) m |= (1u << q);
+      }
+    }
+    fmask[f] = m;
+  }
+}
+
+}  // namespace phj
+
+using namespace phj;
+
+// ---------------------------------------------------------------------------
+// host side
+
+static int g_num_sms = 0;
+
+extern "C" int phj_num_sms(void) {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return g_num_sms;
+}
+
+extern "C" int64_t phj_solve_workspace_bytes(const phj_grid* g, int32_t n_patches,
+                                             int32_t max_sweeps) {
+  (void)n_patches;
+  if (!g) return -1;
+  const int64_t b =
+      g->dim == 2 ? workspace_bytes<2>(*g, max_sweeps) : workspace_bytes<3>(*g, max_sweeps);
+  return align_up(b, 256) + 8 * (int64_t)max_sweeps;  // + transport change history
+}
+
+template <typename K>
+static int coop_launch(K kernel, int want_blocks, size_t smem, void** args, cudaStream_t stream,
+                       int* launched) {
+  PHJ_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  PHJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem));
+  if (occ < 1) {
+    phj_set_error("kernel cannot be resident (smem %zu B)", smem);
+    return PHJ_ERR_UNSUPPORTED;
+  }
+  int blocks = std::min(want_blocks, occ * phj_num_sms());
+  if (blocks < 1) blocks = 1;
+  if (launched) *launched = blocks;
+  PHJ_CUDA(cudaLaunchCooperativeKernel((void*)kernel, dim3(blocks), dim3(kThreads), args, smem,
+                                       stream));
+  return PHJ_OK;
+}
+
+template <int D, typename T, int RULE, int COST>
+static int solve_impl(const phj_solve_args* a) {
+  cudaStream_t stream = (cudaStream_t)a->stream;
+  SolveParams p;
+  p.g = a->grid;
+  p.tg = make_tile_grid<D>(a->grid);
+  p.n_classes = a->st.n_classes;
+  p.nc = a->st.n_controls;
+  p.oct_start = a->st.oct_start;
+  p.nzmask = a->st.nzmask;
+  p.weights = a->st.weights;
+  p.cost = a->st.cost;
+  p.v[0] = a->v0;
+  p.v[1] = a->v1;
+  p.lab = a->lab;
+  p.fmask = a->fmask;
+  p.coef = a->coef;
+  p.coef0 = a->coef0;
+  p.R = a->n_patches;
+  p.max_sweeps = a->max_sweeps;
+  p.mine = a->mine;
+  p.tol = a->tol;
+  p.ws = carve<D>(a->grid, a->workspace);
+  p.maxch = (unsigned long long*)a->maxch_hist;
+  p.patch_sweeps = a->patch_sweeps;
+  p.evals = a->evals;
+  p.info = a->info;
+  const int64_t ws_bytes = workspace_bytes<D>(a->grid, a->max_sweeps);
+  PHJ_CUDA(cudaMemsetAsync(a->workspace, 0, ws_bytes, stream));
+  PHJ_CUDA(cudaMemsetAsync(a->maxch_hist, 0, sizeof(double) * (size_t)a->max_sweeps * a->n_patches,
+                           stream));
+  PHJ_CUDA(cudaMemsetAsync(a->evals, 0, sizeof(unsigned long long), stream));
+  PHJ_CUDA(cudaMemsetAsync(a->info, 0, 4 * sizeof(int32_t), stream));
+  build_list_kernel<D><<<p.tg.total, kThreads, 0, stream>>>(
+      p.g, p.tg, p.lab, p.mine, p.ws.flags[0], p.ws.list[0], p.ws.counts, 0, nullptr, nullptr);
+  PHJ_CUDA(cudaGetLastError());
+  size_t smem = (size_t)StencilSmem<D, T>::bytes(p.n_classes, p.nc) +
+                (size_t)((p.R + 1) / 2 * 2) * 4 + (size_t)std::min(p.R, kSmemPatchReduce) * 8 + 16;
+  void* args[] = {(void*)&p};
+  int launched = 0;
+  int rc = coop_launch(solve_kernel<D, T, RULE, COST>, p.tg.total, smem, args, stream, &launched);
+  if (rc) return rc;
+  PHJ_CUDA(cudaGetLastError());
+  return PHJ_OK;
+}
+
+extern "C" int phj_solve(const phj_solve_args* a) {
+  if (!a || (a->grid.dim != 2 && a->grid.dim != 3) || !a->v0 || !a->v1 || !a->lab || !a->fmask ||
+      !a->workspace || !a->maxch_hist || !a->patch_sweeps || !a->evals || !a->info) {
+    phj_set_error("phj_solve: missing argument");
+    return PHJ_ERR_ARG;
+  }
+  if (a->n_patches < 1 || a->n_patches > kMaxPatches || a->max_sweeps < 1) {
+    phj_set_error("phj_solve: n_patches must be in [1, %d], max_sweeps >= 1", kMaxPatches);
+    return PHJ_ERR_ARG;
+  }
+  if (a->grid.periodic[1] || a->grid.periodic[2]) {
+    phj_set_error("phj_solve: only internal axis 0 may be periodic");
+    return PHJ_ERR_UNSUPPORTED;
+  }
+  if (a->rule == PHJ_RULE_REF && a->dtype == PHJ_F32) {
+    phj_set_error("phj_solve: the reference (sentinel) rule is fp64 only");
+    return PHJ_ERR_UNSUPPORTED;
+  }
+  const int D = a->grid.dim, f32 = a->dtype == PHJ_F32, krz = a->rule == PHJ_RULE_KRUZKOV,
+            cc = a->st.cost_mode == PHJ_COST_CTRL;
+#define PHJ_DISPATCH(DD, TT, RR, CC)                                                        \
+  if (D == DD && f32 == (sizeof(TT) == 4) && krz == (RR == PHJ_RULE_KRUZKOV) &&           \
+      cc == (CC == PHJ_COST_CTRL))                                                         \
+    return solve_impl<DD, TT, RR, CC>(a);
+  PHJ_DISPATCH(2, double, PHJ_RULE_REF, PHJ_COST_NODE)
+  PHJ_DISPATCH(2, double, PHJ_RULE_REF, PHJ_COST_CTRL)
+  PHJ_DISPATCH(2, double, PHJ_RULE_KRUZKOV, PHJ_COST_NODE)
+  PHJ_DISPATCH(2, double, PHJ_RULE_KRUZKOV, PHJ_COST_CTRL)
+  PHJ_DISPATCH(2, float, PHJ_RULE_KRUZKOV, PHJ_COST_NODE)
+  PHJ_DISPATCH(2, float, PHJ_RULE_KRUZKOV, PHJ_COST_CTRL)
+  PHJ_DISPATCH(3, double, PHJ_RULE_REF, PHJ_COST_NODE)
+  PHJ_DISPATCH(3, double, PHJ_RULE_REF, PHJ_COST_CTRL)
+  PHJ_DISPATCH(3, double, PHJ_RULE_KRUZKOV, PHJ_COST_NODE)
+  PHJ_DISPATCH(3, double, PHJ_RULE_KRUZKOV, PHJ_COST_CTRL)
+  PHJ_DISPATCH(3, float, PHJ_RULE_KRUZKOV, PHJ_COST_NODE)
+  PHJ_DISPATCH(3, float, PHJ_RULE_KRUZKOV, PHJ_COST_CTRL)
+#undef PHJ_DISPATCH
+  phj_set_error("phj_solve: unsupported combination");
+  return PHJ_ERR_UNSUPPORTED;
+}
+
+template <int D>
+static int transport_impl(const phj_transport_args* a) {
+  cudaStream_t stream = (cudaStream_t)a->stream;
+  TransportParams p;
+  p.g = a->grid;
+  p.tg = make_tile_grid<D>(a->grid);
+  p.n_classes = a->st.n_classes;
+  p.nc = a->st.n_controls;
+  p.oct_start = a->st.oct_start;
+  p.ctrl = a->st.ctrl;
+  p.weights = a->st.weights;
+  p.phi[0] = a->phi0;
+  p.phi[1] = a->phi1;
+  p.fb = a->fb;
+  p.kind = a->kind;
+  p.tol = a->tol;
+  p.max_sweeps = a->max_sweeps;
+  p.ws = carve<D>(a->grid, a->workspace);
+  const int64_t ws_bytes = workspace_bytes<D>(a->grid, a->max_sweeps);
+  // maxch history lives after the workspace proper
+  p.maxch = (unsigned long long*)((char*)a->workspace + align_up(ws_bytes, 256));
+  p.info = a->info;
+  p.updates = a->updates;
+  PHJ_CUDA(cudaMemsetAsync(a->workspace, 0, align_up(ws_bytes, 256) + 8 * (size_t)a->max_sweeps,
+                           stream));
+  PHJ_CUDA(cudaMemsetAsync(a->info, 0, 4 * sizeof(int32_t), stream));
+  PHJ_CUDA(cudaMemsetAsync(a->updates, 0, sizeof(unsigned long long), stream));
+  build_list_kernel<D><<<p.tg.total, kThreads, 0, stream>>>(
+      p.g, p.tg, nullptr, nullptr, p.ws.flags[0], p.ws.list[0], p.ws.counts, 1, p.fb, p.kind);
+  PHJ_CUDA(cudaGetLastError());
+  const int nent = p.n_classes * p.nc;
+  size_t smem = (size_t)nent * (1 << D) * 8 + (size_t)nent * 4 + (size_t)nent + 16;
+  void* args[] = {(void*)&p};
+  return coop_launch(transport_kernel<D>, p.tg.total, smem, args, stream, nullptr);
+}
+
+extern "C" int phj_transport(const phj_transport_args* a) {
+  if (!a || !a->phi0 || !a->phi1 || !a->fb || !a->kind || !a->workspace || !a->info ||
+      !a->updates || a->max_sweeps < 1) {
+    phj_set_error("phj_transport: missing argument");
+    return PHJ_ERR_ARG;
+  }
+  if (a->grid.periodic[1] || a->grid.periodic[2]) {
+    phj_set_error("phj_transport: only internal axis 0 may be periodic");
+    return PHJ_ERR_UNSUPPORTED;
+  }
+  return a->grid.dim == 2 ? transport_impl<2>(a) : transport_impl<3>(a);
+}
+
+template <int D, typename T, int RULE, int COST>
+static int feedback_impl(const phj_grid* g, const phj_stencil* st, const void* v,
+                         const int8_t* kind, const uint32_t* fmask, const void* coef,
+                         double coef0, double unreach, int32_t* out, unsigned long long* evals,
+                         cudaStream_t stream) {
+  FeedbackParams p;
+  p.g = *g;
+  p.tg = make_tile_grid<D>(*g);
+  p.n_classes = st->n_classes;
+  p.nc = st->n_controls;
+  p.oct_start = st->oct_start;
+  p.ctrl = st->ctrl;
+  p.nzmask = st->nzmask;
+  p.weights = st->weights;
+  p.cost = st->cost;
+  p.v = v;
+  p.kind = kind;
+  p.fmask = fmask;
+  p.coef = coef;
+  p.coef0 = coef0;
+  p.unreach = unreach;
+  p.out = out;
+  p.evals = evals;
+  size_t smem = (size_t)StencilSmem<D, T>::bytes(p.n_classes, p.nc) +
+                (size_t)p.n_classes * p.nc * 4 + 16;
+  auto k = feedback_kernel<D, T, RULE, COST>;
+  PHJ_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int blocks = std::min(p.tg.total, 8 * phj_num_sms());
+  k<<<blocks, kThreads, smem, stream>>>(p);
+  PHJ_CUDA(cudaGetLastError());
+  return PHJ_OK;
+}
+
+extern "C" int phj_feedback(const phj_grid* g, const phj_stencil* st, int32_t dtype, int32_t rule,
+                            const void* v, const int8_t* kind, const uint32_t* fmask,
+                            const void* coef, double coef0, double unreach, int32_t* out,
+                            unsigned long long* evals, void* stream) {
+  if (!g || !st || !v || !kind || !fmask || !out) {
+    phj_set_error("phj_feedback: missing argument");
+    return PHJ_ERR_ARG;
+  }
+  if (rule == PHJ_RULE_REF && dtype == PHJ_F32) {
+    phj_set_error("phj_feedback: the reference (sentinel) rule is fp64 only");
+    return PHJ_ERR_UNSUPPORTED;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const int D = g->dim, f32 = dtype == PHJ_F32, krz = rule == PHJ_RULE_KRUZKOV,
+            cc = st->cost_mode == PHJ_COST_CTRL;
+#define PHJ_FB(DD, TT, RR, CC)                                                             \
+  if (D == DD && f32 == (sizeof(TT) == 4) && krz == (RR == PHJ_RULE_KRUZKOV) &&           \
+      cc == (CC == PHJ_COST_CTRL))                                                         \
+    return feedback_impl<DD, TT, RR, CC>(g, st, v, kind, fmask, coef, coef0, unreach, out, \
+                                         evals, s);
+  PHJ_FB(2, double, PHJ_RULE_REF, PHJ_COST_NODE)
+  PHJ_FB(2, double, PHJ_RULE_REF, PHJ_COST_CTRL)
+  PHJ_FB(2, double, PHJ_RULE_KRUZKOV, PHJ_COST_NODE)
+  PHJ_FB(2, double, PHJ_RULE_KRUZKOV, PHJ_COST_CTRL)
+  PHJ_FB(2, float, PHJ_RULE_KRUZKOV, PHJ_COST_NODE)
+  PHJ_FB(2, float, PHJ_RULE_KRUZKOV, PHJ_COST_CTRL)
+  PHJ_FB(3, double, PHJ_RULE_REF, PHJ_COST_NODE)
+  PHJ_FB(3, double, PHJ_RULE_REF, PHJ_COST_CTRL)
+  PHJ_FB(3, double, PHJ_RULE_KRUZKOV, PHJ_COST_NODE)
+  PHJ_FB(3, double, PHJ_RULE_KRUZKOV, PHJ_COST_CTRL)
+  PHJ_FB(3, float, PHJ_RULE_KRUZKOV, PHJ_COST_NODE)
+  PHJ_FB(3, float, PHJ_RULE_KRUZKOV, PHJ_COST_CTRL)
+#undef PHJ_FB
+  phj_set_error("phj_feedback: unsupported combination");
+  return PHJ_ERR_UNSUPPORTED;
+}
+
+static int fmask_launch(const phj_grid* g, const int16_t* lab, const uint8_t* hard,
+                        uint32_t* fmask, cudaStream_t s) {
+  const int64_t N = g->shape[0] * g->shape[1] * (g->dim == 3 ? g->shape[2] : 1);
+  int blocks = (int)std::min<int64_t>((N + 255) / 256, 32 * phj_num_sms());
+  if (blocks < 1) blocks = 1;
+  if (g->dim == 2) fmask_kernel<2><<<blocks, 256, 0, s>>>(*g, lab, hard, fmask);
+  else fmask_kernel<3><<<blocks, 256, 0, s>>>(*g, lab, hard, fmask);
+  PHJ_CUDA(cudaGetLastError());
+  return PHJ_OK;
+}
+
+extern "C" int phj_fmask_from_labels(const phj_grid* g, const int16_t* lab, uint32_t* fmask,
+                                     void* stream) {
+  if (!g || !lab || !fmask) {
+    phj_set_error("phj_fmask_from_labels: missing argument");
+    return PHJ_ERR_ARG;
+  }
+  return fmask_launch(g, lab, nullptr, fmask, (cudaStream_t)stream);
+}
+
+extern "C" int phj_fmask_from_hard(const phj_grid* g, const uint8_t* hard, uint32_t* fmask,
+                                   void* stream) {
+  if (!g || !hard || !fmask) {
+    phj_set_error("phj_fmask_from_hard: missing argument");
+    return PHJ_ERR_ARG;
+  }
+  return fmask_launch(g, nullptr, hard, fmask, (cudaStream_t)stream);
+}
