@@ -217,6 +217,8 @@ int phj_peak_flops(int32_t dtype, int32_t iters, double* sink, void* stream);
 
 const char* phj_last_error(void);
 int phj_num_sms(void);
+/* number of kernels this library has launched in the process (bench evidence) */
+unsigned long long phj_launch_count(void);
 
 #ifdef __cplusplus
 }

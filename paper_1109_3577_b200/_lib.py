@@ -69,6 +69,7 @@ EXPORTS = (
     "phj_assemble_repair", "phj_assemble_finish", "phj_classify", "phj_node_coef",
     "phj_init_field", "phj_to_kruzkov", "phj_from_kruzkov", "phj_sync_periodic",
     "phj_error_partials", "phj_peak_flops", "phj_last_error", "phj_num_sms",
+    "phj_launch_count",
 )
 
 _lib: Optional[ctypes.CDLL] = None
@@ -110,6 +111,7 @@ def load() -> ctypes.CDLL:
         "phj_peak_flops": (ctypes.c_int, [I32, I32, P, P]),
         "phj_last_error": (ctypes.c_char_p, []),
         "phj_num_sms": (ctypes.c_int, []),
+        "phj_launch_count": (ctypes.c_ulonglong, []),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -143,6 +143,7 @@ __device__ inline int ld_cg(const int* p) { return __ldcg(p); }
 
 // error plumbing shared by the .cu translation units
 void phj_set_error(const char* fmt, ...);
+void phj_count_launch(int n);  // every kernel launch of the library bumps this
 int phj_check_cuda(cudaError_t e, const char* what);
 #define PHJ_CUDA(call)                                   \
   do {                                                   \

@@ -23,6 +23,12 @@ int phj_check_cuda(cudaError_t e, const char* what) {
 }
 
 extern "C" const char* phj_last_error(void) { return g_err; }
+
+static unsigned long long g_launches = 0;
+void phj_count_launch(int n) { __atomic_fetch_add(&g_launches, (unsigned long long)n, __ATOMIC_RELAXED); }
+extern "C" unsigned long long phj_launch_count(void) {
+  return __atomic_load_n(&g_launches, __ATOMIC_RELAXED);
+}
 extern "C" int phj_num_sms(void);
 
 namespace phj {
@@ -479,7 +485,7 @@ extern "C" int phj_lift(const phj_grid* gc, const phj_grid* gf, int32_t dtype, c
                                           sat_value, saturate);
   else
     lift_kernel<double><<<nb, 256, 0, s>>>(*gc, *gf, (const double*)vc, (double*)vf,
-                                           sat_threshold, sat_value, saturate);
+                                           sat_threshold, sat_value, saturate); phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   return PHJ_OK;
 }
@@ -491,7 +497,7 @@ extern "C" int phj_argmax_update(const phj_grid* g, const double* phi, int32_t j
     return PHJ_ERR_ARG;
   }
   argmax_kernel<<<grid_blocks(n_interior(*g)), 256, 0, (cudaStream_t)stream>>>(*g, phi, j, best_val,
-                                                                               best_idx);
+                                                                               best_idx); phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   return PHJ_OK;
 }
@@ -504,7 +510,7 @@ extern "C" int phj_assemble_codes(const phj_grid* g, const double* best_val,
     return PHJ_ERR_ARG;
   }
   codes_kernel<<<grid_blocks(n_interior(*g)), 256, 0, (cudaStream_t)stream>>>(*g, best_val, best_idx,
-                                                                              mask, kind, color);
+                                                                              mask, kind, color); phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   return PHJ_OK;
 }
@@ -518,7 +524,7 @@ extern "C" int phj_assemble_repair(const phj_grid* g, const int32_t* color_in, i
   cudaStream_t s = (cudaStream_t)stream;
   PHJ_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(int32_t), s));
   repair_kernel<<<grid_blocks(n_interior(*g)), 256, 0, s>>>(*g, color_in, color_out, n_colors,
-                                                            counters);
+                                                            counters); phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   return PHJ_OK;
 }
@@ -532,9 +538,9 @@ extern "C" int phj_assemble_finish(const phj_grid* g, int32_t* color, uint8_t* b
   cudaStream_t s = (cudaStream_t)stream;
   const int nb = grid_blocks(n_interior(*g));
   PHJ_CUDA(cudaMemsetAsync(counters + 2, 0, sizeof(int32_t), s));
-  finish_kernel<<<nb, 256, 0, s>>>(*g, color, boundary, lab, counters);
-  finish2_kernel<<<nb, 256, 0, s>>>(*g, color);
-  finish3_kernel<<<nb, 256, 0, s>>>(*g, color, boundary, lab);
+  finish_kernel<<<nb, 256, 0, s>>>(*g, color, boundary, lab, counters); phj_count_launch(1);
+  finish2_kernel<<<nb, 256, 0, s>>>(*g, color); phj_count_launch(1);
+  finish3_kernel<<<nb, 256, 0, s>>>(*g, color, boundary, lab); phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   return PHJ_OK;
 }
@@ -569,7 +575,7 @@ extern "C" int phj_classify(const phj_grid* g, const phj_shapes* sh, const int32
   if (user_axis)
     for (int i = 0; i < d; ++i) ua[i] = user_axis[i];
   classify_kernel<<<grid_blocks(n_interior(*g)), 256, 0, (cudaStream_t)stream>>>(
-      *g, S, ua[0], ua[1], ua[2], kind);
+      *g, S, ua[0], ua[1], ua[2], kind); phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   return PHJ_OK;
 }
@@ -588,7 +594,7 @@ extern "C" int phj_node_coef(const phj_grid* g, const phj_speed_model* m, const 
   if (dtype == PHJ_F32)
     coef_kernel<float><<<nb, 256, 0, s>>>(*g, *m, ua[0], ua[1], ua[2], rule, (float*)coef);
   else
-    coef_kernel<double><<<nb, 256, 0, s>>>(*g, *m, ua[0], ua[1], ua[2], rule, (double*)coef);
+    coef_kernel<double><<<nb, 256, 0, s>>>(*g, *m, ua[0], ua[1], ua[2], rule, (double*)coef); phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   return PHJ_OK;
 }
@@ -604,7 +610,7 @@ extern "C" int phj_init_field(const phj_grid* g, int32_t dtype, const int8_t* ki
   if (dtype == PHJ_F32)
     init_field_kernel<float><<<grid_blocks(NE), 256, 0, s>>>(*g, kind, unreached, (float*)v);
   else
-    init_field_kernel<double><<<grid_blocks(NE), 256, 0, s>>>(*g, kind, unreached, (double*)v);
+    init_field_kernel<double><<<grid_blocks(NE), 256, 0, s>>>(*g, kind, unreached, (double*)v); phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   return PHJ_OK;
 }
@@ -619,7 +625,7 @@ extern "C" int phj_to_kruzkov(int64_t n, int32_t dtype, const double* T, void* v
   if (dtype == PHJ_F32)
     to_kruzkov_kernel<float><<<grid_blocks(n), 256, 0, s>>>(n, T, (float*)v, half_sentinel);
   else
-    to_kruzkov_kernel<double><<<grid_blocks(n), 256, 0, s>>>(n, T, (double*)v, half_sentinel);
+    to_kruzkov_kernel<double><<<grid_blocks(n), 256, 0, s>>>(n, T, (double*)v, half_sentinel); phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   return PHJ_OK;
 }
@@ -634,7 +640,7 @@ extern "C" int phj_from_kruzkov(int64_t n, int32_t dtype, const void* v, double*
   if (dtype == PHJ_F32)
     from_kruzkov_kernel<float><<<grid_blocks(n), 256, 0, s>>>(n, (const float*)v, T, sentinel);
   else
-    from_kruzkov_kernel<double><<<grid_blocks(n), 256, 0, s>>>(n, (const double*)v, T, sentinel);
+    from_kruzkov_kernel<double><<<grid_blocks(n), 256, 0, s>>>(n, (const double*)v, T, sentinel); phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   return PHJ_OK;
 }
@@ -652,10 +658,10 @@ extern "C" int phj_sync_periodic(const phj_grid* g, int32_t elem_bytes, void* v,
       if (a != ax) plane *= g->ext[a];
     const int nb = grid_blocks(plane);
     switch (elem_bytes) {
-      case 1: periodic_kernel<uint8_t><<<nb, 256, 0, s>>>(*g, (uint8_t*)v, ax); break;
-      case 2: periodic_kernel<int16_t><<<nb, 256, 0, s>>>(*g, (int16_t*)v, ax); break;
-      case 4: periodic_kernel<int32_t><<<nb, 256, 0, s>>>(*g, (int32_t*)v, ax); break;
-      case 8: periodic_kernel<int64_t><<<nb, 256, 0, s>>>(*g, (int64_t*)v, ax); break;
+      case 1: periodic_kernel<uint8_t><<<nb, 256, 0, s>>>(*g, (uint8_t*)v, ax); phj_count_launch(1); break;
+      case 2: periodic_kernel<int16_t><<<nb, 256, 0, s>>>(*g, (int16_t*)v, ax); phj_count_launch(1); break;
+      case 4: periodic_kernel<int32_t><<<nb, 256, 0, s>>>(*g, (int32_t*)v, ax); phj_count_launch(1); break;
+      case 8: periodic_kernel<int64_t><<<nb, 256, 0, s>>>(*g, (int64_t*)v, ax); phj_count_launch(1); break;
       default: phj_set_error("phj_sync_periodic: elem_bytes"); return PHJ_ERR_ARG;
     }
   }
@@ -671,7 +677,7 @@ extern "C" int phj_error_partials(int64_t n, const double* a, const double* b, d
   }
   cudaStream_t s = (cudaStream_t)stream;
   PHJ_CUDA(cudaMemsetAsync(out, 0, 3 * sizeof(double), s));
-  error_kernel<<<grid_blocks(n), 256, 0, s>>>(n, a, b, half_a, half_b, out);
+  error_kernel<<<grid_blocks(n), 256, 0, s>>>(n, a, b, half_a, half_b, out); phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   return PHJ_OK;
 }
@@ -680,7 +686,7 @@ extern "C" int phj_peak_flops(int32_t dtype, int32_t iters, double* sink, void* 
   cudaStream_t s = (cudaStream_t)stream;
   const int blocks = 8 * (phj_num_sms() > 0 ? phj_num_sms() : 148);
   if (dtype == PHJ_F32) peak_kernel<float><<<blocks, 256, 0, s>>>(iters, (float*)sink);
-  else peak_kernel<double><<<blocks, 256, 0, s>>>(iters, sink);
+  else peak_kernel<double><<<blocks, 256, 0, s>>>(iters, sink); phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   return PHJ_OK;
 }

@@ -20,6 +20,7 @@
 //    (patchy.py:362-377); later sweeps copy its nodes through unchanged.
 #include <cooperative_groups.h>
 #include <cstdio>
+#include <cstdlib>
 
 #include "phj_common.cuh"
 
@@ -226,8 +227,10 @@ struct EvalAll<D, T, NB, RULE, COST, SLOW, MODE, (1 << D)> {
                                              const int32_t*, T (&)[NB], int (&)[NB]) {}
 };
 
-// Thread -> row mapping inside a tile.  Returns false if the row is outside
-// the grid.  c[] receives the interior index of the thread's first node.
+// Thread -> row mapping inside a tile.  Returns false if the warp's row is
+// outside the grid (warp-uniform: callers use full-mask warp votes after it;
+// lanes past the end of the row are masked per node instead).  c[] receives
+// the interior index of the thread's first node.
 template <int D>
 __device__ inline bool thread_row(const phj_grid& g, const int o[3], int c[3]) {
   using TL = Tile<D>;
@@ -236,12 +239,12 @@ __device__ inline bool thread_row(const phj_grid& g, const int o[3], int c[3]) {
     c[0] = o[0] + warp;
     c[1] = o[1] + lane * TL::NB;
     c[2] = 0;
-    return c[0] < g.shape[0] && c[1] < g.shape[1];
+    return c[0] < g.shape[0];
   } else {
     c[0] = o[0] + warp / TL::TY;
     c[1] = o[1] + warp % TL::TY;
     c[2] = o[2] + lane * TL::NB;
-    return c[0] < g.shape[0] && c[1] < g.shape[1] && c[2] < g.shape[2];
+    return c[0] < g.shape[0] && c[1] < g.shape[1];
   }
 }
 
@@ -855,10 +858,12 @@ static int coop_launch(K kernel, int want_blocks, size_t smem, void** args, cuda
     return PHJ_ERR_UNSUPPORTED;
   }
   int blocks = std::min(want_blocks, occ * phj_num_sms());
+  if (const char* cap = getenv("PHJ_MAX_BLOCKS")) blocks = std::min(blocks, atoi(cap));
   if (blocks < 1) blocks = 1;
   if (launched) *launched = blocks;
   PHJ_CUDA(cudaLaunchCooperativeKernel((void*)kernel, dim3(blocks), dim3(kThreads), args, smem,
                                        stream));
+  phj_count_launch(1);
   return PHJ_OK;
 }
 
@@ -896,7 +901,7 @@ static int solve_impl(const phj_solve_args* a) {
   PHJ_CUDA(cudaMemsetAsync(a->evals, 0, sizeof(unsigned long long), stream));
   PHJ_CUDA(cudaMemsetAsync(a->info, 0, 4 * sizeof(int32_t), stream));
   build_list_kernel<D><<<p.tg.total, kThreads, 0, stream>>>(
-      p.g, p.tg, p.lab, p.mine, p.ws.flags[0], p.ws.list[0], p.ws.counts, 0, nullptr, nullptr);
+      p.g, p.tg, p.lab, p.mine, p.ws.flags[0], p.ws.list[0], p.ws.counts, 0, nullptr, nullptr); phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   size_t smem = (size_t)StencilSmem<D, T>::bytes(p.n_classes, p.nc) +
                 (size_t)((p.R + 1) / 2 * 2) * 4 + (size_t)std::min(p.R, kSmemPatchReduce) * 8 + 16;
@@ -977,7 +982,7 @@ static int transport_impl(const phj_transport_args* a) {
   PHJ_CUDA(cudaMemsetAsync(a->info, 0, 4 * sizeof(int32_t), stream));
   PHJ_CUDA(cudaMemsetAsync(a->updates, 0, sizeof(unsigned long long), stream));
   build_list_kernel<D><<<p.tg.total, kThreads, 0, stream>>>(
-      p.g, p.tg, nullptr, nullptr, p.ws.flags[0], p.ws.list[0], p.ws.counts, 1, p.fb, p.kind);
+      p.g, p.tg, nullptr, nullptr, p.ws.flags[0], p.ws.list[0], p.ws.counts, 1, p.fb, p.kind); phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   const int nent = p.n_classes * p.nc;
   size_t smem = (size_t)nent * (1 << D) * 8 + (size_t)nent * 4 + (size_t)nent + 16;
@@ -1026,7 +1031,7 @@ static int feedback_impl(const phj_grid* g, const phj_stencil* st, const void* v
   auto k = feedback_kernel<D, T, RULE, COST>;
   PHJ_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int blocks = std::min(p.tg.total, 8 * phj_num_sms());
-  k<<<blocks, kThreads, smem, stream>>>(p);
+  k<<<blocks, kThreads, smem, stream>>>(p); phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   return PHJ_OK;
 }
@@ -1074,7 +1079,7 @@ static int fmask_launch(const phj_grid* g, const int16_t* lab, const uint8_t* ha
   int blocks = (int)std::min<int64_t>((N + 255) / 256, 32 * phj_num_sms());
   if (blocks < 1) blocks = 1;
   if (g->dim == 2) fmask_kernel<2><<<blocks, 256, 0, s>>>(*g, lab, hard, fmask);
-  else fmask_kernel<3><<<blocks, 256, 0, s>>>(*g, lab, hard, fmask);
+  else fmask_kernel<3><<<blocks, 256, 0, s>>>(*g, lab, hard, fmask); phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   return PHJ_OK;
 }

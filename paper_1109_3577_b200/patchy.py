@@ -282,12 +282,16 @@ def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Te
     warnings = []
     stats = []
     performed = 0
+    kernel_ms = 0.0
+    sweeps_total = 0
     if pcfg.bc_mode == STATE_CONSTRAINT:
         fmask = plan.fmask_from_labels(lab)
         res = device_solve(plan, work, lab, fmask, n_patches, rule=rule, dtype=dtype, tol=cfg.tol,
                            max_sweeps=cfg.sweep_limit(plan.grid), mine=mine)
         out = res.values
         performed = res.evals
+        kernel_ms += res.device_ms
+        sweeps_total = int(res.info[0])
         for j in range(n_patches):
             if mine is not None and not bool(mine[j]):
                 stats.append(SweepStats())
@@ -322,6 +326,8 @@ def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Te
             oi = plan.interior_int(out)
             oi.copy_(torch.where(own, plan.interior_int(res.values), oi))
             performed += res.evals
+            kernel_ms += res.device_ms
+            sweeps_total += int(res.info[0])
             stats.append(stats_for_patch(res, 0, int(sizes[j]), plan.n_adm, cfg.tol))
         _sync_periodic(plan, out)
     if world > 1:
@@ -336,7 +342,8 @@ def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Te
     blocked = (col3 < 0) & (col3 != TARGET)
     oi.copy_(torch.where(blocked, torch.full_like(oi, unr), oi))
     _sync_periodic(plan, out)
-    return out, stats, warnings, performed
+    return out, stats, warnings, {"performed": performed, "kernel_ms": kernel_ms,
+                                  "sweeps": sweeps_total}
 
 
 # -- public API (reference signatures, user layout) -----------------------------------
@@ -454,18 +461,26 @@ def solve_patches(spec: ProblemSpec, grid: Grid, patch_map: PatchMap, lifted: No
     return res, stats, warnings
 
 
+def make_plans(spec: ProblemSpec, pcfg: PatchyConfig):
+    """(fine plan, coarse plan) for run_patchy -- the 'tables' phase."""
+    fplan = StencilPlan(spec.make_grid(pcfg.fine_nodes), spec)
+    cplan = StencilPlan(spec.make_grid(pcfg.coarse_nodes), _coarse_spec(spec, pcfg.coarse_target))
+    return fplan, cplan
+
+
 def run_patchy(spec: ProblemSpec, pcfg: PatchyConfig, cfg: Optional[SolverConfig] = None,
-               strategy: Optional[ExecutionStrategy] = None) -> PatchyResult:
-    """Full pipeline on the device (patchy.py:405-467)."""
+               strategy: Optional[ExecutionStrategy] = None, *, plans=None,
+               outputs: bool = True) -> PatchyResult:
+    """Full pipeline on the device (patchy.py:405-467).  ``plans`` reuses
+    prebuilt (fine, coarse) StencilPlans; ``outputs=False`` skips building
+    the user-layout lifted/feedback/patch-map outputs (value only)."""
     cfg = cfg or SolverConfig()
     require_cuda()
     stats = RunStats()
-    coarse_grid = spec.make_grid(pcfg.coarse_nodes)
-    fine_grid = spec.make_grid(pcfg.fine_nodes)
     rule, dtype = cfg.rule, cfg.dtype
     with stats.phase("tables"):
-        fplan = StencilPlan(fine_grid, spec)
-        cplan = StencilPlan(coarse_grid, _coarse_spec(spec, pcfg.coarse_target))
+        fplan, cplan = plans if plans is not None else make_plans(spec, pcfg)
+    fine_grid = fplan.grid
     with stats.phase("coarse"):
         vc, cst = solve_full_internal(cplan, cfg)
         stats.merge_counts(cst)
@@ -502,23 +517,27 @@ def run_patchy(spec: ProblemSpec, pcfg: PatchyConfig, cfg: Optional[SolverConfig
             stats.warnings)
         n_colors = max(n_colors, len(parts))
     with stats.phase("patch_solve"):
-        out, pstats, warnings, performed = solve_patches_internal(
+        out, pstats, warnings, pinfo = solve_patches_internal(
             fplan, color, lab, n_colors, pcfg, cfg, vf)
         stats.warnings.extend(warnings)
         for st in pstats:
             stats.merge_counts(st)
-        stats.performed_evals += performed
+        stats.performed_evals += pinfo["performed"]
+        stats.kernels["patch_solve"] = pinfo
     stats.candidate_evals += int(ev.item())
-    stats.finalize()
+    value = NodeField(fine_grid, fplan.user_from_working(out, rule, dtype))
+    if not outputs:
+        stats.finalize()
+        return PatchyResult(value, None, None, None, stats, cst, pstats, transport_sweeps)
     pm = PatchMap(fine_grid, n_colors, fplan.serial_to_user(color), None,
                   fplan.serial_to_user(boundary).bool(),
                   np.arange(n_unc) if n_unc else np.empty(0, dtype=np.int64))
     imb = pm.imbalance_warning()
     if imb:
         stats.warnings.append(imb)
-    value = NodeField(fine_grid, fplan.user_from_working(out, rule, dtype))
     lifted = NodeField(fine_grid, fplan.user_from_working(vf, rule, dtype))
     feedback = FeedbackField(fine_grid, spec.control_set, fplan.serial_to_user(fb))
+    stats.finalize()
     return PatchyResult(value, pm, lifted, feedback, stats, cst, pstats, transport_sweeps)
 
 

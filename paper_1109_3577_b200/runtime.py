@@ -64,6 +64,7 @@ class RunStats:
     warnings: list = field(default_factory=list)
     speedup_vs_serial: float = None
     performed_evals: int = 0
+    kernels: dict = field(default_factory=dict)
     _pending: list = field(default_factory=list, repr=False)
 
     @contextmanager

@@ -410,11 +410,17 @@ def device_solve(plan: StencilPlan, work: torch.Tensor, lab: torch.Tensor, fmask
     a.evals = _lib.ptr(ev)
     a.info = _lib.ptr(info)
     a.stream = _lib.stream_handle()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
     _lib.check(lib.phj_solve(ctypes_ref(a)), "phj_solve")
+    e1.record()
     info_h = info.cpu().numpy()
     res = v1 if int(info_h[1]) == 1 else work
-    return DeviceSolveResult(res, ps.cpu().numpy(), mc.view(max_sweeps, n_patches).cpu().numpy(),
-                             int(ev.item()), info_h)
+    out = DeviceSolveResult(res, ps.cpu().numpy(), mc.view(max_sweeps, n_patches).cpu().numpy(),
+                            int(ev.item()), info_h)
+    out.device_ms = e0.elapsed_time(e1)
+    return out
 
 
 def stats_for_patch(res: DeviceSolveResult, p: int, n_nodes: int, n_adm: int, tol: float,
