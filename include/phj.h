@@ -72,6 +72,10 @@ typedef struct phj_grid {
   double k; /* step length |h f| = k (grid.py:67) */
 } phj_grid;
 
+/* entries evaluated per inner-loop iteration; each octant group of a class
+ * holds a multiple of this many entries */
+#define PHJ_UNROLL(dim) ((dim) == 2 ? 4 : 2)
+
 /* Node-independent interpolation stencils, one set per class (class index =
  * interior index along internal axis 0 when n_classes > 1).  Entries of a
  * class are sorted by foot octant; octant bit ax = foot on the + side of
@@ -80,8 +84,11 @@ typedef struct phj_grid {
 typedef struct phj_stencil {
   int32_t dim;
   int32_t n_classes;
-  int32_t n_controls; /* entries per class */
+  int32_t n_controls; /* entry slots per class (octant groups padded to a
+                         multiple of PHJ_UNROLL(dim) by repeating an entry) */
   int32_t cost_mode;  /* PHJ_COST_NODE or PHJ_COST_CTRL */
+  int32_t n_real;     /* admissible controls per class (work accounting) */
+  int32_t pad_;
   const int32_t* oct_start; /* [n_classes][2^dim + 1] */
   const int32_t* ctrl;      /* [n_classes][nc] original control index */
   const uint32_t* nzmask;   /* [n_classes][nc] nonzero-weight 3^dim positions */
@@ -133,9 +140,10 @@ int phj_feedback(const phj_grid* g, const phj_stencil* st, int32_t dtype, int32_
                  double coef0, double unreach, int32_t* out, unsigned long long* evals,
                  void* stream);
 
-/* Colour transport of one target part to max|change| <= tol (Jacobi, whole
- * loop on device).  phi0/phi1 hold the start field; movers have fb >= 0 and
- * kind == 0.  Result buffer index and sweeps go to info[0..1]. */
+/* Colour transport of all target parts at once, each to its own
+ * max|change| <= tol (Jacobi, whole loop on device, one launch).  phi0/phi1
+ * are colour-major [n_colors][ext nodes] doubles holding the start fields
+ * (1 on the part, 0 elsewhere); movers have fb >= 0 and kind == 0. */
 typedef struct phj_transport_args {
   phj_grid grid;
   phj_stencil st;
@@ -143,13 +151,22 @@ typedef struct phj_transport_args {
   double* phi1;
   const int32_t* fb;    /* per internal serial, original control index or -1 */
   const int8_t* kind;   /* per internal serial */
+  int32_t* ent_scratch; /* [interior nodes] int32 scratch (mover -> stencil entry) */
+  int32_t n_colors;
   double tol;
   int32_t max_sweeps;
   void* workspace;      /* phj_solve_workspace_bytes(g, 1, max_sweeps) */
-  int32_t* info;        /* out [4]: sweeps, result buffer, converged, tiles */
-  unsigned long long* updates; /* out [1] */
+  double* maxch_hist;   /* out [max_sweeps][n_colors] */
+  int32_t* color_sweeps; /* out [n_colors]: sweeps to converge, -(cap) if not */
+  int32_t* info;        /* out [4]: total sweeps, result buffer, -, - */
+  unsigned long long* updates; /* out [1]: mover updates performed */
   void* stream;
 } phj_transport_args;
+
+/* argmax over the colours of a [n_colors][ext] colour field (strict >,
+ * lowest colour on ties, patchy.py:251-256) */
+int phj_argmax_colors(const phj_grid* g, const double* phi, int32_t n_colors, double* best_val,
+                      int32_t* best_idx, void* stream);
 int phj_transport(const phj_transport_args* a);
 
 /* Saturating multilinear lift of a coarse ext field to fine ext interior. */
@@ -205,7 +222,8 @@ int phj_to_kruzkov(int64_t n, int32_t dtype, const double* T, void* v, double ha
                    void* stream);
 int phj_from_kruzkov(int64_t n, int32_t dtype, const void* v, double* T, double sentinel,
                      void* stream);
-/* copy interior ghost layers for periodic axes */
+/* copy interior ghost layers for periodic axes; elem_bytes = bytes per node
+ * (1, 2, 4, 8, or a multiple of 8 for node-major multi-value fields) */
 int phj_sync_periodic(const phj_grid* g, int32_t elem_bytes, void* v, void* stream);
 
 /* E1/Einf partial sums: out[0]=sum|a-b|, out[1]=max, out[2]=compared count */

@@ -12,7 +12,8 @@ import os
 from typing import Optional
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libphj.so")
+# PHJ_LIB_PATH selects an alternative in-tree build (kernel variant A/B runs)
+LIB_PATH = os.environ.get("PHJ_LIB_PATH") or os.path.join(HERE, "_lib", "libphj.so")
 
 PHJ_OK = 0
 F64, F32 = 0, 1
@@ -34,7 +35,13 @@ class Grid(ctypes.Structure):
 
 class Stencil(ctypes.Structure):
     _fields_ = [("dim", I32), ("n_classes", I32), ("n_controls", I32), ("cost_mode", I32),
+                ("n_real", I32), ("pad_", I32),
                 ("oct_start", P), ("ctrl", P), ("nzmask", P), ("weights", P), ("cost", P)]
+
+
+def unroll(dim: int) -> int:
+    """PHJ_UNROLL(dim): octant groups are padded to a multiple of this."""
+    return 4 if dim == 2 else 2
 
 
 class SolveArgs(ctypes.Structure):
@@ -47,8 +54,9 @@ class SolveArgs(ctypes.Structure):
 
 class TransportArgs(ctypes.Structure):
     _fields_ = [("grid", Grid), ("st", Stencil), ("phi0", P), ("phi1", P), ("fb", P),
-                ("kind", P), ("tol", D), ("max_sweeps", I32), ("workspace", P), ("info", P),
-                ("updates", P), ("stream", P)]
+                ("kind", P), ("ent_scratch", P), ("n_colors", I32), ("tol", D),
+                ("max_sweeps", I32), ("workspace", P), ("maxch_hist", P), ("color_sweeps", P),
+                ("info", P), ("updates", P), ("stream", P)]
 
 
 class Shapes(ctypes.Structure):
@@ -65,7 +73,8 @@ class SpeedModel(ctypes.Structure):
 #: every symbol include/phj.h declares (checked by the CPU test suite)
 EXPORTS = (
     "phj_solve_workspace_bytes", "phj_solve", "phj_fmask_from_labels", "phj_fmask_from_hard",
-    "phj_feedback", "phj_transport", "phj_lift", "phj_argmax_update", "phj_assemble_codes",
+    "phj_feedback", "phj_transport", "phj_lift", "phj_argmax_update", "phj_argmax_colors",
+    "phj_assemble_codes",
     "phj_assemble_repair", "phj_assemble_finish", "phj_classify", "phj_node_coef",
     "phj_init_field", "phj_to_kruzkov", "phj_from_kruzkov", "phj_sync_periodic",
     "phj_error_partials", "phj_peak_flops", "phj_last_error", "phj_num_sms",
@@ -98,6 +107,7 @@ def load() -> ctypes.CDLL:
         "phj_transport": (ctypes.c_int, [P]),
         "phj_lift": (ctypes.c_int, [P, P, I32, P, P, D, D, I32, P]),
         "phj_argmax_update": (ctypes.c_int, [P, P, I32, P, P, P]),
+        "phj_argmax_colors": (ctypes.c_int, [P, P, I32, P, P, P]),
         "phj_assemble_codes": (ctypes.c_int, [P, P, P, P, P, P, P]),
         "phj_assemble_repair": (ctypes.c_int, [P, P, P, I32, P, P]),
         "phj_assemble_finish": (ctypes.c_int, [P, P, P, P, P, P]),

@@ -19,7 +19,7 @@ from .dynamics import Dubins, ScaledSpeed, SinProduct
 from .patchy import PatchyConfig
 from .problems import (ControlSet, ProblemSpec, TargetSpec, discretize_circle, fibonacci_sphere,
                        partition_balls_halves, partition_octants, partition_random_directions,
-                       partition_target)
+                       partition_target, target_nodes)
 from .solver import SolverConfig
 
 SEED_C2 = 1109  # disk centres of config 2
@@ -92,10 +92,9 @@ def c3(rule: str = "kruzkov", dtype: str = "float64", n: int = 257,
 
 
 def theta_slabs(n_parts: int) -> Callable:
-    def parts(target, grid):
-        pts = grid.interior_points()
-        serials = np.where(target.contains(pts))[0]
-        th = pts[serials, 2]
+    def parts(target, grid, serials=None):
+        serials, tp = target_nodes(target, grid, serials)
+        th = tp[:, 2]
         code = np.clip(np.floor((th - grid.lo[2]) / (grid.hi[2] - grid.lo[2]) * n_parts)
                        .astype(int), 0, n_parts - 1)
         return [serials[code == j] for j in range(n_parts)]
@@ -133,7 +132,8 @@ def c5(rule: str = "kruzkov", dtype: str = "float32", n: int = 513,
                        dynamics=ScaledSpeed(speed).dynamics(), control_set=fibonacci_sphere(96),
                        target=TargetSpec.ball((0.0, 0.0, 0.0), 0.15), model=ScaledSpeed(speed))
     pcfg = PatchyConfig(n_patches=32, coarse_nodes=nc_, fine_nodes=n,
-                        parts=lambda t, g: partition_random_directions(t, g, 32, seed))
+                        parts=lambda t, g, serials=None: partition_random_directions(
+                            t, g, 32, seed, serials=serials))
     return Workload("c5", f"3D variable speed {n}^3, 96 controls, 32 patches", spec, pcfg,
                     SolverConfig(tol=1e-8 if dtype == "float64" else 1e-6, rule=rule,
                                  dtype=dtype), (n,) * 3, (nc_,) * 3)

@@ -9,62 +9,70 @@
 namespace phj {
 
 constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
 constexpr int kMaxPatches = 1024;
 constexpr int kSmemPatchReduce = 64;  // per-CTA patch max reduction when R <= 64
 
-// Tile geometry: each warp owns one row segment of 32*NB consecutive nodes
-// along the fastest internal axis (so a warp's class index -- internal axis
-// 0 -- is uniform); a CTA owns TY (x TZ) such rows.
-template <int D> struct Tile;
-template <> struct Tile<2> {
-  static constexpr int NB = 4, TX = 128, TY = 8, TZ = 1;
+// Work/activity unit = one warp "block" of nodes: LY rows x (LX lanes * NB
+// consecutive nodes) along the fastest internal axis, one plane of internal
+// axis 0 in 3D (so the stencil class -- internal axis 0 -- is warp-uniform).
+// Each lane keeps its NB nodes' 3^D neighbourhood in registers.
+template <int D> struct Blk;
+template <> struct Blk<2> {
+  static constexpr int NB = 4, LX = 8, LY = 4, BX = LX * NB, BY = LY;
 };
-template <> struct Tile<3> {
-  static constexpr int NB = 2, TX = 64, TY = 4, TZ = 2;
+template <> struct Blk<3> {
+  static constexpr int NB = 2, LX = 8, LY = 4, BX = LX * NB, BY = LY;
 };
 
 struct TileGrid {
-  int n[3];      // tiles per internal axis (axis 0 slowest)
+  int n[3];  // blocks per internal axis (axis 0 slowest)
   int total;
 };
 
 template <int D>
 __host__ __device__ inline TileGrid make_tile_grid(const phj_grid& g) {
   TileGrid t;
+  using B = Blk<D>;
   if (D == 2) {
-    t.n[0] = (int)((g.shape[0] + Tile<2>::TY - 1) / Tile<2>::TY);
-    t.n[1] = (int)((g.shape[1] + Tile<2>::TX - 1) / Tile<2>::TX);
+    t.n[0] = (int)((g.shape[0] + B::BY - 1) / B::BY);
+    t.n[1] = (int)((g.shape[1] + B::BX - 1) / B::BX);
     t.n[2] = 1;
     t.total = t.n[0] * t.n[1];
   } else {
-    t.n[0] = (int)((g.shape[0] + Tile<3>::TZ - 1) / Tile<3>::TZ);
-    t.n[1] = (int)((g.shape[1] + Tile<3>::TY - 1) / Tile<3>::TY);
-    t.n[2] = (int)((g.shape[2] + Tile<3>::TX - 1) / Tile<3>::TX);
+    t.n[0] = (int)g.shape[0];
+    t.n[1] = (int)((g.shape[1] + B::BY - 1) / B::BY);
+    t.n[2] = (int)((g.shape[2] + B::BX - 1) / B::BX);
     t.total = t.n[0] * t.n[1] * t.n[2];
   }
   return t;
 }
 
-// Node-space origin of tile `t` (interior indices along each internal axis).
+// Interior index of this lane's first node in block `t`; returns false when
+// the lane's row lies outside the grid (lanes stay in warp votes regardless).
 template <int D>
-__device__ inline void tile_origin(const TileGrid& tg, int t, int o[3]) {
+__device__ inline bool lane_nodes(const phj_grid& g, const TileGrid& tg, int t, int lane, int c[3]) {
+  using B = Blk<D>;
+  const int ly = lane / B::LX, lx = lane % B::LX;
   if (D == 2) {
-    int tx = t % tg.n[1], ty = t / tg.n[1];
-    o[0] = ty * Tile<2>::TY;
-    o[1] = tx * Tile<2>::TX;
-    o[2] = 0;
+    const int bx = t % tg.n[1], by = t / tg.n[1];
+    c[0] = by * B::BY + ly;
+    c[1] = bx * B::BX + lx * B::NB;
+    c[2] = 0;
+    return c[0] < g.shape[0];
   } else {
-    int tx = t % tg.n[2];
-    int r = t / tg.n[2];
-    int ty = r % tg.n[1], tz = r / tg.n[1];
-    o[0] = tz * Tile<3>::TZ;
-    o[1] = ty * Tile<3>::TY;
-    o[2] = tx * Tile<3>::TX;
+    const int bx = t % tg.n[2];
+    const int r = t / tg.n[2];
+    const int by = r % tg.n[1], bz = r / tg.n[1];
+    c[0] = bz;
+    c[1] = by * B::BY + ly;
+    c[2] = bx * B::BX + lx * B::NB;
+    return c[1] < g.shape[1];
   }
 }
 
-// Mark the 3^D neighbour tiles of tile `t` active for the next sweep
-// (called by threads 0..3^D-1 of a CTA whose tile changed).
+// Mark the 3^D neighbour blocks of block `t` active for the next sweep
+// (lane nid of a warp whose block changed).
 template <int D>
 __device__ inline void mark_neighbour(const TileGrid& tg, const phj_grid& g, int t, int nid,
                                       int* next_flags, int* next_list, int* next_count) {
@@ -75,7 +83,6 @@ __device__ inline void mark_neighbour(const TileGrid& tg, const phj_grid& g, int
     int d0 = nid / 3 - 1, d1 = nid % 3 - 1;
     int a = c[0] + d0, b = c[1] + d1;
     if (g.periodic[0]) a = (a + n[0]) % n[0];
-    if (g.periodic[1]) b = (b + n[1]) % n[1];
     if (a < 0 || a >= n[0] || b < 0 || b >= n[1]) return;
     int nt = a * n[1] + b;
     if (atomicExch(&next_flags[nt], 1) == 0) next_list[atomicAdd(next_count, 1)] = nt;
@@ -87,8 +94,6 @@ __device__ inline void mark_neighbour(const TileGrid& tg, const phj_grid& g, int
     int d0 = nid / 9 - 1, d1 = (nid / 3) % 3 - 1, d2 = nid % 3 - 1;
     int a = c[0] + d0, b = c[1] + d1, e = c[2] + d2;
     if (g.periodic[0]) a = (a + n[0]) % n[0];
-    if (g.periodic[1]) b = (b + n[1]) % n[1];
-    if (g.periodic[2]) e = (e + n[2]) % n[2];
     if (a < 0 || a >= n[0] || b < 0 || b >= n[1] || e < 0 || e >= n[2]) return;
     int nt = (a * n[1] + b) * n[2] + e;
     if (atomicExch(&next_flags[nt], 1) == 0) next_list[atomicAdd(next_count, 1)] = nt;
@@ -99,7 +104,8 @@ __device__ inline void mark_neighbour(const TileGrid& tg, const phj_grid& g, int
 struct Workspace {
   int* list[2];
   int* flags[2];
-  int* counts;  // [max_sweeps + 1]
+  int* counts;  // [max_sweeps + 2] active blocks per sweep
+  int* take;    // [max_sweeps + 2] dynamic work counters
 };
 
 inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
@@ -109,12 +115,12 @@ inline int64_t workspace_bytes(const phj_grid& g, int max_sweeps) {
   TileGrid tg = make_tile_grid<D>(g);
   int64_t b = 0;
   b += 4 * align_up((int64_t)tg.total * 4, 256);
-  b += align_up((int64_t)(max_sweeps + 2) * 4, 256);
-  return b;  // transport appends max_sweeps doubles after align_up(b, 256)
+  b += 2 * align_up((int64_t)(max_sweeps + 2) * 4, 256);
+  return b;
 }
 
 template <int D>
-inline Workspace carve(const phj_grid& g, void* base) {
+inline Workspace carve(const phj_grid& g, void* base, int max_sweeps) {
   TileGrid tg = make_tile_grid<D>(g);
   char* p = (char*)base;
   Workspace w;
@@ -123,7 +129,8 @@ inline Workspace carve(const phj_grid& g, void* base) {
   w.list[1] = (int*)p; p += tb;
   w.flags[0] = (int*)p; p += tb;
   w.flags[1] = (int*)p; p += tb;
-  w.counts = (int*)p;
+  w.counts = (int*)p; p += align_up((int64_t)(max_sweeps + 2) * 4, 256);
+  w.take = (int*)p;
   return w;
 }
 

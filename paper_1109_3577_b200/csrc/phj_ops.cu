@@ -149,6 +149,29 @@ __global__ void argmax_kernel(phj_grid g, const double* __restrict__ phi, int j,
   }
 }
 
+__global__ void argmax_colors_kernel(phj_grid g, const double* __restrict__ phi, int R,
+                                     double* __restrict__ best_val, int32_t* __restrict__ best_idx) {
+  const int64_t N = n_interior(g);
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < N;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    int c[3];
+    unravel(g, s, c);
+    const int64_t plane = g.ext[0] * g.ext[1] * (g.dim == 3 ? g.ext[2] : 1);
+    const double* v = phi + iflat(g, c);
+    double bv = 0.0;
+    int32_t bi = 0;
+    for (int j = 0; j < R; ++j) {
+      const double x = v[j * plane];
+      if (x > bv) {
+        bv = x;
+        bi = j;
+      }
+    }
+    best_val[s] = bv;
+    best_idx[s] = bi;
+  }
+}
+
 __global__ void codes_kernel(phj_grid g, const double* __restrict__ best_val,
                              const int32_t* __restrict__ best_idx, const uint8_t* __restrict__ mask,
                              const int8_t* __restrict__ kind, int32_t* __restrict__ color) {
@@ -266,24 +289,26 @@ __global__ void finish3_kernel(phj_grid g, const int32_t* __restrict__ color,
 
 // ghost planes of periodic axes <- opposite interior planes (all ext entries)
 template <typename E>
-__global__ void periodic_kernel(phj_grid g, E* v, int ax) {
-  // iterate over the ext array restricted to plane index 0 and M+1 of axis ax
+__global__ void periodic_kernel(phj_grid g, E* v, int ax, int per) {
+  // iterate over the ext array restricted to plane index 0 and M+1 of axis ax;
+  // `per` elements of type E per node (multi-colour fields)
   int64_t plane = 1;
   for (int a = 0; a < g.dim; ++a)
     if (a != ax) plane *= g.ext[a];
   const int64_t M = g.shape[ax];
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < plane;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < plane * per;
        i += (int64_t)gridDim.x * blockDim.x) {
     // decode i over the other axes (C order, skipping ax)
-    int64_t rem = i, f = 0;
+    int64_t rem = i / per, f = 0;
+    const int q = (int)(i % per);
     for (int a = g.dim - 1; a >= 0; --a) {
       if (a == ax) continue;
       const int64_t ca = rem % g.ext[a];
       rem /= g.ext[a];
       f += ca * g.strides[a];
     }
-    v[f + 0 * g.strides[ax]] = v[f + M * g.strides[ax]];
-    v[f + (M + 1) * g.strides[ax]] = v[f + 1 * g.strides[ax]];
+    v[(f + 0 * g.strides[ax]) * per + q] = v[(f + M * g.strides[ax]) * per + q];
+    v[(f + (M + 1) * g.strides[ax]) * per + q] = v[(f + 1 * g.strides[ax]) * per + q];
   }
 }
 
@@ -502,6 +527,19 @@ extern "C" int phj_argmax_update(const phj_grid* g, const double* phi, int32_t j
   return PHJ_OK;
 }
 
+extern "C" int phj_argmax_colors(const phj_grid* g, const double* phi, int32_t n_colors,
+                                 double* best_val, int32_t* best_idx, void* stream) {
+  if (!g || !phi || !best_val || !best_idx || n_colors < 1) {
+    phj_set_error("phj_argmax_colors: bad arguments");
+    return PHJ_ERR_ARG;
+  }
+  argmax_colors_kernel<<<grid_blocks(n_interior(*g)), 256, 0, (cudaStream_t)stream>>>(
+      *g, phi, n_colors, best_val, best_idx);
+  phj_count_launch(1);
+  PHJ_CUDA(cudaGetLastError());
+  return PHJ_OK;
+}
+
 extern "C" int phj_assemble_codes(const phj_grid* g, const double* best_val,
                                   const int32_t* best_idx, const uint8_t* mask, const int8_t* kind,
                                   int32_t* color, void* stream) {
@@ -656,14 +694,21 @@ extern "C" int phj_sync_periodic(const phj_grid* g, int32_t elem_bytes, void* v,
     int64_t plane = 1;
     for (int a = 0; a < g->dim; ++a)
       if (a != ax) plane *= g->ext[a];
+    if (elem_bytes > 8 && elem_bytes % 8 == 0) {
+      const int per = elem_bytes / 8;
+      periodic_kernel<int64_t><<<grid_blocks(plane * per), 256, 0, s>>>(*g, (int64_t*)v, ax, per);
+      phj_count_launch(1);
+      continue;
+    }
     const int nb = grid_blocks(plane);
     switch (elem_bytes) {
-      case 1: periodic_kernel<uint8_t><<<nb, 256, 0, s>>>(*g, (uint8_t*)v, ax); phj_count_launch(1); break;
-      case 2: periodic_kernel<int16_t><<<nb, 256, 0, s>>>(*g, (int16_t*)v, ax); phj_count_launch(1); break;
-      case 4: periodic_kernel<int32_t><<<nb, 256, 0, s>>>(*g, (int32_t*)v, ax); phj_count_launch(1); break;
-      case 8: periodic_kernel<int64_t><<<nb, 256, 0, s>>>(*g, (int64_t*)v, ax); phj_count_launch(1); break;
+      case 1: periodic_kernel<uint8_t><<<nb, 256, 0, s>>>(*g, (uint8_t*)v, ax, 1); break;
+      case 2: periodic_kernel<int16_t><<<nb, 256, 0, s>>>(*g, (int16_t*)v, ax, 1); break;
+      case 4: periodic_kernel<int32_t><<<nb, 256, 0, s>>>(*g, (int32_t*)v, ax, 1); break;
+      case 8: periodic_kernel<int64_t><<<nb, 256, 0, s>>>(*g, (int64_t*)v, ax, 1); break;
       default: phj_set_error("phj_sync_periodic: elem_bytes"); return PHJ_ERR_ARG;
     }
+    phj_count_launch(1);
   }
   PHJ_CUDA(cudaGetLastError());
   return PHJ_OK;

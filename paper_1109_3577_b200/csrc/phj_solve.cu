@@ -5,20 +5,23 @@
 //  * Jacobi iteration with two ext buffers; the whole fixed-point loop runs
 //    inside ONE cooperative persistent launch (grid.sync between sweeps), so
 //    there is no host round trip per sweep (reference loop: solver.py:256-273).
-//  * Work is tiled; a tile is re-swept only if a tile in its 3^D neighbourhood
-//    changed in the previous sweep.  This is exact: a node whose stencil
-//    inputs did not change reproduces its previous value (monotone min).
-//  * Each warp owns 32*NB consecutive nodes of one row, so the stencil class
-//    (Dubins heading = internal axis 0) is warp-uniform; each thread keeps its
-//    NB nodes' 3^D neighbourhood in registers and the per-control corner
-//    weights come from shared memory as warp broadcasts.  Controls are grouped
-//    by foot octant on the host, which makes every register index compile-time.
+//  * Work and activity unit = a warp block (Blk<D>: 4 rows x 32 / 16 nodes).
+//    A block is re-swept only if a block in its 3^D neighbourhood changed in
+//    the previous sweep -- exact: a node whose stencil inputs did not change
+//    reproduces its previous value (monotone min).  Warps fetch active blocks
+//    from the sweep's list with an atomic counter; no CTA barrier inside a
+//    sweep.
+//  * Each lane keeps its NB nodes' 3^D neighbourhood in registers; per-control
+//    corner weights come from shared memory as warp broadcasts.  Controls are
+//    grouped by foot octant on the host, which makes every register index a
+//    compile-time constant; two controls are evaluated per iteration for ILP.
 //  * State constraints (patch solves) are per-node 3^D "foreign" bitmasks; a
-//    warp with no foreign neighbour at all takes the rejection-free path.
+//    warp with no foreign neighbour takes the rejection-free path.
 //  * Per-patch convergence: patch p stops at the first sweep whose max change
 //    over p is <= tol, exactly like one reference solve() per patch
 //    (patchy.py:362-377); later sweeps copy its nodes through unchanged.
 #include <cooperative_groups.h>
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -31,7 +34,7 @@ namespace phj {
 struct SolveParams {
   phj_grid g;
   TileGrid tg;
-  int n_classes, nc;
+  int n_classes, nc, n_real;
   const int32_t* oct_start;
   const uint32_t* nzmask;
   const double* weights;
@@ -87,14 +90,29 @@ __device__ inline void stage_stencil(const StencilSmem<D, T>& s, int ncls, int n
                                      const int32_t* oct_start, const uint32_t* nzmask,
                                      const double* weights, const double* cost) {
   const int nent = ncls * nc;
-  for (int i = threadIdx.x; i < nent * (1 << D); i += blockDim.x) s.w[i] = (T)weights[i];
+  constexpr int NC = 1 << D;
+  for (int i = threadIdx.x; i < nent; i += blockDim.x) {
+    // weights in T with the last nonzero one set so that their sequential
+    // sum in T is exactly 1 (I[1] == 1, see dynamics._weights_for)
+    T w[NC];
+    int last = 0;
+    for (int k = 0; k < NC; ++k) {
+      w[k] = (T)weights[(int64_t)i * NC + k];
+      if (w[k] != T(0)) last = k;
+    }
+    T sum = T(0);
+    for (int k = 0; k < last; ++k) sum = sum + w[k];
+    w[last] = T(1) - sum;
+    for (int k = 0; k < NC; ++k) s.w[(int64_t)i * NC + k] = w[k];
+  }
   for (int i = threadIdx.x; i < nent; i += blockDim.x) {
     s.nz[i] = nzmask[i];
     double c = cost ? cost[i] : 0.0;
     if (RULE == PHJ_RULE_KRUZKOV) {
-      double beta = exp(-c);
-      s.a[i] = (T)beta;
-      s.b[i] = (T)(1.0 - beta);
+      // 1 - beta is exact in T (Sterbenz), so beta * 1 + (1 - beta) == 1
+      const T beta = (T)exp(-c);
+      s.a[i] = beta;
+      s.b[i] = T(1) - beta;
     } else {
       s.a[i] = (T)c;
       s.b[i] = (T)0;
@@ -110,7 +128,7 @@ struct Nbhd {
   T v[NR][NB + 2];
 };
 
-// value of corner k of octant o for node r (all compile-time after unrolling)
+// value of corner K of octant O for node r (compile-time after unrolling)
 template <int D, int NB, int O, int K, typename T>
 __device__ __forceinline__ T corner_val(const Nbhd<D, T, NB>& nb, int r) {
   // internal axis ax: offset = (octant bit ? 0 : -1) + corner bit
@@ -138,6 +156,30 @@ struct CornerSum<D, T, NB, O, (1 << D)> {
   }
 };
 
+// One corner step K of U*NB interleaved interpolation chains.
+template <int D, typename T, int NB, int O, int U, int K>
+struct ChainStep {
+  __device__ __forceinline__ static void run(const Nbhd<D, T, NB>& nb, const T (&w)[U][1 << D],
+                                             T (&acc)[U][NB]) {
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int r = 0; r < NB; ++r) acc[u][r] = fma(w[u][K], corner_val<D, NB, O, K>(nb, r), acc[u][r]);
+    ChainStep<D, T, NB, O, U, K + 1>::run(nb, w, acc);
+  }
+};
+template <int D, typename T, int NB, int O, int U>
+struct ChainStep<D, T, NB, O, U, (1 << D)> {
+  __device__ __forceinline__ static void run(const Nbhd<D, T, NB>&, const T (&)[U][1 << D],
+                                             T (&)[U][NB]) {}
+};
+
+template <int D, typename T, int NB, int O>
+__device__ __forceinline__ T interp(const Nbhd<D, T, NB>& nb, const T* w, int r) {
+  T acc = w[0] * corner_val<D, NB, O, 0>(nb, r);
+  return CornerSum<D, T, NB, O, 1>::run(nb, w, r, acc);
+}
+
 template <typename T, int N>
 __device__ __forceinline__ void load_weights(const T* src, T* w) {
   if constexpr (sizeof(T) == 8 && N % 2 == 0) {
@@ -162,48 +204,123 @@ __device__ __forceinline__ void load_weights(const T* src, T* w) {
   }
 }
 
-// Evaluate all controls of octant O for the NB nodes of this thread.
-// MODE 0: min of the candidate values (sweep); MODE 1: argmin with lowest
-// original index on ties (feedback).
+// Candidate post-processing: per-entry cost (COST_CTRL), the per-candidate
+// rule in feedback mode, and state-constraint rejection.
+template <typename T, int RULE, int COST, bool SLOW, int MODE>
+__device__ __forceinline__ T finish_cand(T acc, T ca, T cb, T ncoef, uint32_t fm, uint32_t nz) {
+  if constexpr (COST == PHJ_COST_CTRL) {
+    acc = (RULE == PHJ_RULE_KRUZKOV) ? fma(ca, acc, cb) : acc + ca;
+  } else if constexpr (MODE == 1) {
+    // feedback applies the rule per candidate (SURVEY App. A hoisting caveat)
+    acc = (RULE == PHJ_RULE_KRUZKOV) ? fma(ncoef, acc, T(1) - ncoef) : acc + ncoef;
+  }
+  if constexpr (SLOW) {
+    if (fm & nz) acc = big_value<T>();
+  }
+  return acc;
+}
+
+// Running minimum of non-negative candidates.  For fp64 the compare runs on
+// the bit patterns as int64 (same order for values >= 0; candidates are
+// convex combinations of non-negative values plus non-negative costs), which
+// keeps the FP64 pipe for the interpolation FMAs; fp32 uses FMNMX.
+#ifndef PHJ_MIN_INT
+#define PHJ_MIN_INT 1
+#endif
+#ifndef PHJ_KUNROLL2
+#define PHJ_KUNROLL2 4
+#endif
+template <typename T>
+struct MinAcc;
+template <>
+struct MinAcc<double> {
+#if PHJ_MIN_INT
+  long long b;
+  __device__ __forceinline__ void init() { b = __double_as_longlong(big_value<double>()); }
+  __device__ __forceinline__ void take(double x) { b = min(b, __double_as_longlong(x)); }
+  __device__ __forceinline__ double get() const { return __longlong_as_double(b); }
+#else
+  double b;
+  __device__ __forceinline__ void init() { b = big_value<double>(); }
+  __device__ __forceinline__ void take(double x) { b = x < b ? x : b; }
+  __device__ __forceinline__ double get() const { return b; }
+#endif
+};
+template <>
+struct MinAcc<float> {
+  float b;
+  __device__ __forceinline__ void init() { b = big_value<float>(); }
+  __device__ __forceinline__ void take(float x) { b = fminf(b, x); }
+  __device__ __forceinline__ float get() const { return b; }
+};
+
+// Argmin with the lowest original control index on ties (feedback mode).
+template <typename T>
+__device__ __forceinline__ void take_arg(T acc, int cidx, T& best, int& bidx) {
+  if (acc < best || (acc == best && cidx < bidx && acc < big_value<T>())) {
+    best = acc;
+    bidx = cidx;
+  }
+}
+
+// Evaluate all controls of octant O for the NB nodes of this lane, U entries
+// per iteration (the host pads every octant group to a multiple of U).
+// MODE 0: min (sweep, into mn); MODE 1: argmin with the lowest original
+// index on ties (feedback, into best/bidx).
 template <int D, typename T, int NB, int RULE, int COST, bool SLOW, int MODE, int O>
 __device__ __forceinline__ void eval_octant(const Nbhd<D, T, NB>& nb, const StencilSmem<D, T>& s,
                                             const int* os, const uint32_t (&fm)[NB],
                                             const T (&ncoef)[NB], const int32_t* ctrl_map,
-                                            T (&best)[NB], int (&bidx)[NB]) {
+                                            MinAcc<T> (&mn)[NB], T (&best)[NB], int (&bidx)[NB]) {
   constexpr int NC = 1 << D;
+  constexpr int U = (D == 2) ? PHJ_KUNROLL2 : PHJ_UNROLL(D);  // divides the host padding
   const int e0 = os[O], e1 = os[O + 1];
-  for (int e = e0; e < e1; ++e) {
-    T w[NC];
-    load_weights<T, NC>(s.w + (int64_t)e * NC, w);
-    T ca = T(0), cb = T(0);
-    if constexpr (COST == PHJ_COST_CTRL) {
-      ca = s.a[e];
-      cb = s.b[e];
+  for (int e = e0; e < e1; e += U) {
+    T w[U][NC];
+#pragma unroll
+    for (int u = 0; u < U; ++u) load_weights<T, NC>(s.w + (int64_t)(e + u) * NC, w[u]);
+    T ca[U], cb[U];
+    uint32_t nz[U];
+    int ci[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      ca[u] = T(0);
+      cb[u] = T(0);
+      nz[u] = 0;
+      ci[u] = 0;
+      if constexpr (COST == PHJ_COST_CTRL) {
+        ca[u] = s.a[e + u];
+        cb[u] = s.b[e + u];
+      }
+      if constexpr (SLOW) nz[u] = s.nz[e + u];
+      if constexpr (MODE == 1) ci[u] = ctrl_map[e + u];
     }
-    uint32_t nz = 0;
-    if constexpr (SLOW) nz = s.nz[e];
-    int cidx = 0;
-    if constexpr (MODE == 1) cidx = ctrl_map[e];
+    // corner-major order: U*NB independent FMA chains advance one corner per
+    // step, so consecutive FP64 instructions never depend on each other
+    // (DFMA latency ~8 cycles, 2-cycle issue per warp on sm_100).
+    T acc[U][NB];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int r = 0; r < NB; ++r) acc[u][r] = w[u][0] * corner_val<D, NB, O, 0>(nb, r);
+    ChainStep<D, T, NB, O, U, 1>::run(nb, w, acc);
 #pragma unroll
     for (int r = 0; r < NB; ++r) {
-      T acc = w[0] * corner_val<D, NB, O, 0>(nb, r);
-      acc = CornerSum<D, T, NB, O, 1>::run(nb, w, r, acc);
-      if constexpr (COST == PHJ_COST_CTRL) {
-        acc = (RULE == PHJ_RULE_KRUZKOV) ? fma(ca, acc, cb) : acc + ca;
-      } else if constexpr (MODE == 1) {
-        // feedback applies the rule per candidate (Appendix A hoisting caveat)
-        acc = (RULE == PHJ_RULE_KRUZKOV) ? fma(ncoef[r], acc, T(1) - ncoef[r]) : acc + ncoef[r];
-      }
-      if constexpr (SLOW) {
-        if (fm[r] & nz) acc = big_value<T>();
-      }
+      T x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        x[u] = finish_cand<T, RULE, COST, SLOW, MODE>(acc[u][r], ca[u], cb[u], ncoef[r], fm[r],
+                                                      nz[u]);
       if constexpr (MODE == 0) {
-        best[r] = acc < best[r] ? acc : best[r];
+        // pairwise tree over the U candidates, one link into the running min
+#pragma unroll
+        for (int st = 1; st < U; st <<= 1)
+#pragma unroll
+          for (int u = 0; u + st < U; u += 2 * st) x[u] = x[u + st] < x[u] ? x[u + st] : x[u];
+        mn[r].take(x[0]);
       } else {
-        if (acc < best[r] || (acc == best[r] && cidx < bidx[r] && acc < big_value<T>())) {
-          best[r] = acc;
-          bidx[r] = cidx;
-        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) take_arg<T>(x[u], ci[u], best[r], bidx[r]);
       }
     }
   }
@@ -214,9 +331,10 @@ struct EvalAll {
   __device__ __forceinline__ static void run(const Nbhd<D, T, NB>& nb, const StencilSmem<D, T>& s,
                                              const int* os, const uint32_t (&fm)[NB],
                                              const T (&ncoef)[NB], const int32_t* ctrl_map,
-                                             T (&best)[NB], int (&bidx)[NB]) {
-    eval_octant<D, T, NB, RULE, COST, SLOW, MODE, O>(nb, s, os, fm, ncoef, ctrl_map, best, bidx);
-    EvalAll<D, T, NB, RULE, COST, SLOW, MODE, O + 1>::run(nb, s, os, fm, ncoef, ctrl_map, best,
+                                             MinAcc<T> (&mn)[NB], T (&best)[NB], int (&bidx)[NB]) {
+    eval_octant<D, T, NB, RULE, COST, SLOW, MODE, O>(nb, s, os, fm, ncoef, ctrl_map, mn, best,
+                                                     bidx);
+    EvalAll<D, T, NB, RULE, COST, SLOW, MODE, O + 1>::run(nb, s, os, fm, ncoef, ctrl_map, mn, best,
                                                          bidx);
   }
 };
@@ -224,29 +342,9 @@ template <int D, typename T, int NB, int RULE, int COST, bool SLOW, int MODE>
 struct EvalAll<D, T, NB, RULE, COST, SLOW, MODE, (1 << D)> {
   __device__ __forceinline__ static void run(const Nbhd<D, T, NB>&, const StencilSmem<D, T>&,
                                              const int*, const uint32_t (&)[NB], const T (&)[NB],
-                                             const int32_t*, T (&)[NB], int (&)[NB]) {}
+                                             const int32_t*, MinAcc<T> (&)[NB], T (&)[NB],
+                                             int (&)[NB]) {}
 };
-
-// Thread -> row mapping inside a tile.  Returns false if the warp's row is
-// outside the grid (warp-uniform: callers use full-mask warp votes after it;
-// lanes past the end of the row are masked per node instead).  c[] receives
-// the interior index of the thread's first node.
-template <int D>
-__device__ inline bool thread_row(const phj_grid& g, const int o[3], int c[3]) {
-  using TL = Tile<D>;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if constexpr (D == 2) {
-    c[0] = o[0] + warp;
-    c[1] = o[1] + lane * TL::NB;
-    c[2] = 0;
-    return c[0] < g.shape[0];
-  } else {
-    c[0] = o[0] + warp / TL::TY;
-    c[1] = o[1] + warp % TL::TY;
-    c[2] = o[2] + lane * TL::NB;
-    return c[0] < g.shape[0] && c[1] < g.shape[1];
-  }
-}
 
 template <int D>
 __device__ inline int64_t ext_flat(const phj_grid& g, const int c[3]) {
@@ -266,7 +364,7 @@ __device__ __forceinline__ void load_nbhd(const phj_grid& g, const T* __restrict
                                           Nbhd<D, T, NB>& nb) {
   constexpr int last = D - 1;
   const int64_t xmax = g.ext[last] - 1;
-  const int64_t x0 = c[last];  // ext index of the column left of node 0 = c + 1 - 1
+  const int64_t x0 = c[last];  // ext index of the column left of node 0
   if constexpr (D == 2) {
 #pragma unroll
     for (int dy = 0; dy < 3; ++dy) {
@@ -293,71 +391,76 @@ __device__ inline void atomic_max_change(unsigned long long* addr, T ch) {
   atomicMax(addr, dbits((double)ch));
 }
 
-// One tile of the value sweep.  Returns true if any node changed.
+// One block of the value sweep, processed by one warp.  Returns (warp-
+// uniform) whether any node changed.
 template <int D, typename T, int RULE, int COST>
-__device__ bool sweep_tile(const SolveParams& p, const StencilSmem<D, T>& s, int tile,
-                           const T* __restrict__ vin, T* __restrict__ vout, const int* s_done,
-                           unsigned long long* s_max, unsigned long long* gmax_row,
-                           unsigned long long& evals) {
-  using TL = Tile<D>;
-  constexpr int NB = TL::NB;
+__device__ bool sweep_block(const SolveParams& p, const StencilSmem<D, T>& s, int blk,
+                            const T* __restrict__ vin, T* __restrict__ vout, const int* s_done,
+                            unsigned long long* s_max, unsigned long long* gmax_row,
+                            unsigned long long& evals) {
+  constexpr int NB = Blk<D>::NB;
   constexpr int last = D - 1;
+  const unsigned FULL = 0xffffffffu;
   const phj_grid& g = p.g;
-  int o[3], c[3];
-  tile_origin<D>(p.tg, tile, o);
-  if (!thread_row<D>(g, o, c)) return false;  // whole row outside (warp-uniform)
+  const int lane = threadIdx.x & 31;
+  int c[3];
+  const bool row_ok = lane_nodes<D>(g, p.tg, blk, lane, c);
   const int64_t f0 = ext_flat<D>(g, c);
   const int cls = p.n_classes > 1 ? c[0] : 0;
   const int* os = s.oct + cls * ((1 << D) + 1);
-  const int nadm = os[1 << D] - os[0];
+  const int nadm = p.n_real;
 
-  // per-node classification
+  // Issue every per-node load of the block up front (labels, coefficients,
+  // foreign masks, the 3^D value neighbourhood) so their latencies overlap;
+  // out-of-range lanes read a clamped in-bounds address and are masked.
+  const int64_t nlast = (int64_t)g.ext[0] * g.strides[0] - 1;
   int labv[NB];
-  bool comp[NB], copy[NB];
   uint32_t fm[NB];
   T ncoef[NB];
-  bool any_comp = false;
+  bool in[NB];
 #pragma unroll
   for (int r = 0; r < NB; ++r) {
-    const bool in = c[last] + r < g.shape[last];
-    labv[r] = in ? (int)p.lab[f0 + r] : -1;
+    in[r] = row_ok && c[last] + r < g.shape[last];
+    const int64_t fr = min(f0 + r, nlast);
+    labv[r] = p.lab[fr];
+    fm[r] = p.fmask[fr];
+    ncoef[r] = (COST == PHJ_COST_NODE && p.coef) ? ((const T*)p.coef)[fr] : (T)p.coef0;
+  }
+  Nbhd<D, T, NB> nb;
+  load_nbhd<D, T, NB>(g, vin, c, nb);
+  bool comp[NB], copy[NB];
+  bool any_comp = false, any_copy = false;
+#pragma unroll
+  for (int r = 0; r < NB; ++r) {
+    if (!in[r]) labv[r] = -1;
     comp[r] = false;
     copy[r] = false;
-    fm[r] = 0;
-    ncoef[r] = (T)p.coef0;
     if (labv[r] >= 0) {
-      if (s_done[labv[r]] != 0x7fffffff) {
+      if (s_done[labv[r]] != 0x7fffffff || (COST == PHJ_COST_NODE && ncoef[r] < T(0))) {
         copy[r] = true;
       } else {
-        if (COST == PHJ_COST_NODE && p.coef) ncoef[r] = ((const T*)p.coef)[f0 + r];
-        if (ncoef[r] < T(0) && COST == PHJ_COST_NODE) {
-          copy[r] = true;
-        } else {
-          comp[r] = true;
-          fm[r] = p.fmask[f0 + r];
-          any_comp = true;
-        }
+        comp[r] = true;
+        any_comp = true;
       }
     }
+    if (!comp[r]) fm[r] = 0;
+    any_copy |= copy[r];
   }
-  const unsigned FULL = 0xffffffffu;
-  const bool warp_comp = __any_sync(FULL, any_comp);
   bool changed = false;
   T mych[NB];
 #pragma unroll
   for (int r = 0; r < NB; ++r) mych[r] = T(0);
-
   const int64_t M0 = g.shape[0];
   const bool per0 = g.periodic[0] != 0;
   const int64_t ghost_shift = M0 * g.strides[0];
 
-  if (warp_comp) {
-    Nbhd<D, T, NB> nb;
-    load_nbhd<D, T, NB>(g, vin, c, nb);
+  if (__any_sync(FULL, any_comp)) {
+    MinAcc<T> mn[NB];
     T best[NB];
     int bidx[NB];
 #pragma unroll
     for (int r = 0; r < NB; ++r) {
+      mn[r].init();
       best[r] = big_value<T>();
       bidx[r] = 0;
     }
@@ -365,9 +468,11 @@ __device__ bool sweep_tile(const SolveParams& p, const StencilSmem<D, T>& s, int
 #pragma unroll
     for (int r = 0; r < NB; ++r) fmo |= fm[r];
     if (__any_sync(FULL, fmo != 0))
-      EvalAll<D, T, NB, RULE, COST, true, 0>::run(nb, s, os, fm, ncoef, nullptr, best, bidx);
+      EvalAll<D, T, NB, RULE, COST, true, 0>::run(nb, s, os, fm, ncoef, nullptr, mn, best, bidx);
     else
-      EvalAll<D, T, NB, RULE, COST, false, 0>::run(nb, s, os, fm, ncoef, nullptr, best, bidx);
+      EvalAll<D, T, NB, RULE, COST, false, 0>::run(nb, s, os, fm, ncoef, nullptr, mn, best, bidx);
+#pragma unroll
+    for (int r = 0; r < NB; ++r) best[r] = mn[r].get();
     constexpr int CR = (D == 2) ? 1 : 4;  // centre row of the register block
 #pragma unroll
     for (int r = 0; r < NB; ++r) {
@@ -393,12 +498,12 @@ __device__ bool sweep_tile(const SolveParams& p, const StencilSmem<D, T>& s, int
         else if (c[0] == M0 - 1) vout[f0 + r - ghost_shift] = nv;
       }
     }
-  } else {
-    // copy-through only (done patches / degenerate nodes)
+  } else if (any_copy) {
+    constexpr int CR = (D == 2) ? 1 : 4;
 #pragma unroll
     for (int r = 0; r < NB; ++r) {
       if (!copy[r]) continue;
-      const T old = vin[f0 + r];
+      const T old = nb.v[CR][r + 1];
       vout[f0 + r] = old;
       if (per0) {
         if (c[0] == 0) vout[f0 + r + ghost_shift] = old;
@@ -408,12 +513,16 @@ __device__ bool sweep_tile(const SolveParams& p, const StencilSmem<D, T>& s, int
   }
 
   // per-patch max change
-  if (__any_sync(FULL, changed)) {
-    const int lane = threadIdx.x & 31;
-    int l0 = __shfl_sync(FULL, labv[0], 0);
+  const bool wchanged = __any_sync(FULL, changed);
+  if (wchanged) {
+    int l0 = -1;
+#pragma unroll
+    for (int r = 0; r < NB; ++r)
+      if (mych[r] > T(0)) l0 = labv[r];
+    const int lref = __reduce_max_sync(FULL, l0);
     bool uni = true;
 #pragma unroll
-    for (int r = 0; r < NB; ++r) uni &= (mych[r] == T(0)) || (labv[r] == l0);
+    for (int r = 0; r < NB; ++r) uni &= (mych[r] == T(0)) || (labv[r] == lref);
     if (__all_sync(FULL, uni)) {
       T m = T(0);
 #pragma unroll
@@ -421,8 +530,8 @@ __device__ bool sweep_tile(const SolveParams& p, const StencilSmem<D, T>& s, int
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) m = max(m, __shfl_xor_sync(FULL, m, off));
       if (lane == 0 && m > T(0)) {
-        if (p.R <= kSmemPatchReduce) atomic_max_change(&s_max[l0], m);
-        else atomic_max_change(&gmax_row[l0], m);
+        if (p.R <= kSmemPatchReduce) atomic_max_change(&s_max[lref], m);
+        else atomic_max_change(&gmax_row[lref], m);
       }
     } else {
 #pragma unroll
@@ -434,11 +543,11 @@ __device__ bool sweep_tile(const SolveParams& p, const StencilSmem<D, T>& s, int
       }
     }
   }
-  return changed;
+  return wchanged;
 }
 
 template <int D, typename T, int RULE, int COST>
-__global__ void __launch_bounds__(kThreads, 1) solve_kernel(const __grid_constant__ SolveParams p) {
+__global__ void __launch_bounds__(kThreads, 2) solve_kernel(const __grid_constant__ SolveParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   cg::grid_group grid = cg::this_grid();
   StencilSmem<D, T> s = carve_stencil<D, T>(smem, p.n_classes, p.nc);
@@ -449,8 +558,10 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const __grid_constan
     s_done[i] = (p.mine == nullptr || p.mine[i]) ? 0x7fffffff : 0;
   __syncthreads();
 
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
   unsigned long long evals = 0;
-  int tiles = 0;
+  int blocks_done = 0;
   int sw = 0, buf = 0;
   const int nshared = min(p.R, kSmemPatchReduce);
   for (;;) {
@@ -462,17 +573,25 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const __grid_constan
     int* nxt_flags = p.ws.flags[(sw + 1) & 1];
     int* nxt_list = p.ws.list[(sw + 1) & 1];
     int* nxt_cnt = &p.ws.counts[sw + 1];
+    int* take = &p.ws.take[sw];
     unsigned long long* gmax_row = p.maxch + (int64_t)sw * p.R;
     for (int i = threadIdx.x; i < nshared; i += blockDim.x) s_max[i] = 0ull;
     __syncthreads();
-    for (int li = blockIdx.x; li < cnt; li += gridDim.x) {
-      const int t = __ldcg(&list[li]);
-      if (threadIdx.x == 0) cur_flags[t] = 0;
-      bool ch = sweep_tile<D, T, RULE, COST>(p, s, t, vin, vout, s_done, s_max, gmax_row, evals);
-      const int any = __syncthreads_or(ch);
-      ++tiles;
-      if (any && threadIdx.x < (D == 2 ? 9 : 27))
-        mark_neighbour<D>(p.tg, p.g, t, threadIdx.x, nxt_flags, nxt_list, nxt_cnt);
+    int item = 0;
+    if (lane == 0) item = atomicAdd(take, 1);
+    item = __shfl_sync(FULL, item, 0);
+    while (item < cnt) {
+      // claim the next block now; its index is only needed after this one
+      int nxt_l0 = 0;
+      if (lane == 0) nxt_l0 = atomicAdd(take, 1);
+      const int blk = __ldcg(&list[item]);
+      if (lane == 0) cur_flags[blk] = 0;
+      const bool ch = sweep_block<D, T, RULE, COST>(p, s, blk, vin, vout, s_done, s_max, gmax_row,
+                                                    evals);
+      ++blocks_done;
+      if (ch && lane < (D == 2 ? 9 : 27))
+        mark_neighbour<D>(p.tg, p.g, blk, lane, nxt_flags, nxt_list, nxt_cnt);
+      item = __shfl_sync(FULL, nxt_l0, 0);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < nshared; i += blockDim.x)
@@ -491,7 +610,6 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const __grid_constan
     const int any_pending = __syncthreads_or(pending);
     if (!any_pending || sw >= p.max_sweeps) break;
   }
-  // results
   if (blockIdx.x == 0) {
     for (int i = threadIdx.x; i < p.R; i += blockDim.x) {
       const int d = s_done[i];
@@ -502,38 +620,40 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const __grid_constan
       p.info[1] = buf;
     }
   }
-  // block-reduce evals / tiles
   __shared__ unsigned long long s_ev;
-  __shared__ int s_tiles;
+  __shared__ int s_blk;
   if (threadIdx.x == 0) {
     s_ev = 0;
-    s_tiles = 0;
+    s_blk = 0;
   }
   __syncthreads();
   atomicAdd(&s_ev, evals);
-  if (threadIdx.x == 0) s_tiles = tiles;
+  if (lane == 0) atomicAdd(&s_blk, blocks_done);
   __syncthreads();
   if (threadIdx.x == 0) {
     atomicAdd(p.evals, s_ev);
-    atomicAdd(&p.info[2], s_tiles);
+    atomicAdd(&p.info[2], s_blk);
   }
 }
 
-// Initial active tile list: every tile holding a node of a patch to sweep.
+// Initial active block list: every block holding a node to sweep (solve:
+// label >= 0 of a mine patch; transport: a mover).  One warp per block.
 template <int D>
 __global__ void build_list_kernel(phj_grid g, TileGrid tg, const int16_t* __restrict__ lab,
                                   const uint8_t* __restrict__ mine, int* flags, int* list,
                                   int* count, int want_movers, const int32_t* __restrict__ fb,
                                   const int8_t* __restrict__ kind) {
-  using TL = Tile<D>;
-  const int t = blockIdx.x;
-  int o[3], c[3];
-  tile_origin<D>(tg, t, o);
+  constexpr int NB = Blk<D>::NB;
+  const int lane = threadIdx.x & 31;
+  const int blk = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  if (blk >= tg.total) return;  // whole warp
+  int c[3];
+  const bool row_ok = lane_nodes<D>(g, tg, blk, lane, c);
   bool any = false;
-  if (thread_row<D>(g, o, c)) {
+  if (row_ok) {
     const int64_t f0 = ext_flat<D>(g, c);
     const int64_t s0 = serial_of<D>(g, c);
-    for (int r = 0; r < TL::NB; ++r) {
+    for (int r = 0; r < NB; ++r) {
       if (c[D - 1] + r >= g.shape[D - 1]) break;
       if (want_movers) {
         any |= fb[s0 + r] >= 0 && kind[s0 + r] == 0;
@@ -543,14 +663,22 @@ __global__ void build_list_kernel(phj_grid g, TileGrid tg, const int16_t* __rest
       }
     }
   }
-  if (__syncthreads_or(any) && threadIdx.x == 0) {
-    flags[t] = 1;
-    list[atomicAdd(count, 1)] = t;
+  if (__any_sync(0xffffffffu, any) && lane == 0) {
+    flags[blk] = 1;
+    list[atomicAdd(count, 1)] = blk;
   }
 }
 
 // ---------------------------------------------------------------------------
 // colour transport (patchy.py:183-219): phi_i <- I[phi](x_i + h f(x_i, a*_i))
+//
+// All R colours in one launch, phi stored colour-major ([R][ext] planes) so
+// a warp's reads of one corner of one colour are contiguous.  Each lane owns
+// NB nodes of the warp block; a mover's foot cell (entry -> octant, weights)
+// is resolved once per block and all 2^D x R corner loads are independent.
+// Colour j stops at the first sweep whose max |change| over colour j is
+// <= tol (one reference transport_color loop per colour); afterwards it is
+// copied through.
 
 struct TransportParams {
   phj_grid g;
@@ -562,44 +690,58 @@ struct TransportParams {
   double* phi[2];
   const int32_t* fb;
   const int8_t* kind;
+  const int32_t* ent;  // per internal serial: stencil entry of the mover's feedback, or -1
+  int R;
+  int64_t plane;       // ext nodes per colour plane
   double tol;
   int max_sweeps;
   Workspace ws;
-  unsigned long long* maxch;  // [max_sweeps]
+  unsigned long long* maxch;  // [max_sweeps * R], double bits
+  int32_t* color_sweeps;      // [R]
   int32_t* info;
   unsigned long long* updates;
 };
 
 template <int D>
-__global__ void __launch_bounds__(kThreads, 1) transport_kernel(const __grid_constant__ TransportParams p) {
-  using TL = Tile<D>;
+__global__ void __launch_bounds__(kThreads, 2) transport_kernel(const __grid_constant__ TransportParams p) {
+  using B = Blk<D>;
   constexpr int NC = 1 << D;
-  constexpr int NB = TL::NB;
+  constexpr int NB = B::NB;
   constexpr int last = D - 1;
   extern __shared__ __align__(16) unsigned char smem[];
   cg::grid_group grid = cg::this_grid();
   const int nent = p.n_classes * p.nc;
-  double* s_w = (double*)smem;                  // [nent][NC]
-  int* s_inv = (int*)(s_w + (int64_t)nent * NC);  // [ncls][nc] ctrl -> entry
-  signed char* s_oct = (signed char*)(s_inv + nent);  // [nent]
+  const int R = p.R;
+  double* s_w = (double*)smem;                                                  // [nent][NC]
+  unsigned long long* s_max = (unsigned long long*)(s_w + (int64_t)nent * NC);  // [R]
+  int* s_done = (int*)(s_max + R);                                              // [R]
+  signed char* s_oct = (signed char*)(s_done + R);                              // [nent]
   for (int i = threadIdx.x; i < nent * NC; i += blockDim.x) s_w[i] = p.weights[i];
-  for (int i = threadIdx.x; i < nent; i += blockDim.x) s_inv[i] = -1;
-  __syncthreads();
+  for (int i = threadIdx.x; i < R; i += blockDim.x) s_done[i] = 0x7fffffff;
   for (int cls = 0; cls < p.n_classes; ++cls) {
     const int32_t* os = p.oct_start + cls * (NC + 1);
     for (int e = os[0] + threadIdx.x; e < os[NC]; e += blockDim.x) {
       int oc = 0;
       while (oc < NC - 1 && e >= os[oc + 1]) ++oc;
       s_oct[e] = (signed char)oc;
-      s_inv[cls * p.nc + p.ctrl[e]] = e;
     }
   }
   __syncthreads();
+  const unsigned FULL = 0xffffffffu;
   const phj_grid& g = p.g;
+  const int lane = threadIdx.x & 31;
   const int64_t M0 = g.shape[0];
   const bool per0 = g.periodic[0] != 0;
   const int64_t ghost_shift = M0 * g.strides[0];
-  __shared__ unsigned long long s_mx;
+  int64_t coff[NC];  // corner offsets from the lower corner (bit ax = +stride_ax)
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    int64_t o = 0;
+#pragma unroll
+    for (int ax = 0; ax < D; ++ax)
+      if ((k >> ax) & 1) o += g.strides[ax];
+    coff[k] = o;
+  }
   unsigned long long upd = 0;
   int sw = 0, buf = 0;
   for (;;) {
@@ -608,75 +750,108 @@ __global__ void __launch_bounds__(kThreads, 1) transport_kernel(const __grid_con
     const int cnt = ld_cg(&p.ws.counts[sw]);
     const int* list = p.ws.list[sw & 1];
     int* cur_flags = p.ws.flags[sw & 1];
-    if (threadIdx.x == 0) s_mx = 0ull;
+    int* take = &p.ws.take[sw];
+    for (int i = threadIdx.x; i < R; i += blockDim.x) s_max[i] = 0ull;
     __syncthreads();
-    for (int li = blockIdx.x; li < cnt; li += gridDim.x) {
-      const int t = __ldcg(&list[li]);
-      if (threadIdx.x == 0) cur_flags[t] = 0;
-      int o[3], c[3];
-      tile_origin<D>(p.tg, t, o);
+    int item = 0;
+    if (lane == 0) item = atomicAdd(take, 1);
+    item = __shfl_sync(FULL, item, 0);
+    while (item < cnt) {
+      int nxt_l0 = 0;
+      if (lane == 0) nxt_l0 = atomicAdd(take, 1);
+      const int blk = __ldcg(&list[item]);
+      if (lane == 0) cur_flags[blk] = 0;
+      int c[3];
+      const bool row_ok = lane_nodes<D>(g, p.tg, blk, lane, c);
+      const int64_t f0 = ext_flat<D>(g, c);
+      const int64_t s0 = serial_of<D>(g, c);
+      int e[NB];
+      int64_t base[NB];
+      double w[NB][NC];
+      bool any = false;
+#pragma unroll
+      for (int r = 0; r < NB; ++r) {
+        const bool in = row_ok && c[last] + r < g.shape[last];
+        e[r] = in ? __ldg(&p.ent[s0 + r]) : -1;
+        base[r] = f0 + r;
+        if (e[r] >= 0) {
+          const int oc = s_oct[e[r]];
+#pragma unroll
+          for (int ax = 0; ax < D; ++ax)
+            if (!((oc >> ax) & 1)) base[r] -= g.strides[ax];
+#pragma unroll
+          for (int k = 0; k < NC; ++k) w[r][k] = s_w[(int64_t)e[r] * NC + k];
+          any = true;
+          ++upd;
+        }
+      }
       bool changed = false;
-      double m = 0.0;
-      if (thread_row<D>(g, o, c)) {
-        const int64_t f0 = ext_flat<D>(g, c);
-        const int64_t s0 = serial_of<D>(g, c);
-        const int cls = p.n_classes > 1 ? c[0] : 0;
-        for (int r = 0; r < NB; ++r) {
-          if (c[last] + r >= g.shape[last]) break;
-          const int a = p.fb[s0 + r];
-          if (a < 0 || p.kind[s0 + r] != 0) continue;
-          const int e = s_inv[cls * p.nc + a];
-          if (e < 0) continue;
-          const int oc = s_oct[e];
-          const int64_t f = f0 + r;
-          double v = 0.0;
+      if (__any_sync(FULL, any)) {
+        for (int j = 0; j < R; ++j) {
+          const bool live = s_done[j] == 0x7fffffff;
+          const double* pj = pin + (int64_t)j * p.plane;
+          double* qj = pout + (int64_t)j * p.plane;
+          double lmax = 0.0;
+          double acc[NB], old[NB];
 #pragma unroll
-          for (int k = 0; k < NC; ++k) {
-            const double w = s_w[(int64_t)e * NC + k];
-            if (w != 0.0) {
-              int64_t off = 0;
+          for (int r = 0; r < NB; ++r) {
+            acc[r] = 0.0;
+            old[r] = 0.0;
+            if (e[r] >= 0) {
+              old[r] = pj[f0 + r];
 #pragma unroll
-              for (int ax = 0; ax < D; ++ax) {
-                const int oa = (((oc >> ax) & 1) ? 0 : -1) + ((k >> ax) & 1);
-                off += (int64_t)oa * g.strides[ax];
-              }
-              v = fma(w, pin[f + off], v);
+              for (int k = 0; k < NC; ++k) acc[r] = fma(w[r][k], pj[base[r] + coff[k]], acc[r]);
             }
           }
-          const double ch = fabs(pin[f] - v);
-          pout[f] = v;
-          if (per0) {
-            if (c[0] == 0) pout[f + ghost_shift] = v;
-            else if (c[0] == M0 - 1) pout[f - ghost_shift] = v;
+#pragma unroll
+          for (int r = 0; r < NB; ++r) {
+            if (e[r] < 0) continue;
+            const double nv = live ? acc[r] : old[r];
+            lmax = fmax(lmax, fabs(old[r] - nv));
+            qj[f0 + r] = nv;
+            if (per0) {
+              if (c[0] == 0) qj[f0 + r + ghost_shift] = nv;
+              else if (c[0] == M0 - 1) qj[f0 + r - ghost_shift] = nv;
+            }
           }
-          ++upd;
-          if (ch > 0.0) {
+          if (__any_sync(FULL, lmax > 0.0)) {
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) lmax = fmax(lmax, __shfl_xor_sync(FULL, lmax, off));
+            if (lane == 0) atomicMax(&s_max[j], dbits(lmax));
             changed = true;
-            m = fmax(m, ch);
           }
         }
       }
-      if (m > 0.0) atomicMax(&s_mx, dbits(m));
-      const int any = __syncthreads_or(changed);
-      if (any && threadIdx.x < (D == 2 ? 9 : 27))
-        mark_neighbour<D>(p.tg, g, t, threadIdx.x, p.ws.flags[(sw + 1) & 1],
-                          p.ws.list[(sw + 1) & 1], &p.ws.counts[sw + 1]);
+      if (changed && lane < (D == 2 ? 9 : 27))
+        mark_neighbour<D>(p.tg, g, blk, lane, p.ws.flags[(sw + 1) & 1], p.ws.list[(sw + 1) & 1],
+                          &p.ws.counts[sw + 1]);
+      item = __shfl_sync(FULL, nxt_l0, 0);
     }
     __syncthreads();
-    if (threadIdx.x == 0 && s_mx) atomicMax(&p.maxch[sw], s_mx);
+    unsigned long long* grow = p.maxch + (int64_t)sw * R;
+    for (int i = threadIdx.x; i < R; i += blockDim.x)
+      if (s_max[i]) atomicMax(&grow[i], s_max[i]);
     grid.sync();
-    const double mc = __longlong_as_double((long long)ld_cg(&p.maxch[sw]));
     ++sw;
     buf ^= 1;
-    if (mc <= p.tol) {
-      if (blockIdx.x == 0 && threadIdx.x == 0) p.info[2] = 1;
-      break;
+    int pending = 0;
+    for (int i = threadIdx.x; i < R; i += blockDim.x) {
+      if (s_done[i] == 0x7fffffff) {
+        const double mc = __longlong_as_double((long long)ld_cg(&grow[i]));
+        if (mc <= p.tol) s_done[i] = sw;
+        else pending = 1;
+      }
     }
-    if (sw >= p.max_sweeps) break;
+    const int any_pending = __syncthreads_or(pending);
+    if (!any_pending || sw >= p.max_sweeps) break;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    p.info[0] = sw;
-    p.info[1] = buf;
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i < R; i += blockDim.x)
+      p.color_sweeps[i] = (s_done[i] == 0x7fffffff) ? -sw : s_done[i];
+    if (threadIdx.x == 0) {
+      p.info[0] = sw;
+      p.info[1] = buf;
+    }
   }
   __shared__ unsigned long long s_up;
   if (threadIdx.x == 0) s_up = 0;
@@ -686,13 +861,41 @@ __global__ void __launch_bounds__(kThreads, 1) transport_kernel(const __grid_con
   if (threadIdx.x == 0) atomicAdd(p.updates, s_up);
 }
 
+// Mover -> stencil entry of its feedback control (patchy.py:165-180: movers
+// are free nodes with a defined feedback and an admissible foot).
+template <int D>
+__global__ void transport_entries_kernel(phj_grid g, int ncls, int nc,
+                                         const int32_t* __restrict__ oct_start,
+                                         const int32_t* __restrict__ ctrl,
+                                         const int32_t* __restrict__ fb,
+                                         const int8_t* __restrict__ kind, int32_t* __restrict__ ent) {
+  extern __shared__ int s_inv[];  // [ncls][nc]
+  constexpr int NC = 1 << D;
+  for (int i = threadIdx.x; i < ncls * nc; i += blockDim.x) s_inv[i] = -1;
+  __syncthreads();
+  for (int cls = 0; cls < ncls; ++cls) {
+    const int32_t* os = oct_start + cls * (NC + 1);
+    for (int e = os[0] + threadIdx.x; e < os[NC]; e += blockDim.x) s_inv[cls * nc + ctrl[e]] = e;
+    __syncthreads();
+  }
+  const int64_t N = g.shape[0] * g.shape[1] * (D == 3 ? g.shape[2] : 1);
+  const int64_t plane = N / g.shape[0];
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < N;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int a = fb[s];
+    int e = -1;
+    if (a >= 0 && a < nc && kind[s] == 0) e = s_inv[(ncls > 1 ? (int)(s / plane) : 0) * nc + a];
+    ent[s] = e;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // feedback (extract_feedback, solver.py:413-443; feedback_batch _kernels.py:109-167)
 
 struct FeedbackParams {
   phj_grid g;
   TileGrid tg;
-  int n_classes, nc;
+  int n_classes, nc, n_real;
   const int32_t* oct_start;
   const int32_t* ctrl;
   const uint32_t* nzmask;
@@ -710,8 +913,7 @@ struct FeedbackParams {
 
 template <int D, typename T, int RULE, int COST>
 __global__ void __launch_bounds__(kThreads) feedback_kernel(const __grid_constant__ FeedbackParams p) {
-  using TL = Tile<D>;
-  constexpr int NB = TL::NB;
+  constexpr int NB = Blk<D>::NB;
   constexpr int last = D - 1;
   extern __shared__ __align__(16) unsigned char smem[];
   StencilSmem<D, T> s = carve_stencil<D, T>(smem, p.n_classes, p.nc);
@@ -720,24 +922,25 @@ __global__ void __launch_bounds__(kThreads) feedback_kernel(const __grid_constan
   for (int i = threadIdx.x; i < p.n_classes * p.nc; i += blockDim.x) s_ctrl[i] = p.ctrl[i];
   __syncthreads();
   const phj_grid& g = p.g;
+  const int lane = threadIdx.x & 31;
   unsigned long long ev = 0;
-  for (int t = blockIdx.x; t < p.tg.total; t += gridDim.x) {
-    int o[3], c[3];
-    tile_origin<D>(p.tg, t, o);
-    if (!thread_row<D>(g, o, c)) continue;
+  const T* v = (const T*)p.v;
+  for (int blk = blockIdx.x * kWarps + (threadIdx.x >> 5); blk < p.tg.total;
+       blk += gridDim.x * kWarps) {
+    int c[3];
+    const bool row_ok = lane_nodes<D>(g, p.tg, blk, lane, c);
     const int64_t f0 = ext_flat<D>(g, c);
     const int64_t s0 = serial_of<D>(g, c);
     const int cls = p.n_classes > 1 ? c[0] : 0;
     const int* os = s.oct + cls * ((1 << D) + 1);
-    const int nadm = os[1 << D] - os[0];
+    const int nadm = p.n_real;
     bool comp[NB];
     uint32_t fm[NB];
     T ncoef[NB];
     bool any = false;
-    const T* v = (const T*)p.v;
 #pragma unroll
     for (int r = 0; r < NB; ++r) {
-      const bool in = c[last] + r < g.shape[last];
+      const bool in = row_ok && c[last] + r < g.shape[last];
       comp[r] = false;
       fm[r] = 0;
       ncoef[r] = (T)p.coef0;
@@ -755,6 +958,7 @@ __global__ void __launch_bounds__(kThreads) feedback_kernel(const __grid_constan
     if (!__any_sync(0xffffffffu, any)) continue;
     Nbhd<D, T, NB> nb;
     load_nbhd<D, T, NB>(g, v, c, nb);
+    MinAcc<T> mn[NB];
     T best[NB];
     int bidx[NB];
 #pragma unroll
@@ -762,7 +966,7 @@ __global__ void __launch_bounds__(kThreads) feedback_kernel(const __grid_constan
       best[r] = big_value<T>();
       bidx[r] = 0x7fffffff;
     }
-    EvalAll<D, T, NB, RULE, COST, true, 1>::run(nb, s, os, fm, ncoef, s_ctrl, best, bidx);
+    EvalAll<D, T, NB, RULE, COST, true, 1>::run(nb, s, os, fm, ncoef, s_ctrl, mn, best, bidx);
 #pragma unroll
     for (int r = 0; r < NB; ++r) {
       if (!comp[r]) continue;
@@ -842,11 +1046,11 @@ extern "C" int64_t phj_solve_workspace_bytes(const phj_grid* g, int32_t n_patche
                                              int32_t max_sweeps) {
   (void)n_patches;
   if (!g) return -1;
-  const int64_t b =
-      g->dim == 2 ? workspace_bytes<2>(*g, max_sweeps) : workspace_bytes<3>(*g, max_sweeps);
-  return align_up(b, 256) + 8 * (int64_t)max_sweeps;  // + transport change history
+  return g->dim == 2 ? workspace_bytes<2>(*g, max_sweeps) : workspace_bytes<3>(*g, max_sweeps);
 }
 
+// Cooperative persistent launch: as many CTAs as are co-resident, capped by
+// the work (8 warps per CTA, one block per warp per step).
 template <typename K>
 static int coop_launch(K kernel, int want_blocks, size_t smem, void** args, cudaStream_t stream,
                        int* launched) {
@@ -875,6 +1079,7 @@ static int solve_impl(const phj_solve_args* a) {
   p.tg = make_tile_grid<D>(a->grid);
   p.n_classes = a->st.n_classes;
   p.nc = a->st.n_controls;
+  p.n_real = a->st.n_real;
   p.oct_start = a->st.oct_start;
   p.nzmask = a->st.nzmask;
   p.weights = a->st.weights;
@@ -889,7 +1094,7 @@ static int solve_impl(const phj_solve_args* a) {
   p.max_sweeps = a->max_sweeps;
   p.mine = a->mine;
   p.tol = a->tol;
-  p.ws = carve<D>(a->grid, a->workspace);
+  p.ws = carve<D>(a->grid, a->workspace, a->max_sweeps);
   p.maxch = (unsigned long long*)a->maxch_hist;
   p.patch_sweeps = a->patch_sweeps;
   p.evals = a->evals;
@@ -900,14 +1105,16 @@ static int solve_impl(const phj_solve_args* a) {
                            stream));
   PHJ_CUDA(cudaMemsetAsync(a->evals, 0, sizeof(unsigned long long), stream));
   PHJ_CUDA(cudaMemsetAsync(a->info, 0, 4 * sizeof(int32_t), stream));
-  build_list_kernel<D><<<p.tg.total, kThreads, 0, stream>>>(
-      p.g, p.tg, p.lab, p.mine, p.ws.flags[0], p.ws.list[0], p.ws.counts, 0, nullptr, nullptr); phj_count_launch(1);
+  build_list_kernel<D><<<(p.tg.total + kWarps - 1) / kWarps, kThreads, 0, stream>>>(
+      p.g, p.tg, p.lab, p.mine, p.ws.flags[0], p.ws.list[0], p.ws.counts, 0, nullptr, nullptr);
+  phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   size_t smem = (size_t)StencilSmem<D, T>::bytes(p.n_classes, p.nc) +
                 (size_t)((p.R + 1) / 2 * 2) * 4 + (size_t)std::min(p.R, kSmemPatchReduce) * 8 + 16;
   void* args[] = {(void*)&p};
   int launched = 0;
-  int rc = coop_launch(solve_kernel<D, T, RULE, COST>, p.tg.total, smem, args, stream, &launched);
+  int rc = coop_launch(solve_kernel<D, T, RULE, COST>, (p.tg.total + kWarps - 1) / kWarps, smem,
+                       args, stream, &launched);
   if (rc) return rc;
   PHJ_CUDA(cudaGetLastError());
   return PHJ_OK;
@@ -925,6 +1132,10 @@ extern "C" int phj_solve(const phj_solve_args* a) {
   }
   if (a->grid.periodic[1] || a->grid.periodic[2]) {
     phj_set_error("phj_solve: only internal axis 0 may be periodic");
+    return PHJ_ERR_UNSUPPORTED;
+  }
+  if (a->grid.dim == 2 && a->st.n_classes != 1) {
+    phj_set_error("phj_solve: stencil classes need a 3D grid (class axis = internal axis 0)");
     return PHJ_ERR_UNSUPPORTED;
   }
   if (a->rule == PHJ_RULE_REF && a->dtype == PHJ_F32) {
@@ -969,36 +1180,55 @@ static int transport_impl(const phj_transport_args* a) {
   p.phi[1] = a->phi1;
   p.fb = a->fb;
   p.kind = a->kind;
+  p.ent = a->ent_scratch;
+  p.R = a->n_colors;
+  p.plane = a->grid.ext[0] * a->grid.ext[1] * (D == 3 ? a->grid.ext[2] : 1);
   p.tol = a->tol;
   p.max_sweeps = a->max_sweeps;
-  p.ws = carve<D>(a->grid, a->workspace);
-  const int64_t ws_bytes = workspace_bytes<D>(a->grid, a->max_sweeps);
-  // maxch history lives after the workspace proper
-  p.maxch = (unsigned long long*)((char*)a->workspace + align_up(ws_bytes, 256));
+  p.ws = carve<D>(a->grid, a->workspace, a->max_sweeps);
+  p.maxch = (unsigned long long*)a->maxch_hist;
+  p.color_sweeps = a->color_sweeps;
   p.info = a->info;
   p.updates = a->updates;
-  PHJ_CUDA(cudaMemsetAsync(a->workspace, 0, align_up(ws_bytes, 256) + 8 * (size_t)a->max_sweeps,
-                           stream));
+  const int64_t ws_bytes = workspace_bytes<D>(a->grid, a->max_sweeps);
+  PHJ_CUDA(cudaMemsetAsync(a->workspace, 0, ws_bytes, stream));
+  PHJ_CUDA(cudaMemsetAsync(a->maxch_hist, 0, 8 * (size_t)a->max_sweeps * p.R, stream));
   PHJ_CUDA(cudaMemsetAsync(a->info, 0, 4 * sizeof(int32_t), stream));
   PHJ_CUDA(cudaMemsetAsync(a->updates, 0, sizeof(unsigned long long), stream));
-  build_list_kernel<D><<<p.tg.total, kThreads, 0, stream>>>(
-      p.g, p.tg, nullptr, nullptr, p.ws.flags[0], p.ws.list[0], p.ws.counts, 1, p.fb, p.kind); phj_count_launch(1);
+  {
+    const int64_t N = p.g.shape[0] * p.g.shape[1] * (D == 3 ? p.g.shape[2] : 1);
+    const int nb = (int)std::min<int64_t>((N + 255) / 256, 16 * phj_num_sms());
+    const size_t sm = (size_t)p.n_classes * p.nc * 4;
+    auto k = transport_entries_kernel<D>;
+    PHJ_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k<<<std::max(nb, 1), 256, sm, stream>>>(p.g, p.n_classes, p.nc, p.oct_start, p.ctrl, p.fb,
+                                            p.kind, a->ent_scratch);
+    phj_count_launch(1);
+  }
+  build_list_kernel<D><<<(p.tg.total + kWarps - 1) / kWarps, kThreads, 0, stream>>>(
+      p.g, p.tg, nullptr, nullptr, p.ws.flags[0], p.ws.list[0], p.ws.counts, 1, p.fb, p.kind);
+  phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   const int nent = p.n_classes * p.nc;
-  size_t smem = (size_t)nent * (1 << D) * 8 + (size_t)nent * 4 + (size_t)nent + 16;
+  size_t smem = (size_t)nent * (1 << D) * 8 + (size_t)p.R * 12 + (size_t)nent + 16;
   void* args[] = {(void*)&p};
-  return coop_launch(transport_kernel<D>, p.tg.total, smem, args, stream, nullptr);
+  return coop_launch(transport_kernel<D>, (p.tg.total + kWarps - 1) / kWarps, smem, args, stream,
+                     nullptr);
 }
 
 extern "C" int phj_transport(const phj_transport_args* a) {
-  if (!a || !a->phi0 || !a->phi1 || !a->fb || !a->kind || !a->workspace || !a->info ||
-      !a->updates || a->max_sweeps < 1) {
+  if (!a || !a->phi0 || !a->phi1 || !a->fb || !a->kind || !a->ent_scratch || !a->workspace ||
+      !a->info || !a->updates || a->max_sweeps < 1) {
     phj_set_error("phj_transport: missing argument");
     return PHJ_ERR_ARG;
   }
   if (a->grid.periodic[1] || a->grid.periodic[2]) {
     phj_set_error("phj_transport: only internal axis 0 may be periodic");
     return PHJ_ERR_UNSUPPORTED;
+  }
+  if (a->n_colors < 1 || a->n_colors > 4096 || !a->maxch_hist || !a->color_sweeps) {
+    phj_set_error("phj_transport: n_colors must be in [1, 4096]");
+    return PHJ_ERR_ARG;
   }
   return a->grid.dim == 2 ? transport_impl<2>(a) : transport_impl<3>(a);
 }
@@ -1013,6 +1243,7 @@ static int feedback_impl(const phj_grid* g, const phj_stencil* st, const void* v
   p.tg = make_tile_grid<D>(*g);
   p.n_classes = st->n_classes;
   p.nc = st->n_controls;
+  p.n_real = st->n_real;
   p.oct_start = st->oct_start;
   p.ctrl = st->ctrl;
   p.nzmask = st->nzmask;
@@ -1030,8 +1261,9 @@ static int feedback_impl(const phj_grid* g, const phj_stencil* st, const void* v
                 (size_t)p.n_classes * p.nc * 4 + 16;
   auto k = feedback_kernel<D, T, RULE, COST>;
   PHJ_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int blocks = std::min(p.tg.total, 8 * phj_num_sms());
-  k<<<blocks, kThreads, smem, stream>>>(p); phj_count_launch(1);
+  int blocks = std::min((p.tg.total + kWarps - 1) / kWarps, 8 * phj_num_sms());
+  k<<<blocks, kThreads, smem, stream>>>(p);
+  phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   return PHJ_OK;
 }
@@ -1046,6 +1278,10 @@ extern "C" int phj_feedback(const phj_grid* g, const phj_stencil* st, int32_t dt
   }
   if (rule == PHJ_RULE_REF && dtype == PHJ_F32) {
     phj_set_error("phj_feedback: the reference (sentinel) rule is fp64 only");
+    return PHJ_ERR_UNSUPPORTED;
+  }
+  if (g->dim == 2 && st->n_classes != 1) {
+    phj_set_error("phj_feedback: stencil classes need a 3D grid");
     return PHJ_ERR_UNSUPPORTED;
   }
   cudaStream_t s = (cudaStream_t)stream;
@@ -1079,7 +1315,8 @@ static int fmask_launch(const phj_grid* g, const int16_t* lab, const uint8_t* ha
   int blocks = (int)std::min<int64_t>((N + 255) / 256, 32 * phj_num_sms());
   if (blocks < 1) blocks = 1;
   if (g->dim == 2) fmask_kernel<2><<<blocks, 256, 0, s>>>(*g, lab, hard, fmask);
-  else fmask_kernel<3><<<blocks, 256, 0, s>>>(*g, lab, hard, fmask); phj_count_launch(1);
+  else fmask_kernel<3><<<blocks, 256, 0, s>>>(*g, lab, hard, fmask);
+  phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   return PHJ_OK;
 }

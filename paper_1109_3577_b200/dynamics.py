@@ -96,6 +96,7 @@ class StencilSet:
     weights: np.ndarray    # float64 [ncls * nc, 2^d]
     cost: np.ndarray       # float64 [ncls * nc]
     disp: np.ndarray       # float64 [ncls, nc, d] internal grid units (diagnostics)
+    n_real: int = 0        # admissible controls per class (before padding)
 
 
 @dataclass
@@ -144,20 +145,35 @@ def _weights_for(disp: np.ndarray):
             pos = pos * 3 + (off + 1)
         if w[k] != 0.0:
             nz |= 1 << pos
+    # Make the left-to-right floating-point sum of the weights exactly 1 (the
+    # kernels accumulate corners in this order): I[1] == 1 keeps unreached
+    # Kruzkov nodes (v = 1) and pure colour regions (phi = 1) bit-stable, so
+    # they never look "changed" to the activity tracking.  The adjustment is
+    # at most an ulp of the last nonzero weight.
+    last = max(k for k in range(2 ** d) if w[k] != 0.0)
+    s = 0.0
+    for k in range(last):
+        s = s + float(w[k])
+    w[last] = 1.0 - s
     return octant, w, nz
+
+
+def unroll(dim: int) -> int:
+    """Entries per kernel inner-loop iteration (PHJ_UNROLL in include/phj.h)."""
+    return 4 if dim == 2 else 2
 
 
 def build_stencil(disp: np.ndarray, cost: Optional[np.ndarray], admissible: np.ndarray,
                   cost_mode: int, perm: tuple) -> StencilSet:
     """disp [ncls, nc, d] internal grid units; cost [ncls, nc] or None;
-    admissible [ncls, nc] bool."""
+    admissible [ncls, nc] bool.  Each octant group is padded to a multiple of
+    unroll(d) entries by repeating its last entry (same value, same control
+    index: neither the min nor the lowest-index argmin changes)."""
     ncls, nc, d = disp.shape
     noct = 2 ** d
-    oct_start = np.zeros((ncls, noct + 1), dtype=np.int32)
-    ctrl = np.zeros(ncls * nc, dtype=np.int32)
-    nzm = np.zeros(ncls * nc, dtype=np.uint32)
-    wts = np.zeros((ncls * nc, noct))
-    cst = np.zeros(ncls * nc)
+    U = unroll(d)
+    per_cls = []
+    n_real = 0
     for cls in range(ncls):
         info = []
         for c in range(nc):
@@ -166,21 +182,36 @@ def build_stencil(disp: np.ndarray, cost: Optional[np.ndarray], admissible: np.n
             o, w, nz = _weights_for(disp[cls, c])
             info.append((o, c, w, nz))
         info.sort(key=lambda e: (e[0], e[1]))  # octant, then original order
-        base = cls * nc
-        pos = base
+        groups = []
+        for o in range(noct):
+            g = [e for e in info if e[0] == o]
+            if g:
+                g = g + [g[-1]] * ((-len(g)) % U)
+            groups.append(g)
+        per_cls.append(groups)
+        n_real = max(n_real, len(info))
+    # slots >= the control count, so (class, control) -> entry maps index in range
+    slots = max(1, nc, max(sum(len(g) for g in groups) for groups in per_cls))
+    oct_start = np.zeros((ncls, noct + 1), dtype=np.int32)
+    ctrl = np.zeros(ncls * slots, dtype=np.int32)
+    nzm = np.zeros(ncls * slots, dtype=np.uint32)
+    wts = np.zeros((ncls * slots, noct))
+    cst = np.zeros(ncls * slots)
+    for cls, groups in enumerate(per_cls):
+        pos = cls * slots
         for o in range(noct):
             oct_start[cls, o] = pos
-            for (oo, c, w, nz) in info:
-                if oo != o:
-                    continue
+            for (_, c, w, nz) in groups[o]:
                 ctrl[pos] = c
                 nzm[pos] = nz
                 wts[pos] = w
                 cst[pos] = cost[cls, c] if cost is not None else 0.0
                 pos += 1
         oct_start[cls, noct] = pos
-    return StencilSet(d, ncls, nc, cost_mode, tuple(perm), oct_start, ctrl, nzm, wts, cst,
-                      disp.copy())
+    st = StencilSet(d, ncls, slots, cost_mode, tuple(perm), oct_start, ctrl, nzm, wts, cst,
+                    disp.copy())
+    st.n_real = n_real
+    return st
 
 
 def _unit_norm(A: np.ndarray) -> float:

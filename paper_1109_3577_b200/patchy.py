@@ -37,6 +37,9 @@ TARGET = -2
 OBSTACLE = -3
 UNCOVERED = -4
 
+#: last transport launch diagnostics (kernel ms, active blocks per sweep)
+TRANSPORT_DIAG: dict = {}
+
 
 @dataclass
 class PatchyConfig:
@@ -183,17 +186,22 @@ def lift_internal(cplan: StencilPlan, vc: torch.Tensor, fplan: StencilPlan, rule
     return vf
 
 
-def transport_internal(plan: StencilPlan, fb_int: torch.Tensor, part_flat: torch.Tensor,
+def transport_internal(plan: StencilPlan, fb_int: torch.Tensor, parts_flat: Sequence,
                        tol: float, max_sweeps: int):
-    """One colour, Jacobi to max|change| <= tol.  Returns (phi internal ext,
-    sweeps, updates, converged)."""
+    """All colours in one launch, each Jacobi to its own max|change| <= tol.
+    ``parts_flat``: per colour, internal ext flat indices of its part.
+    Returns (phi [R][ext] tensor, R, per-colour sweeps, updates)."""
     lib = _lib.load()
-    phi0 = torch.zeros(plan.int_ext, dtype=torch.float64, device=plan.device)
-    phi0.view(-1)[part_flat] = 1.0
-    _sync_periodic(plan, phi0)
+    R = len(parts_flat)
+    phi0 = torch.zeros((R,) + plan.int_ext, dtype=torch.float64, device=plan.device)
+    for j, pf in enumerate(parts_flat):
+        phi0[j].view(-1)[pf] = 1.0
+        _sync_periodic(plan, phi0[j])
     phi1 = phi0.clone()
     wsb = lib.phj_solve_workspace_bytes(ctypes_ref(plan.gs), 1, max_sweeps)
     ws = torch.empty(int(wsb), dtype=torch.uint8, device=plan.device)
+    mc = torch.zeros(max_sweeps * R, dtype=torch.float64, device=plan.device)
+    csw = torch.zeros(R, dtype=torch.int32, device=plan.device)
     info = torch.zeros(4, dtype=torch.int32, device=plan.device)
     upd = torch.zeros(1, dtype=torch.int64, device=plan.device)
     a = _lib.TransportArgs()
@@ -203,33 +211,62 @@ def transport_internal(plan: StencilPlan, fb_int: torch.Tensor, part_flat: torch
     a.phi1 = _lib.ptr(phi1)
     a.fb = _lib.ptr(fb_int)
     a.kind = _lib.ptr(plan.kind)
+    ent = torch.empty(plan.grid.n_interior, dtype=torch.int32, device=plan.device)
+    a.ent_scratch = _lib.ptr(ent)
+    a.n_colors = R
     a.tol = tol
     a.max_sweeps = max_sweeps
     a.workspace = _lib.ptr(ws)
+    a.maxch_hist = _lib.ptr(mc)
+    a.color_sweeps = _lib.ptr(csw)
     a.info = _lib.ptr(info)
     a.updates = _lib.ptr(upd)
     a.stream = _lib.stream_handle()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
     _lib.check(lib.phj_transport(ctypes_ref(a)), "phj_transport")
+    e1.record()
     ih = info.cpu().numpy()
     phi = phi1 if int(ih[1]) == 1 else phi0
-    return phi, int(ih[0]), int(upd.item()), bool(ih[2])
+    from .solver import active_blocks_per_sweep
+
+    TRANSPORT_DIAG["kernel_ms"] = e0.elapsed_time(e1)
+    TRANSPORT_DIAG["block_counts"] = active_blocks_per_sweep(plan, ws, max_sweeps, int(ih[0]))
+    return phi, R, [int(x) for x in csw.cpu().tolist()], int(upd.item())
 
 
-def assemble_internal(plan_or_grid, gs, phis, mask_serial: Optional[torch.Tensor],
-                      kind_serial: torch.Tensor, n_serial: int, device, warnings=None):
-    """Running argmax (strict >) + codes + majority repair + fallback +
-    boundary + solve labels (patchy.py:236-301).  `phis` yields (j, phi ext)
-    in the layout described by `gs`.  Returns (color, n_colors, n_uncovered,
-    boundary, lab)."""
+def argmax_stream(gs, phis, n_serial: int, device):
+    """Running argmax over streamed single-colour fields (patchy.py:251-256)."""
     lib = _lib.load()
-    stream = _lib.stream_handle()
     best_val = torch.zeros(n_serial, dtype=torch.float64, device=device)
     best_idx = torch.zeros(n_serial, dtype=torch.int32, device=device)
     n_colors = 0
     for j, phi in phis:
-        _lib.check(lib.phj_argmax_update(ctypes_ref(gs), _lib.ptr(phi), int(j), _lib.ptr(best_val),
-                                         _lib.ptr(best_idx), stream), "argmax")
+        _lib.check(lib.phj_argmax_update(ctypes_ref(gs), _lib.ptr(phi), int(j),
+                                         _lib.ptr(best_val), _lib.ptr(best_idx),
+                                         _lib.stream_handle()), "argmax")
         n_colors = max(n_colors, int(j) + 1)
+    return best_val, best_idx, n_colors
+
+
+def argmax_batched(gs, phi: torch.Tensor, R: int, n_serial: int, device):
+    lib = _lib.load()
+    best_val = torch.empty(n_serial, dtype=torch.float64, device=device)
+    best_idx = torch.empty(n_serial, dtype=torch.int32, device=device)
+    _lib.check(lib.phj_argmax_colors(ctypes_ref(gs), _lib.ptr(phi), R, _lib.ptr(best_val),
+                                     _lib.ptr(best_idx), _lib.stream_handle()), "argmax")
+    return best_val, best_idx
+
+
+def assemble_internal(gs, best_val: torch.Tensor, best_idx: torch.Tensor, n_colors: int,
+                      mask_serial: Optional[torch.Tensor], kind_serial: torch.Tensor,
+                      n_serial: int, device, warnings=None):
+    """Codes + majority repair + fallback + boundary + solve labels
+    (patchy.py:258-300) after the argmax.  Returns (color, n_uncovered,
+    boundary, lab)."""
+    lib = _lib.load()
+    stream = _lib.stream_handle()
     color = torch.empty(n_serial, dtype=torch.int32, device=device)
     mask_u8 = None if mask_serial is None else mask_serial.to(torch.uint8).contiguous()
     _lib.check(lib.phj_assemble_codes(ctypes_ref(gs), _lib.ptr(best_val), _lib.ptr(best_idx),
@@ -254,7 +291,7 @@ def assemble_internal(plan_or_grid, gs, phis, mask_serial: Optional[torch.Tensor
         warnings.append(f"{n_unc} reachable nodes reached by no color; folded into patch 0")
     if any(gs.periodic[i] for i in range(gs.dim)):
         _lib.check(lib.phj_sync_periodic(ctypes_ref(gs), 2, _lib.ptr(lab), stream), "sync")
-    return color, n_colors, n_unc, boundary, lab
+    return color, n_unc, boundary, lab
 
 
 def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Tensor,
@@ -284,6 +321,8 @@ def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Te
     performed = 0
     kernel_ms = 0.0
     sweeps_total = 0
+    tiles_total = 0
+    block_counts = None
     if pcfg.bc_mode == STATE_CONSTRAINT:
         fmask = plan.fmask_from_labels(lab)
         res = device_solve(plan, work, lab, fmask, n_patches, rule=rule, dtype=dtype, tol=cfg.tol,
@@ -292,6 +331,8 @@ def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Te
         performed = res.evals
         kernel_ms += res.device_ms
         sweeps_total = int(res.info[0])
+        tiles_total = int(res.info[2])
+        block_counts = res.block_counts
         for j in range(n_patches):
             if mine is not None and not bool(mine[j]):
                 stats.append(SweepStats())
@@ -343,7 +384,8 @@ def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Te
     oi.copy_(torch.where(blocked, torch.full_like(oi, unr), oi))
     _sync_periodic(plan, out)
     return out, stats, warnings, {"performed": performed, "kernel_ms": kernel_ms,
-                                  "sweeps": sweeps_total}
+                                  "sweeps": sweeps_total, "tiles": tiles_total,
+                                  "block_counts": block_counts}
 
 
 # -- public API (reference signatures, user layout) -----------------------------------
@@ -397,9 +439,11 @@ def transport_color(spec: ProblemSpec, grid: Grid, feedback: FeedbackField, part
                                                      dtype=torch.int32)).contiguous()
     part_flat = plan.user_serials_to_internal_flat(np.asarray(part_serials, dtype=np.int64))
     limit = max_sweeps if max_sweeps is not None else 10 * max(grid.shape)
-    phi, sweeps, upd, ok = transport_internal(plan, fb_int, part_flat, color_tol, limit)
-    warning = None if ok else (f"color transport: no convergence after {sweeps} sweeps "
-                               f"(color_tol {color_tol:.1e})")
+    phi, _, csw, upd = transport_internal(plan, fb_int, [part_flat], color_tol, limit)
+    sweeps = abs(csw[0])
+    warning = None if csw[0] > 0 else (f"color transport: no convergence after {sweeps} sweeps "
+                                       f"(color_tol {color_tol:.1e})")
+    phi = phi.view(plan.int_ext)
     return NodeField(grid, plan.to_user(phi), sentinel=SENTINEL), sweeps, upd, warning
 
 
@@ -421,8 +465,9 @@ def assemble_patches(color_fields, mask, grid: Grid, *, kind, warnings: Optional
             vals = phi.values if isinstance(phi, NodeField) else phi
             yield j, torch.as_tensor(vals, device=dev, dtype=torch.float64).contiguous()
 
-    color, n_colors, n_unc, boundary, _ = assemble_internal(
-        None, gs, stream(), mask_t, kind_t, grid.n_interior, dev, warnings)
+    best_val, best_idx, n_colors = argmax_stream(gs, stream(), grid.n_interior, dev)
+    color, n_unc, boundary, _ = assemble_internal(gs, best_val, best_idx, n_colors, mask_t,
+                                                  kind_t, grid.n_interior, dev, warnings)
     unc = np.empty(0, dtype=np.int64)
     if n_unc:
         unc = np.arange(n_unc)  # count-only; serials are not tracked on the device
@@ -498,24 +543,23 @@ def run_patchy(spec: ProblemSpec, pcfg: PatchyConfig, cfg: Optional[SolverConfig
             thr = unreach_threshold(rule) if ut is None else (
                 ut if rule == "reference" else float(-np.expm1(-ut)))
             mask = plan_interior_serial(fplan, vf) >= thr
-        parts = _resolve_parts(pcfg, spec, fine_grid)
+        parts = _resolve_parts(pcfg, spec, fine_grid, fplan)
         limit = pcfg.transport_max_sweeps or 10 * max(fine_grid.shape)
-
-        def colours():
-            for j, part in enumerate(parts):
-                pf = fplan.user_serials_to_internal_flat(part)
-                phi, sw, upd, ok = transport_internal(fplan, fb, pf, pcfg.color_tol, limit)
-                stats.transport_updates += upd
-                transport_sweeps.append(sw)
-                if not ok:
-                    stats.warnings.append(f"color {j}: color transport: no convergence after "
-                                          f"{sw} sweeps (color_tol {pcfg.color_tol:.1e})")
-                yield j, phi
-
-        color, n_colors, n_unc, boundary, lab = assemble_internal(
-            fplan, fplan.gs, colours(), mask, fplan.kind, fine_grid.n_interior, fplan.device,
-            stats.warnings)
-        n_colors = max(n_colors, len(parts))
+        parts_flat = [fplan.user_serials_to_internal_flat(p) for p in parts]
+        phi, _, csw, upd = transport_internal(fplan, fb, parts_flat, pcfg.color_tol, limit)
+        stats.transport_updates += upd
+        transport_sweeps = [abs(x) for x in csw]
+        for j, x in enumerate(csw):
+            if x <= 0:
+                stats.warnings.append(f"color {j}: color transport: no convergence after "
+                                      f"{abs(x)} sweeps (color_tol {pcfg.color_tol:.1e})")
+        n_colors = len(parts)
+        best_val, best_idx = argmax_batched(fplan.gs, phi, n_colors, fine_grid.n_interior,
+                                            fplan.device)
+        del phi
+        color, n_unc, boundary, lab = assemble_internal(
+            fplan.gs, best_val, best_idx, n_colors, mask, fplan.kind, fine_grid.n_interior,
+            fplan.device, stats.warnings)
     with stats.phase("patch_solve"):
         out, pstats, warnings, pinfo = solve_patches_internal(
             fplan, color, lab, n_colors, pcfg, cfg, vf)
@@ -546,9 +590,29 @@ def plan_interior_serial(plan: StencilPlan, w: torch.Tensor) -> torch.Tensor:
     return plan.interior_int(w).reshape(-1)
 
 
-def _resolve_parts(pcfg: PatchyConfig, spec: ProblemSpec, grid: Grid):
+def _resolve_parts(pcfg: PatchyConfig, spec: ProblemSpec, grid: Grid, plan=None):
+    """Target partition; the target serials come from the device
+    classification so only target points are formed on the host (cached on
+    the plan)."""
+    if pcfg.parts is not None and not callable(pcfg.parts):
+        return [np.asarray(p, dtype=np.int64) for p in pcfg.parts]
+    key = ("parts", id(pcfg.parts), pcfg.n_patches)
+    cache = getattr(plan, "_parts_cache", None) if plan is not None else None
+    if cache is not None and key in cache:
+        return cache[key]
+    serials = None
+    if plan is not None:
+        kind_user = plan.serial_to_user(plan.kind)
+        serials = torch.nonzero(kind_user == KIND_TARGET).view(-1).cpu().numpy()
     if pcfg.parts is None:
-        return partition_target(spec.target, grid, pcfg.n_patches)
-    if callable(pcfg.parts):
-        return pcfg.parts(spec.target, grid)
-    return [np.asarray(p, dtype=np.int64) for p in pcfg.parts]
+        parts = partition_target(spec.target, grid, pcfg.n_patches, serials=serials)
+    else:
+        try:
+            parts = pcfg.parts(spec.target, grid, serials=serials)
+        except TypeError:
+            parts = pcfg.parts(spec.target, grid)
+    if plan is not None:
+        if cache is None:
+            plan._parts_cache = cache = {}
+        cache[key] = parts
+    return parts

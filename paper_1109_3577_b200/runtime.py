@@ -18,6 +18,11 @@ import torch
 
 from .grid import ConfigurationError
 
+import os
+
+#: PHJ_SYNC_PHASES=1 times phases by host wall clock around device syncs
+_SYNC_PHASES = os.environ.get("PHJ_SYNC_PHASES", "0") == "1"
+
 SERIAL = "serial"
 METHOD1 = "method1"
 METHOD2 = "method2"
@@ -69,7 +74,17 @@ class RunStats:
 
     @contextmanager
     def phase(self, name: str):
-        if torch.cuda.is_available():
+        if _SYNC_PHASES and torch.cuda.is_available():
+            import time
+
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            try:
+                yield
+            finally:
+                torch.cuda.synchronize()
+                self.phases[name] = self.phases.get(name, 0.0) + time.perf_counter() - t0
+        elif torch.cuda.is_available():
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             a.record()

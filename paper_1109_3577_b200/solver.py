@@ -152,7 +152,7 @@ class StencilPlan:
         self.d_nz = torch.as_tensor(st.nzmask.view(np.int32), device=dev)
         self.d_w = torch.as_tensor(st.weights.ravel(), dtype=torch.float64, device=dev)
         self.d_cost = torch.as_tensor(st.cost, dtype=torch.float64, device=dev)
-        self.n_adm = int(st.oct_start[0, -1] - st.oct_start[0, 0])
+        self.n_adm = int(st.n_real)
         self.kind = self._classify(lib)
         # hard base = ghost + obstacle (solver.py:111-126); periodic ghosts copy
         hard = torch.ones(self.int_ext, dtype=torch.uint8, device=dev)
@@ -263,7 +263,8 @@ class StencilPlan:
 
     def stencil_struct(self) -> _lib.Stencil:
         st = self.stencils
-        return _lib.Stencil(st.dim, st.n_classes, st.nc, st.cost_mode, _lib.ptr(self.d_oct),
+        return _lib.Stencil(st.dim, st.n_classes, st.nc, st.cost_mode, int(st.n_real), 0,
+                            _lib.ptr(self.d_oct),
                             _lib.ptr(self.d_ctrl), _lib.ptr(self.d_nz), _lib.ptr(self.d_w),
                             _lib.ptr(self.d_cost))
 
@@ -373,6 +374,7 @@ class DeviceSolveResult:
     evals: int
     info: np.ndarray
     device_ms: float = 0.0
+    block_counts: Optional[np.ndarray] = None
 
 
 def device_solve(plan: StencilPlan, work: torch.Tensor, lab: torch.Tensor, fmask: torch.Tensor,
@@ -420,7 +422,22 @@ def device_solve(plan: StencilPlan, work: torch.Tensor, lab: torch.Tensor, fmask
     out = DeviceSolveResult(res, ps.cpu().numpy(), mc.view(max_sweeps, n_patches).cpu().numpy(),
                             int(ev.item()), info_h)
     out.device_ms = e0.elapsed_time(e1)
+    out.block_counts = active_blocks_per_sweep(plan, ws, max_sweeps, int(info_h[0]))
     return out
+
+
+def active_blocks_per_sweep(plan: StencilPlan, ws: torch.Tensor, max_sweeps: int, sweeps: int):
+    """Active warp blocks per sweep from the solve workspace (diagnostics;
+    layout of carve() in csrc/phj_common.cuh)."""
+    g = plan.gs
+    if g.dim == 2:
+        total = -(-g.shape[0] // 4) * -(-g.shape[1] // 32)
+    else:
+        total = g.shape[0] * -(-g.shape[1] // 4) * -(-g.shape[2] // 16)
+    tb = -(-total * 4 // 256) * 256
+    off = 4 * tb
+    counts = ws[off: off + 4 * (max_sweeps + 2)].view(torch.int32)
+    return counts[:sweeps].cpu().numpy()
 
 
 def stats_for_patch(res: DeviceSolveResult, p: int, n_nodes: int, n_adm: int, tol: float,
