@@ -154,6 +154,9 @@ typedef struct phj_transport_args {
   int32_t* ent_scratch; /* [interior nodes] int32 scratch (mover -> stencil entry) */
   int32_t n_colors;
   double tol;
+  double act_eps;       /* a block re-activates its neighbours for colour j only
+                           when some node of it changed colour j by more than
+                           this (0 = exact Jacobi activity) */
   int32_t max_sweeps;
   void* workspace;      /* phj_solve_workspace_bytes(g, 1, max_sweeps) */
   double* maxch_hist;   /* out [max_sweeps][n_colors] */

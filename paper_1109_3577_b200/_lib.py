@@ -54,7 +54,7 @@ class SolveArgs(ctypes.Structure):
 
 class TransportArgs(ctypes.Structure):
     _fields_ = [("grid", Grid), ("st", Stencil), ("phi0", P), ("phi1", P), ("fb", P),
-                ("kind", P), ("ent_scratch", P), ("n_colors", I32), ("tol", D),
+                ("kind", P), ("ent_scratch", P), ("n_colors", I32), ("tol", D), ("act_eps", D),
                 ("max_sweeps", I32), ("workspace", P), ("maxch_hist", P), ("color_sweeps", P),
                 ("info", P), ("updates", P), ("stream", P)]
 

@@ -100,12 +100,36 @@ __device__ inline void mark_neighbour(const TileGrid& tg, const phj_grid& g, int
   }
 }
 
+// Colour-mask variant (transport): OR the changed colours into the
+// neighbour's next-sweep mask; the first setter appends the block.
+template <int D>
+__device__ inline void mark_neighbour_mask(const TileGrid& tg, const phj_grid& g, int t, int nid,
+                                           unsigned long long bits, unsigned long long* next_mask,
+                                           int* next_list, int* next_count) {
+  int n[3] = {tg.n[0], tg.n[1], tg.n[2]};
+  int nt;
+  if (D == 2) {
+    int a = t / n[1] + nid / 3 - 1, b = t % n[1] + nid % 3 - 1;
+    if (g.periodic[0]) a = (a + n[0]) % n[0];
+    if (a < 0 || a >= n[0] || b < 0 || b >= n[1]) return;
+    nt = a * n[1] + b;
+  } else {
+    const int r = t / n[2];
+    int a = r / n[1] + nid / 9 - 1, b = r % n[1] + (nid / 3) % 3 - 1, e = t % n[2] + nid % 3 - 1;
+    if (g.periodic[0]) a = (a + n[0]) % n[0];
+    if (a < 0 || a >= n[0] || b < 0 || b >= n[1] || e < 0 || e >= n[2]) return;
+    nt = (a * n[1] + b) * n[2] + e;
+  }
+  if (atomicOr(&next_mask[nt], bits) == 0ull) next_list[atomicAdd(next_count, 1)] = nt;
+}
+
 // Workspace carve-up shared by solve/transport.
 struct Workspace {
   int* list[2];
   int* flags[2];
   int* counts;  // [max_sweeps + 2] active blocks per sweep
   int* take;    // [max_sweeps + 2] dynamic work counters
+  unsigned long long* cmask[2];  // transport: per-block active-colour masks
 };
 
 inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
@@ -116,6 +140,7 @@ inline int64_t workspace_bytes(const phj_grid& g, int max_sweeps) {
   int64_t b = 0;
   b += 4 * align_up((int64_t)tg.total * 4, 256);
   b += 2 * align_up((int64_t)(max_sweeps + 2) * 4, 256);
+  b += 2 * align_up((int64_t)tg.total * 8, 256);
   return b;
 }
 
@@ -130,7 +155,9 @@ inline Workspace carve(const phj_grid& g, void* base, int max_sweeps) {
   w.flags[0] = (int*)p; p += tb;
   w.flags[1] = (int*)p; p += tb;
   w.counts = (int*)p; p += align_up((int64_t)(max_sweeps + 2) * 4, 256);
-  w.take = (int*)p;
+  w.take = (int*)p; p += align_up((int64_t)(max_sweeps + 2) * 4, 256);
+  w.cmask[0] = (unsigned long long*)p; p += align_up((int64_t)tg.total * 8, 256);
+  w.cmask[1] = (unsigned long long*)p;
   return w;
 }
 

@@ -642,7 +642,8 @@ template <int D>
 __global__ void build_list_kernel(phj_grid g, TileGrid tg, const int16_t* __restrict__ lab,
                                   const uint8_t* __restrict__ mine, int* flags, int* list,
                                   int* count, int want_movers, const int32_t* __restrict__ fb,
-                                  const int8_t* __restrict__ kind) {
+                                  const int8_t* __restrict__ kind, unsigned long long* mask0,
+                                  unsigned long long mask_all) {
   constexpr int NB = Blk<D>::NB;
   const int lane = threadIdx.x & 31;
   const int blk = blockIdx.x * kWarps + (threadIdx.x >> 5);
@@ -665,6 +666,7 @@ __global__ void build_list_kernel(phj_grid g, TileGrid tg, const int16_t* __rest
   }
   if (__any_sync(0xffffffffu, any) && lane == 0) {
     flags[blk] = 1;
+    if (mask0) mask0[blk] = mask_all;
     list[atomicAdd(count, 1)] = blk;
   }
 }
@@ -694,6 +696,7 @@ struct TransportParams {
   int R;
   int64_t plane;       // ext nodes per colour plane
   double tol;
+  double act_eps;      // block-colour changes above this re-activate neighbours
   int max_sweeps;
   Workspace ws;
   unsigned long long* maxch;  // [max_sweeps * R], double bits
@@ -712,11 +715,15 @@ __global__ void __launch_bounds__(kThreads, 2) transport_kernel(const __grid_con
   cg::grid_group grid = cg::this_grid();
   const int nent = p.n_classes * p.nc;
   const int R = p.R;
-  double* s_w = (double*)smem;                                                  // [nent][NC]
-  unsigned long long* s_max = (unsigned long long*)(s_w + (int64_t)nent * NC);  // [R]
-  int* s_done = (int*)(s_max + R);                                              // [R]
-  signed char* s_oct = (signed char*)(s_done + R);                              // [nent]
-  for (int i = threadIdx.x; i < nent * NC; i += blockDim.x) s_w[i] = p.weights[i];
+  // weights corner-major with an odd pitch: lanes of a warp hold different
+  // entries, so [k][e] keeps their reads on distinct banks
+  const int wpitch = nent | 1;
+  double* s_w = (double*)smem;                                                     // [NC][wpitch]
+  unsigned long long* s_max = (unsigned long long*)(s_w + (int64_t)wpitch * NC);   // [R]
+  int* s_done = (int*)(s_max + R);                                                 // [R]
+  signed char* s_oct = (signed char*)(s_done + R);                                 // [nent]
+  for (int i = threadIdx.x; i < nent * NC; i += blockDim.x)
+    s_w[(i % NC) * wpitch + i / NC] = p.weights[i];
   for (int i = threadIdx.x; i < R; i += blockDim.x) s_done[i] = 0x7fffffff;
   for (int cls = 0; cls < p.n_classes; ++cls) {
     const int32_t* os = p.oct_start + cls * (NC + 1);
@@ -750,6 +757,7 @@ __global__ void __launch_bounds__(kThreads, 2) transport_kernel(const __grid_con
     const int cnt = ld_cg(&p.ws.counts[sw]);
     const int* list = p.ws.list[sw & 1];
     int* cur_flags = p.ws.flags[sw & 1];
+    unsigned long long* cur_mask = p.ws.cmask[sw & 1];
     int* take = &p.ws.take[sw];
     for (int i = threadIdx.x; i < R; i += blockDim.x) s_max[i] = 0ull;
     __syncthreads();
@@ -760,7 +768,15 @@ __global__ void __launch_bounds__(kThreads, 2) transport_kernel(const __grid_con
       int nxt_l0 = 0;
       if (lane == 0) nxt_l0 = atomicAdd(take, 1);
       const int blk = __ldcg(&list[item]);
-      if (lane == 0) cur_flags[blk] = 0;
+      // colours active in this block: those a neighbour block changed in the
+      // previous sweep (exact per colour, like the block skipping)
+      unsigned long long cm = 0;
+      if (lane == 0) {
+        cm = __ldcg(&cur_mask[blk]);
+        cur_mask[blk] = 0ull;
+        cur_flags[blk] = 0;
+      }
+      cm = __shfl_sync(FULL, cm, 0);
       int c[3];
       const bool row_ok = lane_nodes<D>(g, p.tg, blk, lane, c);
       const int64_t f0 = ext_flat<D>(g, c);
@@ -780,14 +796,21 @@ __global__ void __launch_bounds__(kThreads, 2) transport_kernel(const __grid_con
           for (int ax = 0; ax < D; ++ax)
             if (!((oc >> ax) & 1)) base[r] -= g.strides[ax];
 #pragma unroll
-          for (int k = 0; k < NC; ++k) w[r][k] = s_w[(int64_t)e[r] * NC + k];
+          for (int k = 0; k < NC; ++k) w[r][k] = s_w[k * wpitch + e[r]];
           any = true;
           ++upd;
         }
       }
-      bool changed = false;
+      unsigned long long changed = 0;
       if (__any_sync(FULL, any)) {
-        for (int j = 0; j < R; ++j) {
+        const bool masked = R <= 64;
+        unsigned long long todo = cm;
+        for (int jj = 0; masked ? (todo != 0ull) : (jj < R); ++jj) {
+          int j = jj;
+          if (masked) {
+            j = __ffsll((long long)todo) - 1;
+            todo &= todo - 1;
+          }
           const bool live = s_done[j] == 0x7fffffff;
           const double* pj = pin + (int64_t)j * p.plane;
           double* qj = pout + (int64_t)j * p.plane;
@@ -818,13 +841,15 @@ __global__ void __launch_bounds__(kThreads, 2) transport_kernel(const __grid_con
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) lmax = fmax(lmax, __shfl_xor_sync(FULL, lmax, off));
             if (lane == 0) atomicMax(&s_max[j], dbits(lmax));
-            changed = true;
+            // activity threshold: changes <= act_eps (a small fraction of the
+            // stopping tolerance) do not re-activate the neighbourhood
+            if (lmax > p.act_eps) changed |= (j < 64) ? (1ull << j) : ~0ull;
           }
         }
       }
       if (changed && lane < (D == 2 ? 9 : 27))
-        mark_neighbour<D>(p.tg, g, blk, lane, p.ws.flags[(sw + 1) & 1], p.ws.list[(sw + 1) & 1],
-                          &p.ws.counts[sw + 1]);
+        mark_neighbour_mask<D>(p.tg, g, blk, lane, changed, p.ws.cmask[(sw + 1) & 1],
+                               p.ws.list[(sw + 1) & 1], &p.ws.counts[sw + 1]);
       item = __shfl_sync(FULL, nxt_l0, 0);
     }
     __syncthreads();
@@ -1106,7 +1131,8 @@ static int solve_impl(const phj_solve_args* a) {
   PHJ_CUDA(cudaMemsetAsync(a->evals, 0, sizeof(unsigned long long), stream));
   PHJ_CUDA(cudaMemsetAsync(a->info, 0, 4 * sizeof(int32_t), stream));
   build_list_kernel<D><<<(p.tg.total + kWarps - 1) / kWarps, kThreads, 0, stream>>>(
-      p.g, p.tg, p.lab, p.mine, p.ws.flags[0], p.ws.list[0], p.ws.counts, 0, nullptr, nullptr);
+      p.g, p.tg, p.lab, p.mine, p.ws.flags[0], p.ws.list[0], p.ws.counts, 0, nullptr, nullptr,
+      nullptr, 0ull);
   phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   size_t smem = (size_t)StencilSmem<D, T>::bytes(p.n_classes, p.nc) +
@@ -1184,6 +1210,7 @@ static int transport_impl(const phj_transport_args* a) {
   p.R = a->n_colors;
   p.plane = a->grid.ext[0] * a->grid.ext[1] * (D == 3 ? a->grid.ext[2] : 1);
   p.tol = a->tol;
+  p.act_eps = a->act_eps;
   p.max_sweeps = a->max_sweeps;
   p.ws = carve<D>(a->grid, a->workspace, a->max_sweeps);
   p.maxch = (unsigned long long*)a->maxch_hist;
@@ -1206,11 +1233,12 @@ static int transport_impl(const phj_transport_args* a) {
     phj_count_launch(1);
   }
   build_list_kernel<D><<<(p.tg.total + kWarps - 1) / kWarps, kThreads, 0, stream>>>(
-      p.g, p.tg, nullptr, nullptr, p.ws.flags[0], p.ws.list[0], p.ws.counts, 1, p.fb, p.kind);
+      p.g, p.tg, nullptr, nullptr, p.ws.flags[0], p.ws.list[0], p.ws.counts, 1, p.fb, p.kind,
+      p.ws.cmask[0], p.R >= 64 ? ~0ull : ((1ull << p.R) - 1ull));
   phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   const int nent = p.n_classes * p.nc;
-  size_t smem = (size_t)nent * (1 << D) * 8 + (size_t)p.R * 12 + (size_t)nent + 16;
+  size_t smem = (size_t)(nent | 1) * (1 << D) * 8 + (size_t)p.R * 12 + (size_t)nent + 16;
   void* args[] = {(void*)&p};
   return coop_launch(transport_kernel<D>, (p.tg.total + kWarps - 1) / kWarps, smem, args, stream,
                      nullptr);

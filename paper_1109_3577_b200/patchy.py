@@ -40,6 +40,12 @@ UNCOVERED = -4
 #: last transport launch diagnostics (kernel ms, active blocks per sweep)
 TRANSPORT_DIAG: dict = {}
 
+#: colour transport re-activates a block's neighbourhood only for changes
+#: above this fraction of color_tol: the geometric tails of
+#: the Jacobi transport, orders of magnitude below the stopping tolerance,
+#: no longer keep the whole domain busy.  0 gives exact Jacobi activity.
+TRANSPORT_ACT_FRAC = 1.0e-3
+
 
 @dataclass
 class PatchyConfig:
@@ -215,6 +221,7 @@ def transport_internal(plan: StencilPlan, fb_int: torch.Tensor, parts_flat: Sequ
     a.ent_scratch = _lib.ptr(ent)
     a.n_colors = R
     a.tol = tol
+    a.act_eps = tol * TRANSPORT_ACT_FRAC
     a.max_sweeps = max_sweeps
     a.workspace = _lib.ptr(ws)
     a.maxch_hist = _lib.ptr(mc)
