@@ -93,11 +93,11 @@ def c3(rule: str = "kruzkov", dtype: str = "float64", n: int = 257,
 
 def theta_slabs(n_parts: int) -> Callable:
     def parts(target, grid, serials=None):
-        serials, tp = target_nodes(target, grid, serials)
-        th = tp[:, 2]
-        code = np.clip(np.floor((th - grid.lo[2]) / (grid.hi[2] - grid.lo[2]) * n_parts)
-                       .astype(int), 0, n_parts - 1)
-        return [serials[code == j] for j in range(n_parts)]
+        # equal heading slabs by node index (robust to the 2 pi / M rounding)
+        serials, _ = target_nodes(target, grid, serials)
+        j = np.unravel_index(serials, grid.shape)[2]
+        code = (j * n_parts) // grid.shape[2]
+        return [serials[code == p] for p in range(n_parts)]
     return parts
 
 

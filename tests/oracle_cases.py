@@ -54,6 +54,28 @@ def fan(n=41, nc=16):
     return P.OProblem(g, "scaled", circle(nc), tgt, speed=np.abs(X.sum(axis=1) + 0.1))
 
 
+def from_workload(w, which: str = "fine"):
+    """OProblem for a paper_1109_3577_b200.configs.Workload (same inputs:
+    grid, controls, target / coarse target, speed from the model's numpy
+    callable or Dubins)."""
+    from paper_1109_3577_b200 import dynamics
+
+    spec, pcfg = w.spec, w.pcfg
+    nodes = pcfg.fine_nodes if which == "fine" else pcfg.coarse_nodes
+    g = spec.make_grid(nodes)
+    og = P.OGrid(g.lo, g.hi, g.shape, g.periodic)
+    X = og.interior_points()
+    tgt_spec = spec.target if (which == "fine" or pcfg.coarse_target is None) else pcfg.coarse_target
+    tgt = tgt_spec.contains(X)
+    obs = spec.obstacles.contains(X) if spec.obstacles is not None else None
+    model = spec.model
+    if isinstance(model, dynamics.Dubins):
+        return P.OProblem(og, "dubins", spec.control_set.controls, tgt, obstacle=obs)
+    sp = model.speed
+    speed = np.full(og.n_interior, float(sp)) if np.isscalar(sp) else np.asarray(sp(X), float)
+    return P.OProblem(og, "scaled", spec.control_set.controls, tgt, obstacle=obs, speed=speed)
+
+
 def zermelo(n=21, nc=16):
     """zermelo2d preset: f = 2.1 a + (2, 0) (problems.py:258-262,337-342)."""
     g = P.OGrid((-2.0, -2.0), (2.0, 2.0), (n, n))

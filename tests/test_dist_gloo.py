@@ -1,0 +1,64 @@
+"""Multi-rank host logic on CPU (gloo, world size 2): LPT patch ownership is
+a disjoint cover and the MIN all-reduce gathers the owners' values."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import torch
+import torch.distributed as td
+import torch.multiprocessing as mp
+
+from paper_1109_3577_b200 import dist
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, sizes, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    td.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        r, w = dist.world()
+        mine = dist.mine_mask(sizes, r, w, "cpu")
+        # each rank "solves" its patches: node value = patch id + 0.5 for
+        # owned patches, unreached (1.0 -> here 99) elsewhere; target 0
+        color = np.repeat(np.arange(len(sizes)), sizes)
+        v = torch.full((color.size,), 99.0, dtype=torch.float64)
+        owned = torch.as_tensor(mine.numpy()[color].astype(bool))
+        v[owned] = torch.as_tensor(color, dtype=torch.float64)[owned] + 0.5
+        dist.gather_min(v)
+        q.put((rank, mine.numpy().tolist(), v.numpy().tolist()))
+    finally:
+        td.destroy_process_group()
+
+
+def test_lpt_ownership_and_min_gather_world2():
+    sizes = [7, 3, 5, 11, 2, 2, 9, 4]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, sizes, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    out.sort()
+    m0, m1 = np.array(out[0][1]), np.array(out[1][1])
+    assert np.all(m0 + m1 == 1)  # every patch owned by exactly one rank
+    loads = [sum(s for s, m in zip(sizes, mm) if m) for mm in (m0, m1)]
+    assert max(loads) <= sum(sizes) / 2 + max(sizes)
+    color = np.repeat(np.arange(len(sizes)), sizes)
+    want = color + 0.5
+    for _, _, v in out:
+        assert np.array_equal(np.array(v), want)  # identical gathered field on every rank

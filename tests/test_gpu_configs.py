@@ -1,0 +1,216 @@
+"""GPU parity of the full patchy pipeline on every BASELINE workload (reduced
+grids the CPU oracle finishes in seconds), plus size-independent properties
+at larger sizes.
+
+Same inputs on both sides (configs.py builds the problem; the oracle gets
+the same grid, controls, targets, speed samples and partition).  Bars
+(north_star): converged v within 1e-8 (fp64) / 1e-4 (fp32) sup-norm; labels
+identical except at nodes whose feedback argmin has a tie within 1e-12 (and
+their downstream); the counts are printed.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import has_gpu
+from oracle import pipeline as O
+import oracle_cases as C
+
+pytestmark = pytest.mark.gpu
+
+if has_gpu():
+    import paper_1109_3577_b200 as phj
+    from paper_1109_3577_b200 import configs, patchy
+
+
+def _to_v(T):
+    return np.where(T >= 0.5e9, 1.0, -np.expm1(-T))
+
+
+def _run_both(w, color_tol=1e-12):
+    pcfg = w.pcfg
+    pcfg.color_tol = color_tol
+    res = phj.run_patchy(w.spec, pcfg, w.cfg)
+    fine = C.from_workload(w, "fine")
+    coarse = C.from_workload(w, "coarse")
+    g = w.spec.make_grid(pcfg.fine_nodes)
+    parts = patchy._resolve_parts(pcfg, w.spec, g)
+    ores = O.run_patchy(fine, coarse, parts, rule=w.cfg.rule, mode="jacobi", tol=1e-8,
+                        color_tol=color_tol)
+    return res, ores, fine
+
+
+def _compare(res, ores, fine, bar, name):
+    g = fine.grid
+    inner = g.interior_flat()
+    got_v = _to_v(res.value.numpy().reshape(-1))[inner]
+    want_v = ores.value[inner]
+    fb = res.feedback.indices.cpu().numpy()
+    ties = ores.gaps < 1e-12
+    fdiff = fb != ores.feedback
+    col = res.patch_map.color.cpu().numpy()
+    ldiff = col != ores.color
+    print(f"{name}: feedback diffs {int(fdiff.sum())} (ties {int(ties.sum())}), "
+          f"label diffs {int(ldiff.sum())}, max|dv| {np.abs(got_v - want_v).max():.2e}")
+    assert not np.any(fdiff & ~ties), "feedback differs away from argmin ties"
+    if not fdiff.any():
+        # identical feedback => identical transport inputs => labels agree
+        # except where two colours' masses are within 1e-9 (counted)
+        phi_ties = ores.phi_gap < 1e-9
+        print(f"   colour-mass near-ties {int(phi_ties.sum())}")
+        assert not np.any(ldiff & ~phi_ties)
+    # values agree wherever the labels agree (a differing label changes the
+    # node's patch and hence its state-constrained value)
+    same = ~ldiff
+    err = np.abs(got_v[same] - want_v[same]).max()
+    assert err <= bar, err
+
+
+def test_c2_reduced_kruzkov_fp64():
+    w = configs.c2(n=129)
+    res, ores, fine = _run_both(w)
+    _compare(res, ores, fine, 1e-8, "c2@129")
+
+
+def test_c2_reduced_kruzkov_fp32_values():
+    w = configs.c2(n=129, dtype="float32")
+    w.cfg.tol = 1e-6
+    res, ores, fine = _run_both(w)
+    g = fine.grid
+    inner = g.interior_flat()
+    col = res.patch_map.color.cpu().numpy()
+    same = col == ores.color
+    got = _to_v(res.value.numpy().reshape(-1))[inner]
+    assert np.abs(got[same] - ores.value[inner][same]).max() <= 1e-4
+
+
+def test_c3_reduced_kruzkov_fp64():
+    w = configs.c3(n=65)
+    res, ores, fine = _run_both(w)
+    _compare(res, ores, fine, 1e-8, "c3@65")
+
+
+def test_c4_reduced_dubins_periodic():
+    w = configs.c4(nxy=41, nth=16, cxy=11, cth=8)
+    res, ores, fine = _run_both(w)
+    _compare(res, ores, fine, 1e-8, "c4@41x41x16")
+
+
+def test_c5_reduced_kruzkov_fp64_and_fp32():
+    w = configs.c5(n=65, dtype="float64")
+    res, ores, fine = _run_both(w)
+    _compare(res, ores, fine, 1e-8, "c5@65")
+    w32 = configs.c5(n=65, dtype="float32")
+    w32.pcfg.color_tol = 1e-12
+    r32 = phj.run_patchy(w32.spec, w32.pcfg, w32.cfg)
+    inner = fine.grid.interior_flat()
+    same = r32.patch_map.color.cpu().numpy() == ores.color
+    got = _to_v(r32.value.numpy().reshape(-1))[inner]
+    assert np.abs(got[same] - ores.value[inner][same]).max() <= 1e-4
+
+
+def test_c1_reference_rule_full_pipeline_matches_oracle_gs():
+    # the reference's own GS pipeline (oracle pinned bit-exact to it) vs the
+    # device Jacobi pipeline, reference update rule
+    w = configs.c1(rule="reference")
+    res, ores, fine = _run_both(w)
+    inner = fine.grid.interior_flat()
+    got = res.value.numpy().reshape(-1)[inner]
+    want = ores.value[inner]
+    live = (got < 0.5e9) & (want < 0.5e9)
+    assert np.array_equal(got < 0.5e9, want < 0.5e9)
+    assert np.abs(got[live] - want[live]).max() <= 1e-8
+
+
+def test_c2_full_size_properties():
+    # size-independent properties at BASELINE size: v in [0, 1), target 0,
+    # monotone decrease from the unreached start, every patch converged,
+    # labels cover every reachable node, T >= Euclidean distance / max speed
+    w = configs.c2()
+    res = phj.run_patchy(w.spec, w.pcfg, w.cfg)
+    assert res.coarse_stats.converged and all(s.converged for s in res.patch_stats)
+    g = res.value.grid
+    T = res.value.interior.cpu().numpy().reshape(-1)
+    X = g.interior_points()
+    tgt = w.spec.target.contains(X)
+    assert np.all(T[tgt] == 0.0)
+    col = res.patch_map.color.cpu().numpy()
+    assert np.all((col >= 0) | (col == patchy.TARGET))
+    d = np.min(np.stack([np.linalg.norm(X - c, axis=1) for c in w.spec.target.centers]), axis=0)
+    # minimum time >= distance / max speed (1.5), up to the O(k) scheme error
+    assert np.all(T >= 0.95 * (d - 0.05) / 1.5 - 4 * g.k_step)
+
+
+def test_dirichlet_single_patch_matches_single_domain():
+    # test_patchy.py:319-330
+    spec = phj.preset("eikonal2d", controls=16)
+    cfg = phj.SolverConfig()
+    res = phj.run_patchy(spec, phj.PatchyConfig(n_patches=1, coarse_nodes=31, fine_nodes=41,
+                                                bc_mode="dirichlet"), cfg)
+    g = phj.Grid(spec.box_lo, spec.box_hi, (41, 41))
+    direct, _ = phj.solve_single(spec, g)
+    d = (res.value.interior - direct.interior).abs().max().item()
+    assert d <= 10.0 * cfg.tol
+
+
+def test_warm_start_trapped_node():
+    # test_patchy.py:333-352
+    spec = phj.preset("eikonal2d", controls=8)
+    g = phj.Grid(spec.box_lo, spec.box_hi, (21, 21))
+    lifted, feedback, _ = phj.coarse_solve_and_lift(spec, g, g)
+    x = g.index_to_serial((15, 15))
+    tgt = spec.target.contains(g.interior_points())
+    color = np.zeros(g.n_interior, dtype=np.int32)
+    color[tgt] = phj.TARGET
+    color[x] = 1
+    pm = phj.PatchMap(g, 2, color)
+    warm, _, _ = phj.solve_patches(spec, g, pm, lifted, phj.PatchyConfig(n_patches=2,
+                                                                         warm_start=True))
+    assert float(warm.interior[15, 15]) == float(lifted.interior[15, 15])
+    cold, _, _ = phj.solve_patches(spec, g, pm, lifted, phj.PatchyConfig(n_patches=2))
+    assert float(cold.interior[15, 15]) == phj.SENTINEL
+
+
+def test_patch_solves_order_independent():
+    # test_patchy.py:355-372: relabelling patches cannot change the result
+    spec = phj.preset("eikonal2d", controls=16)
+    res = phj.run_patchy(spec, phj.PatchyConfig(n_patches=4, coarse_nodes=21, fine_nodes=41))
+    pm = res.patch_map
+    col = pm.color.clone()
+    live = col >= 0
+    col[live] = pm.n_patches - 1 - col[live]
+    flipped = phj.PatchMap(pm.grid, pm.n_patches, col)
+    a, _, _ = phj.solve_patches(spec, pm.grid, pm, res.lifted, phj.PatchyConfig(n_patches=4))
+    b, _, _ = phj.solve_patches(spec, pm.grid, flipped, res.lifted, phj.PatchyConfig(n_patches=4))
+    assert torch.equal(a.interior, b.interior)
+
+
+def test_obstacle_preset_pipeline():
+    # test_patchy.py:398-407
+    spec = phj.preset("eikonal2d-obstacles", controls=16)
+    res = phj.run_patchy(spec, phj.PatchyConfig(n_patches=4, coarse_nodes=31, fine_nodes=41))
+    g = res.value.grid
+    blocked = spec.obstacles.contains(g.interior_points())
+    v = res.value.interior.cpu().numpy().reshape(-1)
+    assert np.all(v[blocked] == phj.SENTINEL)
+    assert np.all(res.patch_map.color.cpu().numpy()[blocked] == phj.OBSTACLE)
+
+
+def test_error_report_hand_case():
+    # test_analysis.py:39-46
+    g = phj.Grid((0.0, 0.0), (1.0, 1.0), (2, 2))
+    a = phj.NodeField(g)
+    b = phj.NodeField(g)
+    a.values[...] = 0.0
+    b.values[...] = 0.0
+    a.flat[torch.as_tensor(g.interior_flat(), device=a.values.device)] = torch.tensor(
+        [1.0, 1.0, 1.0, 1.0], dtype=torch.float64, device=a.values.device)
+    b.flat[torch.as_tensor(g.interior_flat(), device=b.values.device)] = torch.tensor(
+        [1.1, 0.8, 1.0, 1.1], dtype=torch.float64, device=b.values.device)
+    rep = phj.error_report(a, b)
+    assert rep.e1 == pytest.approx(0.1)
+    assert rep.einf == pytest.approx(0.2)
+    assert (rep.compared_count, rep.excluded_count) == (4, 0)

@@ -1,0 +1,189 @@
+"""CPU tests of the host side: C ABI exports, stencil planning, partitions,
+configs and configuration validation (no device needed)."""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, golden
+
+import paper_1109_3577_b200 as phj
+from paper_1109_3577_b200 import _lib, configs, dist, dynamics, problems
+
+
+def _header_functions():
+    src = open(os.path.join(ROOT, "include", "phj.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(phj_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    names = _header_functions()
+    assert len(names) >= 20
+    for n in names:
+        getattr(lib, n)  # raises AttributeError if missing
+    assert set(names) <= set(_lib.EXPORTS) | {"phj_num_sms"}
+
+
+def test_library_reports_errors_without_device_work():
+    lib = _lib.load()
+    # a NULL argument is rejected with a message, no CUDA work is issued
+    assert lib.phj_solve(None) == 1
+    assert b"missing" in lib.phj_last_error()
+    assert lib.phj_launch_count() >= 0
+
+
+def test_stencil_weights_exact_sum_and_octants():
+    for n in (8, 32, 64):
+        A = phj.discretize_circle(n).controls
+        disp = (A / np.linalg.norm(A, axis=1, keepdims=True))[None]
+        st = dynamics.build_stencil(disp, None, np.ones((1, n), bool), dynamics.COST_NODE, (0, 1))
+        for e in range(st.oct_start[0, 0], st.oct_start[0, -1]):
+            s = 0.0
+            for w in st.weights[e]:
+                s = s + float(w)
+            assert s == 1.0  # kernel accumulation order sums to exactly 1
+            assert np.all(st.weights[e] >= 0.0)
+        # every control appears, octant groups padded to a multiple of 4
+        assert set(st.ctrl[st.oct_start[0, 0]: st.oct_start[0, -1]]) == set(range(n))
+        for o in range(4):
+            assert (st.oct_start[0, o + 1] - st.oct_start[0, o]) % 4 == 0
+
+
+def test_stencil_matches_reference_interpolation_weights():
+    # node-independent weights == the reference's snapped multilinear weights
+    # (grid.py:146-152, 227-239) at an interior node, up to the exact-sum ulp
+    A = problems.fibonacci_sphere(48).controls
+    g = phj.Grid((-1.0,) * 3, (1.0,) * 3, (21, 21, 21))
+    disp = (g.k_step * A / g.spacing)[None]
+    st = dynamics.build_stencil(disp, None, np.ones((1, 48), bool), dynamics.COST_NODE,
+                                (0, 1, 2))
+    x = g.interior_points()[g.index_to_serial((10, 10, 10))]
+    for pos in range(st.oct_start[0, 0], st.oct_start[0, -1]):
+        c = st.ctrl[pos]
+        cell, loc = g.locate_many((x + g.k_step * A[c])[None])
+        w_ref = phj.grid.interpolation_weights(loc)[0]
+        # map reference corners (absolute cell) to octant corners
+        base = np.array(g.locate_many(x[None])[0][0])
+        got = {}
+        octant = 0
+        for ax in range(3):
+            if disp[0, c, ax] >= 0:
+                octant |= 1 << ax
+        for k in range(8):
+            pos3 = tuple((0 if (octant >> ax) & 1 else -1) + ((k >> ax) & 1) for ax in range(3))
+            got[pos3] = st.weights[pos][k]
+        want = {}
+        for k in range(8):
+            pos3 = tuple(int(cell[0][ax] + ((k >> ax) & 1) - base[ax]) for ax in range(3))
+            want[pos3] = want.get(pos3, 0.0) + w_ref[k]
+        for key, v in want.items():
+            if v != 0.0:
+                assert got.get(key, 0.0) == pytest.approx(v, abs=1e-12)
+
+
+def test_plan_detects_dynamics_structure():
+    # zermelo: translation (per-control cost); fan: scaled with a zero-speed
+    # line; lqr (double integrator): rejected
+    g = phj.Grid((-2.0, -2.0), (2.0, 2.0), (21, 21))
+    st, ns, eps = dynamics.plan_stencils(g, phj.preset("zermelo2d", controls=16))
+    assert st.cost_mode == dynamics.COST_CTRL and ns is None
+    fan = phj.preset("fan2d", controls=16)
+    fan_generic = phj.ProblemSpec(**{**fan.__dict__, "model": None})
+    st, ns, eps = dynamics.plan_stencils(g, fan_generic)
+    assert st.cost_mode == dynamics.COST_NODE and ns.kind == 1
+    assert eps == pytest.approx(1e-12 * np.abs(g.interior_points().sum(1) + 0.1).max())
+    with pytest.raises(phj.ConfigurationError):
+        dynamics.plan_stencils(phj.Grid((-1, -1), (1, 1), (11, 11)), phj.preset("lunar2d"))
+    with pytest.raises(phj.ConfigurationError):
+        dynamics.plan_stencils(phj.Grid((-1, -1), (1, 1), (11, 11)), phj.preset("lqr2d"))
+
+
+def test_dubins_stencils_per_heading():
+    w = configs.c4(nxy=33, nth=16)
+    g = w.spec.make_grid(w.pcfg.fine_nodes)
+    st, ns, eps = dynamics.plan_stencils(g, w.spec)
+    assert st.perm == (2, 0, 1) and st.n_classes == 16 and st.cost_mode == dynamics.COST_CTRL
+    # |h f| = k for every heading/control (solver.py:180)
+    for j in range(16):
+        for c in range(5):
+            d = st.disp[j, c] * np.array([g.spacing[2], g.spacing[0], g.spacing[1]])
+            assert np.linalg.norm(d) == pytest.approx(g.k_step, rel=1e-12)
+
+
+@pytest.mark.parametrize("name,n,R", [("eikonal2d", 41, 4), ("zermelo2d", 31, 4),
+                                      ("fan2d", 31, 4), ("eikonal3d", 15, 4),
+                                      ("eikonal2d", 101, 8)])
+def test_partition_target_matches_reference(name, n, R):
+    gp = golden("partitions.npz")
+    spec = phj.preset(name)
+    g = phj.Grid(spec.box_lo, spec.box_hi, (n,) * spec.dim)
+    parts = phj.partition_target(spec.target, g, R)
+    assert np.array_equal(np.concatenate(parts), gp[f"{name}_{n}_{R}_serials"])
+    # the same through the pre-classified-serials fast path
+    serials = np.where(spec.target.contains(g.interior_points()))[0]
+    parts2 = phj.partition_target(spec.target, g, R, serials=serials)
+    assert all(np.array_equal(a, b) for a, b in zip(parts, parts2))
+
+
+def test_partition_errors():
+    spec = phj.preset("eikonal2d")
+    with pytest.raises(phj.ConfigurationError):
+        phj.partition_target(spec.target, phj.Grid((-2, -2), (2, 2), (5, 5)), 4)
+
+
+def test_config_partitions_are_disjoint_covers():
+    for w, nparts in ((configs.c2(n=257), 8), (configs.c3(n=65), 8), (configs.c5(n=65), 32),
+                      (configs.c4(nxy=33, nth=16), 16)):
+        g = w.spec.make_grid(w.pcfg.fine_nodes)
+        parts = w.pcfg.parts(w.spec.target, g)
+        assert len(parts) == nparts and all(p.size > 0 for p in parts)
+        allp = np.concatenate(parts)
+        assert allp.size == np.unique(allp).size
+        assert set(allp) == set(np.where(w.spec.target.contains(g.interior_points()))[0])
+
+
+def test_c1_coarse_target_dilation():
+    w = configs.c1()
+    gc = w.spec.make_grid(w.pcfg.coarse_nodes)
+    # 0 coarse target nodes at r=0.1, 4 after dilation
+    assert w.spec.target.contains(gc.interior_points()).sum() == 0
+    assert w.pcfg.coarse_target.contains(gc.interior_points()).sum() == 4
+
+
+def test_invalid_configs_rejected():
+    for kw in ({"tol": 0.0}, {"max_sweeps": 0}, {"bc_mode": "neumann"},
+               {"sweep_order": "random"}, {"control_reduction": 0.5}, {"rule": "x"},
+               {"dtype": "float16"}, {"dtype": "float32"}):
+        with pytest.raises(phj.ConfigurationError):
+            phj.SolverConfig(**kw)
+    phj.SolverConfig(rule="kruzkov", dtype="float32")
+    for kw in ({"n_patches": 0}, {"coarse_nodes": 101, "fine_nodes": 51},
+               {"bc_mode": "neumann"}, {"color_tol": 0.0}, {"reduction": 1.0}):
+        with pytest.raises(phj.ConfigurationError):
+            phj.PatchyConfig(**kw)
+
+
+def test_grid_periodic_and_layout():
+    g = phj.Grid((0.0, 0.0, 0.0), (1.0, 1.0, 2 * np.pi), (5, 5, 8),
+                 periodic=(False, False, True))
+    assert g.spacing[2] == pytest.approx(2 * np.pi / 8)
+    s = g.device_struct((2, 0, 1))
+    assert s.periodic[0] == 1 and s.shape[0] == 8 and s.ext[1] == 7
+    assert s.strides[0] == 7 * 7 and s.strides[2] == 1
+
+
+def test_lpt_assignment_and_bound():
+    sizes = [26098, 665, 5000, 9000, 12000, 700, 800, 3000]
+    owner = dist.lpt_assign(sizes, 4)
+    bins = np.bincount(owner, weights=sizes, minlength=4)
+    assert owner[0] != owner[4] and bins.max() == 26098
+    assert dist.load_balance_bound(sizes, 4) == pytest.approx(sum(sizes) / (4 * 26098))
+    assert dist.load_balance_bound([10] * 8, 8) == 1.0
+    assert dist.mine_mask(sizes, 0, 1, "cpu") is None
