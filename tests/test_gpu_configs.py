@@ -43,17 +43,28 @@ def _run_both(w, color_tol=1e-12):
     return res, ores, fine
 
 
-def _compare(res, ores, fine, bar, name):
+def _values_on_oracle_labels(w, ores, fine):
+    """Device patch solve on the oracle's patch map: isolates the value
+    solve from label differences at argmin ties."""
+    g = w.spec.make_grid(w.pcfg.fine_nodes)
+    R = int(ores.color.max()) + 1
+    pm = phj.PatchMap(g, R, ores.color)
+    lifted = phj.NodeField(g)  # not read by cold state-constrained solves
+    val, _, _ = phj.solve_patches(w.spec, g, pm, lifted, w.pcfg, w.cfg)
+    return _to_v(val.numpy().reshape(-1))[fine.grid.interior_flat()]
+
+
+def _compare(res, ores, fine, bar, name, w, tie_gap=1e-12):
     g = fine.grid
     inner = g.interior_flat()
     got_v = _to_v(res.value.numpy().reshape(-1))[inner]
     want_v = ores.value[inner]
     fb = res.feedback.indices.cpu().numpy()
-    ties = ores.gaps < 1e-12
+    ties = ores.gaps < tie_gap
     fdiff = fb != ores.feedback
     col = res.patch_map.color.cpu().numpy()
     ldiff = col != ores.color
-    print(f"{name}: feedback diffs {int(fdiff.sum())} (ties {int(ties.sum())}), "
+    print(f"{name}: feedback diffs {int(fdiff.sum())} (ties<{tie_gap:g}: {int(ties.sum())}), "
           f"label diffs {int(ldiff.sum())}, max|dv| {np.abs(got_v - want_v).max():.2e}")
     assert not np.any(fdiff & ~ties), "feedback differs away from argmin ties"
     if not fdiff.any():
@@ -62,54 +73,51 @@ def _compare(res, ores, fine, bar, name):
         phi_ties = ores.phi_gap < 1e-9
         print(f"   colour-mass near-ties {int(phi_ties.sum())}")
         assert not np.any(ldiff & ~phi_ties)
-    # values agree wherever the labels agree (a differing label changes the
-    # node's patch and hence its state-constrained value)
-    same = ~ldiff
-    err = np.abs(got_v[same] - want_v[same]).max()
+    if ldiff.any():
+        # a tie moved a patch boundary; compare the value solve on the
+        # oracle's labels instead (same patches => same state constraint)
+        got_v = _values_on_oracle_labels(w, ores, fine)
+    err = np.abs(got_v - want_v).max()
+    print(f"   max|dv| on common labels {err:.2e}")
     assert err <= bar, err
 
 
 def test_c2_reduced_kruzkov_fp64():
     w = configs.c2(n=129)
     res, ores, fine = _run_both(w)
-    _compare(res, ores, fine, 1e-8, "c2@129")
+    _compare(res, ores, fine, 1e-8, "c2@129", w)
 
 
-def test_c2_reduced_kruzkov_fp32_values():
+def test_c2_reduced_kruzkov_fp32():
+    # fp32 rounding moves near-equal argmins (gaps ~1e-7) -- compare labels
+    # away from such gaps, values on common labels at 1e-4
     w = configs.c2(n=129, dtype="float32")
-    w.cfg.tol = 1e-6
     res, ores, fine = _run_both(w)
-    g = fine.grid
-    inner = g.interior_flat()
-    col = res.patch_map.color.cpu().numpy()
-    same = col == ores.color
-    got = _to_v(res.value.numpy().reshape(-1))[inner]
-    assert np.abs(got[same] - ores.value[inner][same]).max() <= 1e-4
+    _compare(res, ores, fine, 1e-4, "c2@129 fp32", w, tie_gap=1e-5)
 
 
 def test_c3_reduced_kruzkov_fp64():
     w = configs.c3(n=65)
     res, ores, fine = _run_both(w)
-    _compare(res, ores, fine, 1e-8, "c3@65")
+    _compare(res, ores, fine, 1e-8, "c3@65", w)
 
 
 def test_c4_reduced_dubins_periodic():
     w = configs.c4(nxy=41, nth=16, cxy=11, cth=8)
     res, ores, fine = _run_both(w)
-    _compare(res, ores, fine, 1e-8, "c4@41x41x16")
+    _compare(res, ores, fine, 1e-8, "c4@41x41x16", w)
 
 
-def test_c5_reduced_kruzkov_fp64_and_fp32():
+def test_c5_reduced_kruzkov_fp64():
     w = configs.c5(n=65, dtype="float64")
     res, ores, fine = _run_both(w)
-    _compare(res, ores, fine, 1e-8, "c5@65")
-    w32 = configs.c5(n=65, dtype="float32")
-    w32.pcfg.color_tol = 1e-12
-    r32 = phj.run_patchy(w32.spec, w32.pcfg, w32.cfg)
-    inner = fine.grid.interior_flat()
-    same = r32.patch_map.color.cpu().numpy() == ores.color
-    got = _to_v(r32.value.numpy().reshape(-1))[inner]
-    assert np.abs(got[same] - ores.value[inner][same]).max() <= 1e-4
+    _compare(res, ores, fine, 1e-8, "c5@65", w)
+
+
+def test_c5_reduced_kruzkov_fp32():
+    w = configs.c5(n=65, dtype="float32")
+    res, ores, fine = _run_both(w)
+    _compare(res, ores, fine, 1e-4, "c5@65 fp32", w, tie_gap=1e-5)
 
 
 def test_c1_reference_rule_full_pipeline_matches_oracle_gs():
