@@ -122,6 +122,8 @@ typedef struct phj_solve_args {
 } phj_solve_args;
 
 int64_t phj_solve_workspace_bytes(const phj_grid* g, int32_t n_patches, int32_t max_sweeps);
+/* number of warp blocks (work/activity units) of a grid (diagnostics) */
+int64_t phj_blocks_total(const phj_grid* g);
 int phj_solve(const phj_solve_args* a);
 
 /* foreign-position masks: bit p set when 3^dim neighbour p of the node is not

@@ -72,7 +72,8 @@ class SpeedModel(ctypes.Structure):
 
 #: every symbol include/phj.h declares (checked by the CPU test suite)
 EXPORTS = (
-    "phj_solve_workspace_bytes", "phj_solve", "phj_fmask_from_labels", "phj_fmask_from_hard",
+    "phj_solve_workspace_bytes", "phj_blocks_total", "phj_solve", "phj_fmask_from_labels",
+    "phj_fmask_from_hard",
     "phj_feedback", "phj_transport", "phj_lift", "phj_argmax_update", "phj_argmax_colors",
     "phj_assemble_codes",
     "phj_assemble_repair", "phj_assemble_finish", "phj_classify", "phj_node_coef",
@@ -100,6 +101,7 @@ def load() -> ctypes.CDLL:
     lib = ctypes.CDLL(LIB_PATH)
     sig = {
         "phj_solve_workspace_bytes": (I64, [P, I32, I32]),
+        "phj_blocks_total": (I64, [P]),
         "phj_solve": (ctypes.c_int, [P]),
         "phj_fmask_from_labels": (ctypes.c_int, [P, P, P, P]),
         "phj_fmask_from_hard": (ctypes.c_int, [P, P, P, P]),

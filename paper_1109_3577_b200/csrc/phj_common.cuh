@@ -8,8 +8,15 @@
 
 namespace phj {
 
-constexpr int kThreads = 256;
+#ifndef PHJ_CTA_WARPS
+#define PHJ_CTA_WARPS 8
+#endif
+#ifndef PHJ_NB2D
+#define PHJ_NB2D 2
+#endif
+constexpr int kThreads = 32 * PHJ_CTA_WARPS;
 constexpr int kWarps = kThreads / 32;
+constexpr int kCtasPerSm = 16 / PHJ_CTA_WARPS;  // 16 resident warps per SM
 constexpr int kMaxPatches = 1024;
 constexpr int kSmemPatchReduce = 64;  // per-CTA patch max reduction when R <= 64
 
@@ -18,11 +25,20 @@ constexpr int kSmemPatchReduce = 64;  // per-CTA patch max reduction when R <= 6
 // axis 0 in 3D (so the stencil class -- internal axis 0 -- is warp-uniform).
 // Each lane keeps its NB nodes' 3^D neighbourhood in registers.
 template <int D> struct Blk;
+#ifndef PHJ_LX2D
+#define PHJ_LX2D 8
+#endif
+#ifndef PHJ_NB3D
+#define PHJ_NB3D 2
+#endif
+#ifndef PHJ_LX3D
+#define PHJ_LX3D 4
+#endif
 template <> struct Blk<2> {
-  static constexpr int NB = 4, LX = 8, LY = 4, BX = LX * NB, BY = LY;
+  static constexpr int NB = PHJ_NB2D, LX = PHJ_LX2D, LY = 32 / LX, BX = LX * NB, BY = LY;
 };
 template <> struct Blk<3> {
-  static constexpr int NB = 2, LX = 8, LY = 4, BX = LX * NB, BY = LY;
+  static constexpr int NB = PHJ_NB3D, LX = PHJ_LX3D, LY = 32 / LX, BX = LX * NB, BY = LY;
 };
 
 struct TileGrid {

@@ -547,7 +547,7 @@ __device__ bool sweep_block(const SolveParams& p, const StencilSmem<D, T>& s, in
 }
 
 template <int D, typename T, int RULE, int COST>
-__global__ void __launch_bounds__(kThreads, 2) solve_kernel(const __grid_constant__ SolveParams p) {
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __grid_constant__ SolveParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   cg::grid_group grid = cg::this_grid();
   StencilSmem<D, T> s = carve_stencil<D, T>(smem, p.n_classes, p.nc);
@@ -577,21 +577,27 @@ __global__ void __launch_bounds__(kThreads, 2) solve_kernel(const __grid_constan
     unsigned long long* gmax_row = p.maxch + (int64_t)sw * p.R;
     for (int i = threadIdx.x; i < nshared; i += blockDim.x) s_max[i] = 0ull;
     __syncthreads();
-    int item = 0;
-    if (lane == 0) item = atomicAdd(take, 1);
-    item = __shfl_sync(FULL, item, 0);
+    // Work items are claimed two ahead and their block ids read one ahead, so
+    // the claim (atomic) and list-read round trips overlap a block's compute;
+    // the first claim of a warp is its static index.
+    const int gwarp = blockIdx.x * kWarps + (threadIdx.x >> 5);
+    const int nwarps = gridDim.x * kWarps;
+    int item = gwarp;
+    int blk = item < cnt ? __ldcg(&list[item]) : 0;
+    int nxt_l0 = 0;
+    if (lane == 0) nxt_l0 = nwarps + atomicAdd(take, 1);
     while (item < cnt) {
-      // claim the next block now; its index is only needed after this one
-      int nxt_l0 = 0;
-      if (lane == 0) nxt_l0 = atomicAdd(take, 1);
-      const int blk = __ldcg(&list[item]);
+      const int nxt = __shfl_sync(FULL, nxt_l0, 0);
+      const int nblk = nxt < cnt ? __ldcg(&list[nxt]) : 0;
+      if (lane == 0 && nxt < cnt) nxt_l0 = nwarps + atomicAdd(take, 1);
       if (lane == 0) cur_flags[blk] = 0;
       const bool ch = sweep_block<D, T, RULE, COST>(p, s, blk, vin, vout, s_done, s_max, gmax_row,
                                                     evals);
       ++blocks_done;
       if (ch && lane < (D == 2 ? 9 : 27))
         mark_neighbour<D>(p.tg, p.g, blk, lane, nxt_flags, nxt_list, nxt_cnt);
-      item = __shfl_sync(FULL, nxt_l0, 0);
+      item = nxt;
+      blk = nblk;
     }
     __syncthreads();
     for (int i = threadIdx.x; i < nshared; i += blockDim.x)
@@ -706,7 +712,7 @@ struct TransportParams {
 };
 
 template <int D>
-__global__ void __launch_bounds__(kThreads, 2) transport_kernel(const __grid_constant__ TransportParams p) {
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) transport_kernel(const __grid_constant__ TransportParams p) {
   using B = Blk<D>;
   constexpr int NC = 1 << D;
   constexpr int NB = B::NB;
@@ -761,12 +767,12 @@ __global__ void __launch_bounds__(kThreads, 2) transport_kernel(const __grid_con
     int* take = &p.ws.take[sw];
     for (int i = threadIdx.x; i < R; i += blockDim.x) s_max[i] = 0ull;
     __syncthreads();
-    int item = 0;
-    if (lane == 0) item = atomicAdd(take, 1);
-    item = __shfl_sync(FULL, item, 0);
+    const int gwarp = blockIdx.x * kWarps + (threadIdx.x >> 5);
+    const int nwarps = gridDim.x * kWarps;
+    int item = gwarp;
     while (item < cnt) {
       int nxt_l0 = 0;
-      if (lane == 0) nxt_l0 = atomicAdd(take, 1);
+      if (lane == 0) nxt_l0 = nwarps + atomicAdd(take, 1);
       const int blk = __ldcg(&list[item]);
       // colours active in this block: those a neighbour block changed in the
       // previous sweep (exact per colour, like the block skipping)
@@ -1065,6 +1071,11 @@ extern "C" int phj_num_sms(void) {
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   return g_num_sms;
+}
+
+extern "C" int64_t phj_blocks_total(const phj_grid* g) {
+  if (!g) return -1;
+  return g->dim == 2 ? make_tile_grid<2>(*g).total : make_tile_grid<3>(*g).total;
 }
 
 extern "C" int64_t phj_solve_workspace_bytes(const phj_grid* g, int32_t n_patches,

@@ -429,11 +429,7 @@ def device_solve(plan: StencilPlan, work: torch.Tensor, lab: torch.Tensor, fmask
 def active_blocks_per_sweep(plan: StencilPlan, ws: torch.Tensor, max_sweeps: int, sweeps: int):
     """Active warp blocks per sweep from the solve workspace (diagnostics;
     layout of carve() in csrc/phj_common.cuh)."""
-    g = plan.gs
-    if g.dim == 2:
-        total = -(-g.shape[0] // 4) * -(-g.shape[1] // 32)
-    else:
-        total = g.shape[0] * -(-g.shape[1] // 4) * -(-g.shape[2] // 16)
+    total = int(_lib.load().phj_blocks_total(ctypes_ref(plan.gs)))
     tb = -(-total * 4 // 256) * 256
     off = 4 * tb
     counts = ws[off: off + 4 * (max_sweeps + 2)].view(torch.int32)
