@@ -115,7 +115,9 @@ typedef struct phj_solve_args {
   void* workspace;            /* phj_solve_workspace_bytes() bytes */
   int32_t* patch_sweeps;      /* out [n_patches]: sweeps to converge, -(cap) if not */
   double* maxch_hist;         /* out [max_sweeps * n_patches], may be NULL */
-  unsigned long long* evals;  /* out [1]: candidate evaluations performed */
+  unsigned long long* evals;  /* out [2]: [0] candidate evaluations of the swept nodes
+                                 (nodes x admissible controls), [1] stencil-entry
+                                 evaluations executed (incl. padding, after pruning) */
   int32_t* info;              /* out [4]: total sweeps, index of result buffer,
                                  tiles processed, launches */
   void* stream;               /* cudaStream_t */

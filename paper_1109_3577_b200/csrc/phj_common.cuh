@@ -16,7 +16,10 @@ namespace phj {
 #endif
 constexpr int kThreads = 32 * PHJ_CTA_WARPS;
 constexpr int kWarps = kThreads / 32;
-constexpr int kCtasPerSm = 16 / PHJ_CTA_WARPS;  // 16 resident warps per SM
+#ifndef PHJ_MIN_CTAS
+#define PHJ_MIN_CTAS (16 / PHJ_CTA_WARPS)  // 16 resident warps per SM
+#endif
+constexpr int kCtasPerSm = PHJ_MIN_CTAS;
 constexpr int kMaxPatches = 1024;
 constexpr int kSmemPatchReduce = 64;  // per-CTA patch max reduction when R <= 64
 
@@ -41,13 +44,29 @@ template <> struct Blk<3> {
   static constexpr int NB = PHJ_NB3D, LX = PHJ_LX3D, LY = 32 / LX, BX = LX * NB, BY = LY;
 };
 
+// n / d for 0 <= n < 2^31 by multiply-high ("round-up" magic number, the
+// usual replacement for a runtime integer division); set up on the host.
+struct FastDiv {
+  uint32_t d, m, l;
+  __host__ void init(uint32_t dd) {
+    d = dd < 1 ? 1 : dd;
+    l = 0;
+    while ((1ull << l) < d) ++l;
+    m = (uint32_t)((((1ull << 32) * ((1ull << l) - d)) / d) + 1);
+  }
+  __device__ __forceinline__ int div(int n) const {
+    return (int)((__umulhi((uint32_t)n, m) + (uint32_t)n) >> l);
+  }
+};
+
 struct TileGrid {
   int n[3];  // blocks per internal axis (axis 0 slowest)
   int total;
+  FastDiv f1, f2;  // division by n[1], n[2]
 };
 
 template <int D>
-__host__ __device__ inline TileGrid make_tile_grid(const phj_grid& g) {
+__host__ inline TileGrid make_tile_grid(const phj_grid& g) {
   TileGrid t;
   using B = Blk<D>;
   if (D == 2) {
@@ -61,7 +80,24 @@ __host__ __device__ inline TileGrid make_tile_grid(const phj_grid& g) {
     t.n[2] = (int)((g.shape[2] + B::BX - 1) / B::BX);
     t.total = t.n[0] * t.n[1] * t.n[2];
   }
+  t.f1.init((uint32_t)t.n[1]);
+  t.f2.init((uint32_t)t.n[2]);
   return t;
+}
+
+// block id -> block coordinates along internal axes (axis 0 slowest)
+template <int D>
+__device__ __forceinline__ void decode_block(const TileGrid& tg, int t, int b[3]) {
+  if (D == 2) {
+    b[0] = tg.f1.div(t);
+    b[1] = t - b[0] * tg.n[1];
+    b[2] = 0;
+  } else {
+    const int r = tg.f2.div(t);
+    b[2] = t - r * tg.n[2];
+    b[0] = tg.f1.div(r);
+    b[1] = r - b[0] * tg.n[1];
+  }
 }
 
 // Interior index of this lane's first node in block `t`; returns false when
@@ -70,72 +106,48 @@ template <int D>
 __device__ inline bool lane_nodes(const phj_grid& g, const TileGrid& tg, int t, int lane, int c[3]) {
   using B = Blk<D>;
   const int ly = lane / B::LX, lx = lane % B::LX;
+  int b[3];
+  decode_block<D>(tg, t, b);
   if (D == 2) {
-    const int bx = t % tg.n[1], by = t / tg.n[1];
-    c[0] = by * B::BY + ly;
-    c[1] = bx * B::BX + lx * B::NB;
+    c[0] = b[0] * B::BY + ly;
+    c[1] = b[1] * B::BX + lx * B::NB;
     c[2] = 0;
     return c[0] < g.shape[0];
   } else {
-    const int bx = t % tg.n[2];
-    const int r = t / tg.n[2];
-    const int by = r % tg.n[1], bz = r / tg.n[1];
-    c[0] = bz;
-    c[1] = by * B::BY + ly;
-    c[2] = bx * B::BX + lx * B::NB;
+    c[0] = b[0];
+    c[1] = b[1] * B::BY + ly;
+    c[2] = b[2] * B::BX + lx * B::NB;
     return c[1] < g.shape[1];
   }
 }
 
-// Mark the 3^D neighbour blocks of block `t` active for the next sweep
-// (lane nid of a warp whose block changed).
+// Id of neighbour nid (0 .. 3^D - 1) of block t, -1 outside the grid.
 template <int D>
-__device__ inline void mark_neighbour(const TileGrid& tg, const phj_grid& g, int t, int nid,
-                                      int* next_flags, int* next_list, int* next_count) {
-  int c[3], n[3] = {tg.n[0], tg.n[1], tg.n[2]};
+__device__ inline int neighbour_block(const TileGrid& tg, const phj_grid& g, int t, int nid) {
+  const int* n = tg.n;
+  int b[3];
+  decode_block<D>(tg, t, b);
   if (D == 2) {
-    c[1] = t % n[1];
-    c[0] = t / n[1];
-    int d0 = nid / 3 - 1, d1 = nid % 3 - 1;
-    int a = c[0] + d0, b = c[1] + d1;
-    if (g.periodic[0]) a = (a + n[0]) % n[0];
-    if (a < 0 || a >= n[0] || b < 0 || b >= n[1]) return;
-    int nt = a * n[1] + b;
-    if (atomicExch(&next_flags[nt], 1) == 0) next_list[atomicAdd(next_count, 1)] = nt;
+    int a = b[0] + nid / 3 - 1, c = b[1] + nid % 3 - 1;
+    if (g.periodic[0]) a = a < 0 ? a + n[0] : (a >= n[0] ? a - n[0] : a);
+    if (a < 0 || a >= n[0] || c < 0 || c >= n[1]) return -1;
+    return a * n[1] + c;
   } else {
-    c[2] = t % n[2];
-    int r = t / n[2];
-    c[1] = r % n[1];
-    c[0] = r / n[1];
-    int d0 = nid / 9 - 1, d1 = (nid / 3) % 3 - 1, d2 = nid % 3 - 1;
-    int a = c[0] + d0, b = c[1] + d1, e = c[2] + d2;
-    if (g.periodic[0]) a = (a + n[0]) % n[0];
-    if (a < 0 || a >= n[0] || b < 0 || b >= n[1] || e < 0 || e >= n[2]) return;
-    int nt = (a * n[1] + b) * n[2] + e;
-    if (atomicExch(&next_flags[nt], 1) == 0) next_list[atomicAdd(next_count, 1)] = nt;
+    int a = b[0] + nid / 9 - 1, c = b[1] + (nid / 3) % 3 - 1, e = b[2] + nid % 3 - 1;
+    if (g.periodic[0]) a = a < 0 ? a + n[0] : (a >= n[0] ? a - n[0] : a);
+    if (a < 0 || a >= n[0] || c < 0 || c >= n[1] || e < 0 || e >= n[2]) return -1;
+    return (a * n[1] + c) * n[2] + e;
   }
 }
 
-// Colour-mask variant (transport): OR the changed colours into the
-// neighbour's next-sweep mask; the first setter appends the block.
+// Colour-mask marking (transport): OR the changed colours into neighbour
+// nid's next-sweep mask; the first setter appends the block.
 template <int D>
 __device__ inline void mark_neighbour_mask(const TileGrid& tg, const phj_grid& g, int t, int nid,
                                            unsigned long long bits, unsigned long long* next_mask,
                                            int* next_list, int* next_count) {
-  int n[3] = {tg.n[0], tg.n[1], tg.n[2]};
-  int nt;
-  if (D == 2) {
-    int a = t / n[1] + nid / 3 - 1, b = t % n[1] + nid % 3 - 1;
-    if (g.periodic[0]) a = (a + n[0]) % n[0];
-    if (a < 0 || a >= n[0] || b < 0 || b >= n[1]) return;
-    nt = a * n[1] + b;
-  } else {
-    const int r = t / n[2];
-    int a = r / n[1] + nid / 9 - 1, b = r % n[1] + (nid / 3) % 3 - 1, e = t % n[2] + nid % 3 - 1;
-    if (g.periodic[0]) a = (a + n[0]) % n[0];
-    if (a < 0 || a >= n[0] || b < 0 || b >= n[1] || e < 0 || e >= n[2]) return;
-    nt = (a * n[1] + b) * n[2] + e;
-  }
+  const int nt = neighbour_block<D>(tg, g, t, nid);
+  if (nt < 0) return;
   if (atomicOr(&next_mask[nt], bits) == 0ull) next_list[atomicAdd(next_count, 1)] = nt;
 }
 
@@ -148,7 +160,7 @@ struct Workspace {
   unsigned long long* cmask[2];  // transport: per-block active-colour masks
 };
 
-inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+__host__ __device__ inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 template <int D>
 inline int64_t workspace_bytes(const phj_grid& g, int max_sweeps) {

@@ -31,6 +31,29 @@ namespace cg = cooperative_groups;
 
 namespace phj {
 
+// Optional per-phase cycle accounting (diagnostic builds only, -DPHJ_TIMING).
+#ifdef PHJ_TIMING
+__device__ unsigned long long g_phase_cycles[8];
+struct PhaseTimer {
+  unsigned long long acc[8];
+  long long prev;
+  __device__ void start() {
+    for (int i = 0; i < 8; ++i) acc[i] = 0;
+    prev = clock64();
+  }
+  __device__ void mark(int i) {
+    long long t = clock64();
+    acc[i] += (unsigned long long)(t - prev);
+    prev = t;
+  }
+};
+#else
+struct PhaseTimer {
+  __device__ void start() {}
+  __device__ void mark(int) {}
+};
+#endif
+
 struct SolveParams {
   phj_grid g;
   TileGrid tg;
@@ -121,64 +144,59 @@ __device__ inline void stage_stencil(const StencilSmem<D, T>& s, int ncls, int n
   for (int i = threadIdx.x; i < ncls * ((1 << D) + 1); i += blockDim.x) s.oct[i] = oct_start[i];
 }
 
-// Neighbourhood register block: NR rows (3^(D-1)) x (NB + 2) columns.
+// Neighbourhood sources.  Evaluation code asks a source for corner K of
+// octant O of the lane's node r (all compile-time after unrolling):
+//  * Nbhd  -- the full 3^D neighbourhood of the NB nodes in registers
+//             (feedback extraction);
+//  * OctNb -- only the 2^D-corner cells of ONE octant, loaded from the
+//             warp's staged tile right before that octant is evaluated
+//             (value sweep; keeps the 3D register footprint small).
+// Corner K, internal axis i: offset (O_i ? 0 : -1) + K_i from the node.
 template <int D, typename T, int NB>
 struct Nbhd {
   static constexpr int NR = (D == 2) ? 3 : 9;
   T v[NR][NB + 2];
-};
-
-// value of corner K of octant O for node r (compile-time after unrolling)
-template <int D, int NB, int O, int K, typename T>
-__device__ __forceinline__ T corner_val(const Nbhd<D, T, NB>& nb, int r) {
-  // internal axis ax: offset = (octant bit ? 0 : -1) + corner bit
-  constexpr int off0 = (((O >> 0) & 1) ? 0 : -1) + ((K >> 0) & 1);
-  constexpr int off1 = (((O >> 1) & 1) ? 0 : -1) + ((K >> 1) & 1);
-  if constexpr (D == 2) {
-    return nb.v[off0 + 1][r + off1 + 1];
-  } else {
-    constexpr int off2 = (((O >> 2) & 1) ? 0 : -1) + ((K >> 2) & 1);
-    return nb.v[(off0 + 1) * 3 + (off1 + 1)][r + off2 + 1];
-  }
-}
-
-template <int D, typename T, int NB, int O, int K>
-struct CornerSum {
-  __device__ __forceinline__ static T run(const Nbhd<D, T, NB>& nb, const T* w, int r, T acc) {
-    acc = fma(w[K], corner_val<D, NB, O, K>(nb, r), acc);
-    return CornerSum<D, T, NB, O, K + 1>::run(nb, w, r, acc);
+  template <int O, int K>
+  __device__ __forceinline__ T corner(int r) const {
+    constexpr int off0 = (((O >> 0) & 1) ? 0 : -1) + ((K >> 0) & 1);
+    constexpr int off1 = (((O >> 1) & 1) ? 0 : -1) + ((K >> 1) & 1);
+    if constexpr (D == 2) {
+      return v[off0 + 1][r + off1 + 1];
+    } else {
+      constexpr int off2 = (((O >> 2) & 1) ? 0 : -1) + ((K >> 2) & 1);
+      return v[(off0 + 1) * 3 + (off1 + 1)][r + off2 + 1];
+    }
   }
 };
+
+// Octant view of a full register neighbourhood (compile-time octant).
 template <int D, typename T, int NB, int O>
-struct CornerSum<D, T, NB, O, (1 << D)> {
-  __device__ __forceinline__ static T run(const Nbhd<D, T, NB>&, const T*, int, T acc) {
-    return acc;
+struct NbhdOct {
+  const Nbhd<D, T, NB>& nb;
+  template <int K>
+  __device__ __forceinline__ T corner(int r) const {
+    return nb.template corner<O, K>(r);
   }
 };
 
-// One corner step K of U*NB interleaved interpolation chains.
-template <int D, typename T, int NB, int O, int U, int K>
+// One corner step K of U*NB interleaved interpolation chains over a cell
+// source (corner<K>(r) of one octant).
+template <int D, typename T, int NB, int U, int K, typename Src>
 struct ChainStep {
-  __device__ __forceinline__ static void run(const Nbhd<D, T, NB>& nb, const T (&w)[U][1 << D],
+  __device__ __forceinline__ static void run(const Src& cell, const T (&w)[U][1 << D],
                                              T (&acc)[U][NB]) {
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
-      for (int r = 0; r < NB; ++r) acc[u][r] = fma(w[u][K], corner_val<D, NB, O, K>(nb, r), acc[u][r]);
-    ChainStep<D, T, NB, O, U, K + 1>::run(nb, w, acc);
+      for (int r = 0; r < NB; ++r)
+        acc[u][r] = fma(w[u][K], cell.template corner<K>(r), acc[u][r]);
+    ChainStep<D, T, NB, U, K + 1, Src>::run(cell, w, acc);
   }
 };
-template <int D, typename T, int NB, int O, int U>
-struct ChainStep<D, T, NB, O, U, (1 << D)> {
-  __device__ __forceinline__ static void run(const Nbhd<D, T, NB>&, const T (&)[U][1 << D],
-                                             T (&)[U][NB]) {}
+template <int D, typename T, int NB, int U, typename Src>
+struct ChainStep<D, T, NB, U, (1 << D), Src> {
+  __device__ __forceinline__ static void run(const Src&, const T (&)[U][1 << D], T (&)[U][NB]) {}
 };
-
-template <int D, typename T, int NB, int O>
-__device__ __forceinline__ T interp(const Nbhd<D, T, NB>& nb, const T* w, int r) {
-  T acc = w[0] * corner_val<D, NB, O, 0>(nb, r);
-  return CornerSum<D, T, NB, O, 1>::run(nb, w, r, acc);
-}
 
 template <typename T, int N>
 __device__ __forceinline__ void load_weights(const T* src, T* w) {
@@ -230,6 +248,12 @@ __device__ __forceinline__ T finish_cand(T acc, T ca, T cb, T ncoef, uint32_t fm
 #ifndef PHJ_KUNROLL2
 #define PHJ_KUNROLL2 4
 #endif
+#ifndef PHJ_PRUNE
+#define PHJ_PRUNE 1
+#endif
+#ifndef PHJ_WPIPE
+#define PHJ_WPIPE 0
+#endif
 template <typename T>
 struct MinAcc;
 template <>
@@ -267,18 +291,19 @@ __device__ __forceinline__ void take_arg(T acc, int cidx, T& best, int& bidx) {
 // per iteration (the host pads every octant group to a multiple of U).
 // MODE 0: min (sweep, into mn); MODE 1: argmin with the lowest original
 // index on ties (feedback, into best/bidx).
-template <int D, typename T, int NB, int RULE, int COST, bool SLOW, int MODE, int O>
-__device__ __forceinline__ void eval_octant(const Nbhd<D, T, NB>& nb, const StencilSmem<D, T>& s,
+template <int D, typename T, int NB, int RULE, int COST, bool SLOW, int MODE, typename Src>
+__device__ __forceinline__ void eval_octant(const Src& cell, int O, const StencilSmem<D, T>& s,
                                             const int* os, const uint32_t (&fm)[NB],
                                             const T (&ncoef)[NB], const int32_t* ctrl_map,
                                             MinAcc<T> (&mn)[NB], T (&best)[NB], int (&bidx)[NB]) {
   constexpr int NC = 1 << D;
   constexpr int U = (D == 2) ? PHJ_KUNROLL2 : PHJ_UNROLL(D);  // divides the host padding
   const int e0 = os[O], e1 = os[O + 1];
-  for (int e = e0; e < e1; e += U) {
-    T w[U][NC];
-#pragma unroll
-    for (int u = 0; u < U; ++u) load_weights<T, NC>(s.w + (int64_t)(e + u) * NC, w[u]);
+  if (e0 >= e1) return;
+  // U entries from e: corner-major order -- U*NB independent FMA chains
+  // advance one corner per step, so consecutive FP64 instructions never
+  // depend on each other (DFMA latency ~8 cycles, 2-cycle issue per warp).
+  auto step = [&](const T (&w)[U][NC], int e) {
     T ca[U], cb[U];
     uint32_t nz[U];
     int ci[U];
@@ -295,15 +320,12 @@ __device__ __forceinline__ void eval_octant(const Nbhd<D, T, NB>& nb, const Sten
       if constexpr (SLOW) nz[u] = s.nz[e + u];
       if constexpr (MODE == 1) ci[u] = ctrl_map[e + u];
     }
-    // corner-major order: U*NB independent FMA chains advance one corner per
-    // step, so consecutive FP64 instructions never depend on each other
-    // (DFMA latency ~8 cycles, 2-cycle issue per warp on sm_100).
     T acc[U][NB];
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
-      for (int r = 0; r < NB; ++r) acc[u][r] = w[u][0] * corner_val<D, NB, O, 0>(nb, r);
-    ChainStep<D, T, NB, O, U, 1>::run(nb, w, acc);
+      for (int r = 0; r < NB; ++r) acc[u][r] = w[u][0] * cell.template corner<0>(r);
+    ChainStep<D, T, NB, U, 1, Src>::run(cell, w, acc);
 #pragma unroll
     for (int r = 0; r < NB; ++r) {
       T x[U];
@@ -323,28 +345,228 @@ __device__ __forceinline__ void eval_octant(const Nbhd<D, T, NB>& nb, const Sten
         for (int u = 0; u < U; ++u) take_arg<T>(x[u], ci[u], best[r], bidx[r]);
       }
     }
+  };
+  auto load = [&](T (&w)[U][NC], int e) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) load_weights<T, NC>(s.w + (int64_t)(e + u) * NC, w[u]);
+  };
+#if PHJ_WPIPE
+  // weights double-buffered one step ahead (the shared-memory latency of a
+  // step's weights overlaps the previous step's FMA chains)
+  const int elast = e1 - U;
+  T wa[U][NC], wb[U][NC];
+  load(wa, e0);
+  for (int e = e0; e < e1; e += 2 * U) {
+    load(wb, min(e + U, elast));
+    step(wa, e);
+    if (e + U >= e1) break;
+    load(wa, min(e + 2 * U, elast));
+    step(wb, e + U);
   }
+#else
+  for (int e = e0; e < e1; e += U) {
+    T w[U][NC];
+    load(w, e);
+    step(w, e);
+  }
+#endif
 }
 
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+// All octants in order; `hook` runs once, right after octant 0 (the solve
+// sweep issues the next block's loads there so they overlap the rest).
 template <int D, typename T, int NB, int RULE, int COST, bool SLOW, int MODE, int O = 0>
 struct EvalAll {
+  template <typename Hook>
   __device__ __forceinline__ static void run(const Nbhd<D, T, NB>& nb, const StencilSmem<D, T>& s,
                                              const int* os, const uint32_t (&fm)[NB],
                                              const T (&ncoef)[NB], const int32_t* ctrl_map,
-                                             MinAcc<T> (&mn)[NB], T (&best)[NB], int (&bidx)[NB]) {
-    eval_octant<D, T, NB, RULE, COST, SLOW, MODE, O>(nb, s, os, fm, ncoef, ctrl_map, mn, best,
-                                                     bidx);
+                                             MinAcc<T> (&mn)[NB], T (&best)[NB], int (&bidx)[NB],
+                                             const Hook& hook) {
+    eval_octant<D, T, NB, RULE, COST, SLOW, MODE>(NbhdOct<D, T, NB, O>{nb}, O, s, os, fm, ncoef,
+                                                  ctrl_map, mn, best, bidx);
+    if constexpr (O == 0) hook();
     EvalAll<D, T, NB, RULE, COST, SLOW, MODE, O + 1>::run(nb, s, os, fm, ncoef, ctrl_map, mn, best,
-                                                         bidx);
+                                                         bidx, hook);
   }
 };
 template <int D, typename T, int NB, int RULE, int COST, bool SLOW, int MODE>
 struct EvalAll<D, T, NB, RULE, COST, SLOW, MODE, (1 << D)> {
+  template <typename Hook>
   __device__ __forceinline__ static void run(const Nbhd<D, T, NB>&, const StencilSmem<D, T>&,
                                              const int*, const uint32_t (&)[NB], const T (&)[NB],
                                              const int32_t*, MinAcc<T> (&)[NB], T (&)[NB],
-                                             int (&)[NB]) {}
+                                             int (&)[NB], const Hook&) {}
 };
+
+// ---- octant pruning (MODE 0, per-node cost) --------------------------------
+// Every candidate of octant O is a convex combination of the octant's 2^D
+// corner values (non-negative weights summing exactly to 1 in T, fma chain
+// with non-negative terms), so in floating point it is >= min corner *
+// (1 - 2^D u).  An octant whose corner minimum (lowered by a margin of many
+// ulps) is not below the node's running minimum cannot lower it: skipping
+// it leaves the minimum bit-identical.  Values are >= 0, so the order of
+// their bit patterns as integers is the order of the values.
+template <typename T>
+struct OrdKey;
+template <>
+struct OrdKey<double> {
+  // coarse key: the high word (monotone in the value for x >= 0); the
+  // bound test below only compares coarse keys, which is conservative
+  using I = int;
+  static __device__ __forceinline__ I coarse(double x) { return __double2hiint(x); }
+};
+template <>
+struct OrdKey<float> {
+  using I = int;
+  static __device__ __forceinline__ I coarse(float x) { return __float_as_int(x); }
+};
+
+template <int D, typename T, int NB, int K, typename Src>
+struct CornerMin {
+  __device__ __forceinline__ static int run(const Src& cell, int r, int m) {
+    m = min(m, OrdKey<T>::coarse(cell.template corner<K>(r)));
+    return CornerMin<D, T, NB, K + 1, Src>::run(cell, r, m);
+  }
+};
+template <int D, typename T, int NB, typename Src>
+struct CornerMin<D, T, NB, (1 << D), Src> {
+  __device__ __forceinline__ static int run(const Src&, int, int m) { return m; }
+};
+
+// Does any computing node of the lane still need the octant of `cell`?
+// Skip only if  coarse(min corner) - margin >= coarse(best): for fp64
+// (coarse = high word, margin 2) the min corner is then >= 2^32 ulps above
+// best, for fp32 (full key, margin 64) >= 64 ulps -- both far above the
+// rounding of a 2^D-term convex combination (<= 2^D/2 ulps below its min).
+template <int D, typename T, int NB, typename Src>
+__device__ __forceinline__ bool octant_needed(const Src& cell, const bool (&comp)[NB],
+                                              const MinAcc<T> (&mn)[NB]) {
+  using K = OrdKey<T>;
+  constexpr int margin = sizeof(T) == 8 ? 2 : 64;
+  bool need = false;
+#pragma unroll
+  for (int r = 0; r < NB; ++r) {
+    const int cmin = CornerMin<D, T, NB, 1, Src>::run(cell, r, K::coarse(cell.template corner<0>(r)));
+    need |= comp[r] && cmin - margin < K::coarse(mn[r].get());
+  }
+  return need;
+}
+
+// ---- the warp's staged halo tile ---------------------------------------------
+// Warp-block halo tile: the union of the 3^D neighbourhoods of a block's
+// nodes (ext values, clamped like load_nbhd), staged into shared memory by
+// the whole warp with cp.async -- every ext value is fetched once per block,
+// and the copy of the next block overlaps the current block's control loop.
+template <int D>
+struct TileShape {
+  using B = Blk<D>;
+  static constexpr int RB = B::BY + 2;                    // rows per plane
+  static constexpr int R = (D == 2) ? RB : 3 * RB;        // rows (x 3 planes in 3D)
+  static constexpr int C = B::BX + 2 + ((B::BX + 2) % 2 == 0);  // columns (odd pitch: banks)
+  static constexpr int N = R * C;
+};
+
+// The lane's origin in the tile (its first node's 3^D neighbourhood starts
+// here) and the element of that node displaced by (d0, d1[, d2]).
+template <int D, typename T>
+__device__ __forceinline__ const T* lane_tile(const T* tile, int lane) {
+  using B = Blk<D>;
+  using S = TileShape<D>;
+  return tile + (lane / B::LX) * S::C + (lane % B::LX) * B::NB;
+}
+template <int D, typename T>
+__device__ __forceinline__ T tile_at(const T* lt, int d0, int d1, int d2 = 0) {
+  using S = TileShape<D>;
+  if constexpr (D == 2) return lt[(1 + d0) * S::C + 1 + d1];
+  else return lt[((1 + d0) * S::RB + 1 + d1) * S::C + 1 + d2];
+}
+
+// The 2^D-corner cells of one octant (runtime O) for the lane's NB nodes;
+// the accessors are octant-independent, so one copy of the control loop
+// serves every octant.
+template <int D, typename T, int NB>
+struct OctNb {
+  static constexpr int NR = 1 << (D - 1);
+  T v[NR][NB + 1];
+  template <int K>
+  __device__ __forceinline__ T corner(int r) const {
+    if constexpr (D == 2) return v[K & 1][r + ((K >> 1) & 1)];
+    else return v[(K & 1) * 2 + ((K >> 1) & 1)][r + ((K >> 2) & 1)];
+  }
+  __device__ __forceinline__ void load(const T* lt, int O) {
+    using S = TileShape<D>;
+    const int b0 = O & 1, b1 = (O >> 1) & 1, b2 = (O >> 2) & 1;
+    if constexpr (D == 2) {
+      const T* t0 = lt + b0 * S::C + b1;
+#pragma unroll
+      for (int k0 = 0; k0 < 2; ++k0)
+#pragma unroll
+        for (int j = 0; j <= NB; ++j) v[k0][j] = t0[k0 * S::C + j];
+    } else {
+      const T* t0 = lt + (b0 * S::RB + b1) * S::C + b2;
+#pragma unroll
+      for (int k0 = 0; k0 < 2; ++k0)
+#pragma unroll
+        for (int k1 = 0; k1 < 2; ++k1)
+#pragma unroll
+          for (int j = 0; j <= NB; ++j) v[k0 * 2 + k1][j] = t0[(k0 * S::RB + k1) * S::C + j];
+    }
+  }
+};
+
+// the octant of steepest descent at the lane's first node, majority over
+// the warp (warp-uniform)
+template <int D, typename T>
+__device__ __forceinline__ int preferred_octant(const T* lt) {
+  const unsigned FULL = 0xffffffffu;
+  bool down[D];
+  if constexpr (D == 2) {
+    down[0] = tile_at<D>(lt, 1, 0) < tile_at<D>(lt, -1, 0);
+    down[1] = tile_at<D>(lt, 0, 1) < tile_at<D>(lt, 0, -1);
+  } else {
+    down[0] = tile_at<D>(lt, 1, 0, 0) < tile_at<D>(lt, -1, 0, 0);
+    down[1] = tile_at<D>(lt, 0, 1, 0) < tile_at<D>(lt, 0, -1, 0);
+    down[2] = tile_at<D>(lt, 0, 0, 1) < tile_at<D>(lt, 0, 0, -1);
+  }
+  int o = 0;
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+    if (__popc(__ballot_sync(FULL, down[i])) >= 16) o |= 1 << i;
+  return o;
+}
+
+// Sweep evaluation of one block from its staged tile: with per-node costs
+// the warp's preferred octant first, then the others unless pruned; with
+// per-control costs every octant in order.  `hook` runs once, after the
+// first octant.  Returns the stencil entries evaluated per node.
+template <int D, typename T, int NB, int RULE, int COST, bool SLOW, typename Hook>
+__device__ __forceinline__ int eval_sweep(const T* lt, const StencilSmem<D, T>& s,
+                                          const int* os, const uint32_t (&fm)[NB],
+                                          const T (&ncoef)[NB], const bool (&comp)[NB],
+                                          MinAcc<T> (&mn)[NB], T (&best)[NB], int (&bidx)[NB],
+                                          const Hook& hook) {
+  constexpr bool PRUNE = COST == PHJ_COST_NODE && PHJ_PRUNE;
+  const int first = PRUNE ? preferred_octant<D, T>(lt) : 0;
+  OctNb<D, T, NB> cell;
+  cell.load(lt, first);
+  eval_octant<D, T, NB, RULE, COST, SLOW, 0>(cell, first, s, os, fm, ncoef, nullptr, mn, best,
+                                             bidx);
+  int n_ent = os[first + 1] - os[first];
+  hook();
+#pragma unroll 1
+  for (int O = 0; O < (1 << D); ++O) {
+    if (O == first) continue;
+    cell.load(lt, O);
+    if (PRUNE && !__any_sync(0xffffffffu, octant_needed<D, T, NB>(cell, comp, mn))) continue;
+    eval_octant<D, T, NB, RULE, COST, SLOW, 0>(cell, O, s, os, fm, ncoef, nullptr, mn, best, bidx);
+    n_ent += os[O + 1] - os[O];
+  }
+  return n_ent;
+}
 
 template <int D>
 __device__ inline int64_t ext_flat(const phj_grid& g, const int c[3]) {
@@ -391,14 +613,138 @@ __device__ inline void atomic_max_change(unsigned long long* addr, T ch) {
   atomicMax(addr, dbits((double)ch));
 }
 
-// One block of the value sweep, processed by one warp.  Returns (warp-
-// uniform) whether any node changed.
-template <int D, typename T, int RULE, int COST>
-__device__ bool sweep_block(const SolveParams& p, const StencilSmem<D, T>& s, int blk,
-                            const T* __restrict__ vin, T* __restrict__ vout, const int* s_done,
-                            unsigned long long* s_max, unsigned long long* gmax_row,
-                            unsigned long long& evals) {
-  constexpr int NB = Blk<D>::NB;
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(d), "l"(src), "n"(BYTES));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
+// Per-node inputs of a staged block: node coefficients, foreign masks and
+// labels (int16, copied as the 32-bit words covering each row).
+template <int D, typename T>
+struct NodeStage {
+  using B = Blk<D>;
+  static constexpr int NN = B::BY * B::BX;
+  static constexpr int LW = B::BX / 2 + 1;  // label words per row
+  T coef[NN];
+  uint32_t fm[NN];
+  uint32_t labw[B::BY * LW];
+};
+
+// ext index of the first node of row ly of the block at coordinates b
+template <int D>
+__device__ __forceinline__ int64_t block_row_ext(const phj_grid& g, const int (&b)[3], int ly) {
+  using B = Blk<D>;
+  if constexpr (D == 2) {
+    return (int64_t)(b[0] * B::BY + ly + 1) * g.strides[0] + b[1] * B::BX + 1;
+  } else {
+    return (int64_t)(b[0] + 1) * g.strides[0] + (int64_t)(b[1] * B::BY + ly + 1) * g.strides[1] +
+           b[2] * B::BX + 1;
+  }
+}
+
+// Stage block blk (halo tile of v + node inputs) into the warp's buffers as
+// one cp.async group.  Addresses are clamped into the arrays; lanes whose
+// nodes lie outside the grid are masked by the consumer.
+template <int D, typename T, int COST>
+__device__ __forceinline__ void stage_block(const SolveParams& p, const T* __restrict__ v, int blk,
+                                            T* tile, NodeStage<D, T>* ns, int lane) {
+  using B = Blk<D>;
+  using S = TileShape<D>;
+  using NS = NodeStage<D, T>;
+  const phj_grid& g = p.g;
+  const TileGrid& tg = p.tg;
+  int b[3];
+  decode_block<D>(tg, blk, b);
+  if constexpr (D == 2) {
+    const int row0 = b[0] * B::BY, col0 = b[1] * B::BX;
+    const int rmax = (int)g.ext[0] - 1, cmax = (int)g.ext[1] - 1;
+#pragma unroll
+    for (int i0 = 0; i0 < S::N; i0 += 32) {
+      const int i = i0 + lane;
+      if (i0 + 32 <= S::N || i < S::N) {
+        const int r = i / S::C, cc = i - r * S::C;
+        const int64_t off = (int64_t)min(row0 + r, rmax) * g.strides[0] + min(col0 + cc, cmax);
+        cp_async<sizeof(T)>(tile + i, v + off);
+      }
+    }
+  } else {
+    const int bz = b[0], row0 = b[1] * B::BY, col0 = b[2] * B::BX;
+    const int pmax = (int)g.ext[0] - 1, rmax = (int)g.ext[1] - 1, cmax = (int)g.ext[2] - 1;
+#pragma unroll
+    for (int i0 = 0; i0 < S::N; i0 += 32) {
+      const int i = i0 + lane;
+      if (i0 + 32 <= S::N || i < S::N) {
+        const int r = i / S::C, cc = i - r * S::C;
+        const int pl = r / S::RB, rr = r - pl * S::RB;
+        const int64_t off = (int64_t)min(bz + pl, pmax) * g.strides[0] +
+                            (int64_t)min(row0 + rr, rmax) * g.strides[1] + min(col0 + cc, cmax);
+        cp_async<sizeof(T)>(tile + i, v + off);
+      }
+    }
+  }
+  const int64_t nlast = (int64_t)g.ext[0] * g.strides[0] - 1;
+  const bool stage_coef = COST == PHJ_COST_NODE && p.coef != nullptr;
+#pragma unroll
+  for (int i0 = 0; i0 < NS::NN; i0 += 32) {
+    const int i = i0 + lane;
+    if (i0 + 32 <= NS::NN || i < NS::NN) {
+      const int ly = i / B::BX, j = i - ly * B::BX;
+      const int64_t f = min(block_row_ext<D>(g, b, ly) + j, nlast);
+      cp_async<4>(&ns->fm[i], p.fmask + f);
+      if (stage_coef) cp_async<sizeof(T)>(&ns->coef[i], (const T*)p.coef + f);
+    }
+  }
+  const int64_t wmax = (nlast - 1) >> 1;  // last whole 32-bit word of the label array
+  const uint32_t* labw = (const uint32_t*)p.lab;
+#pragma unroll
+  for (int i0 = 0; i0 < B::BY * NS::LW; i0 += 32) {
+    const int i = i0 + lane;
+    if (i0 + 32 <= B::BY * NS::LW || i < B::BY * NS::LW) {
+      const int ly = i / NS::LW, w = i - ly * NS::LW;
+      const int64_t wi = min((block_row_ext<D>(g, b, ly) >> 1) + w, wmax);
+      cp_async<4>(&ns->labw[i], labw + wi);
+    }
+  }
+  cp_async_commit();
+}
+
+// Warp-local running max change of the patch the warp's recent blocks
+// belonged to; flushed into the CTA (or global) per-patch max when the
+// patch changes and at the end of the sweep.
+struct PatchMax {
+  int lab;
+  double m;
+};
+
+__device__ __forceinline__ void flush_patch_max(const SolveParams& p, PatchMax& pm,
+                                                unsigned long long* s_max,
+                                                unsigned long long* gmax_row) {
+  if (pm.lab >= 0 && (threadIdx.x & 31) == 0) {
+    if (p.R <= kSmemPatchReduce) atomicMax(&s_max[pm.lab], dbits(pm.m));
+    else atomicMax(&gmax_row[pm.lab], dbits(pm.m));
+  }
+  pm.lab = -1;
+  pm.m = 0.0;
+}
+
+// One block of the value sweep, processed by one warp from its staged halo
+// tile and node inputs.  `hook` (the next block's loads, deferred marks)
+// runs exactly once.  Returns (warp-uniform) whether any node changed.
+template <int D, typename T, int RULE, int COST, typename Hook>
+__device__ __forceinline__ bool sweep_block(const SolveParams& p, const StencilSmem<D, T>& s,
+                                            int blk, const T* tile, const NodeStage<D, T>* ns,
+                                            T* __restrict__ vout, const int* s_done,
+                                            unsigned long long* s_max, unsigned long long* gmax_row,
+                                            unsigned long long& evals, unsigned long long& exec,
+                                            PatchMax& pm, PhaseTimer& tm, const Hook& hook) {
+  using B = Blk<D>;
+  using NS = NodeStage<D, T>;
+  constexpr int NB = B::NB;
   constexpr int last = D - 1;
   const unsigned FULL = 0xffffffffu;
   const phj_grid& g = p.g;
@@ -409,30 +755,26 @@ __device__ bool sweep_block(const SolveParams& p, const StencilSmem<D, T>& s, in
   const int cls = p.n_classes > 1 ? c[0] : 0;
   const int* os = s.oct + cls * ((1 << D) + 1);
   const int nadm = p.n_real;
+  const int ly = lane / B::LX, lx = lane % B::LX;
+  const int lshift = (int)((f0 - lx * NB) & 1);  // label half-word offset of the row
+  const bool stage_coef = COST == PHJ_COST_NODE && p.coef != nullptr;
+  const T* lt = lane_tile<D>(tile, lane);
 
-  // Issue every per-node load of the block up front (labels, coefficients,
-  // foreign masks, the 3^D value neighbourhood) so their latencies overlap;
-  // out-of-range lanes read a clamped in-bounds address and are masked.
-  const int64_t nlast = (int64_t)g.ext[0] * g.strides[0] - 1;
   int labv[NB];
   uint32_t fm[NB];
   T ncoef[NB];
-  bool in[NB];
-#pragma unroll
-  for (int r = 0; r < NB; ++r) {
-    in[r] = row_ok && c[last] + r < g.shape[last];
-    const int64_t fr = min(f0 + r, nlast);
-    labv[r] = p.lab[fr];
-    fm[r] = p.fmask[fr];
-    ncoef[r] = (COST == PHJ_COST_NODE && p.coef) ? ((const T*)p.coef)[fr] : (T)p.coef0;
-  }
-  Nbhd<D, T, NB> nb;
-  load_nbhd<D, T, NB>(g, vin, c, nb);
   bool comp[NB], copy[NB];
   bool any_comp = false, any_copy = false;
 #pragma unroll
   for (int r = 0; r < NB; ++r) {
-    if (!in[r]) labv[r] = -1;
+    const bool in = row_ok && c[last] + r < g.shape[last];
+    const int j = lx * NB + r;
+    const int hw = lshift + j;
+    const uint32_t word = ns->labw[ly * NS::LW + (hw >> 1)];
+    const int lab = (int)(int16_t)(uint16_t)(word >> ((hw & 1) * 16));
+    labv[r] = in ? lab : -1;
+    fm[r] = ns->fm[ly * B::BX + j];
+    ncoef[r] = stage_coef ? ns->coef[ly * B::BX + j] : (T)p.coef0;
     comp[r] = false;
     copy[r] = false;
     if (labv[r] >= 0) {
@@ -454,7 +796,9 @@ __device__ bool sweep_block(const SolveParams& p, const StencilSmem<D, T>& s, in
   const bool per0 = g.periodic[0] != 0;
   const int64_t ghost_shift = M0 * g.strides[0];
 
-  if (__any_sync(FULL, any_comp)) {
+  const bool warp_comp = __any_sync(FULL, any_comp);
+  tm.mark(2);
+  if (warp_comp) {
     MinAcc<T> mn[NB];
     T best[NB];
     int bidx[NB];
@@ -467,17 +811,21 @@ __device__ bool sweep_block(const SolveParams& p, const StencilSmem<D, T>& s, in
     uint32_t fmo = 0;
 #pragma unroll
     for (int r = 0; r < NB; ++r) fmo |= fm[r];
+    int n_ent;
     if (__any_sync(FULL, fmo != 0))
-      EvalAll<D, T, NB, RULE, COST, true, 0>::run(nb, s, os, fm, ncoef, nullptr, mn, best, bidx);
+      n_ent = eval_sweep<D, T, NB, RULE, COST, true>(lt, s, os, fm, ncoef, comp, mn, best, bidx,
+                                                     hook);
     else
-      EvalAll<D, T, NB, RULE, COST, false, 0>::run(nb, s, os, fm, ncoef, nullptr, mn, best, bidx);
+      n_ent = eval_sweep<D, T, NB, RULE, COST, false>(lt, s, os, fm, ncoef, comp, mn, best, bidx,
+                                                      hook);
+    exec += (unsigned long long)n_ent * NB;
 #pragma unroll
     for (int r = 0; r < NB; ++r) best[r] = mn[r].get();
-    constexpr int CR = (D == 2) ? 1 : 4;  // centre row of the register block
+    tm.mark(3);
 #pragma unroll
     for (int r = 0; r < NB; ++r) {
       if (!(comp[r] || copy[r])) continue;
-      const T old = nb.v[CR][r + 1];
+      const T old = (D == 2) ? tile_at<D>(lt, 0, r) : tile_at<D>(lt, 0, 0, r);
       T nv = old;
       if (comp[r]) {
         evals += (unsigned long long)nadm;
@@ -498,22 +846,25 @@ __device__ bool sweep_block(const SolveParams& p, const StencilSmem<D, T>& s, in
         else if (c[0] == M0 - 1) vout[f0 + r - ghost_shift] = nv;
       }
     }
-  } else if (any_copy) {
-    constexpr int CR = (D == 2) ? 1 : 4;
+  } else {
+    hook();
+    if (any_copy) {
 #pragma unroll
-    for (int r = 0; r < NB; ++r) {
-      if (!copy[r]) continue;
-      const T old = nb.v[CR][r + 1];
-      vout[f0 + r] = old;
-      if (per0) {
-        if (c[0] == 0) vout[f0 + r + ghost_shift] = old;
-        else if (c[0] == M0 - 1) vout[f0 + r - ghost_shift] = old;
+      for (int r = 0; r < NB; ++r) {
+        if (!copy[r]) continue;
+        const T old = (D == 2) ? tile_at<D>(lt, 0, r) : tile_at<D>(lt, 0, 0, r);
+        vout[f0 + r] = old;
+        if (per0) {
+          if (c[0] == 0) vout[f0 + r + ghost_shift] = old;
+          else if (c[0] == M0 - 1) vout[f0 + r - ghost_shift] = old;
+        }
       }
     }
   }
 
   // per-patch max change
   const bool wchanged = __any_sync(FULL, changed);
+  tm.mark(4);
   if (wchanged) {
     int l0 = -1;
 #pragma unroll
@@ -529,10 +880,9 @@ __device__ bool sweep_block(const SolveParams& p, const StencilSmem<D, T>& s, in
       for (int r = 0; r < NB; ++r) m = max(m, mych[r]);
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) m = max(m, __shfl_xor_sync(FULL, m, off));
-      if (lane == 0 && m > T(0)) {
-        if (p.R <= kSmemPatchReduce) atomic_max_change(&s_max[lref], m);
-        else atomic_max_change(&gmax_row[lref], m);
-      }
+      if (lref != pm.lab) flush_patch_max(p, pm, s_max, gmax_row);
+      pm.lab = lref;
+      pm.m = max(pm.m, (double)m);
     } else {
 #pragma unroll
       for (int r = 0; r < NB; ++r) {
@@ -543,27 +893,103 @@ __device__ bool sweep_block(const SolveParams& p, const StencilSmem<D, T>& s, in
       }
     }
   }
+  tm.mark(5);
   return wchanged;
+}
+
+// Deferred neighbour marking: a changed block's flag exchanges are issued
+// at its end (stage A), the list slots are reserved with one warp-aggregated
+// atomic at the next block's hook (stage B) and written one block later --
+// no atomic round trip is waited for inside a block.
+template <int D>
+struct MarkQueue {
+  int a_nt, a_old;           // A: neighbour id (-1 none), exchanged flag
+  int b_nt, b_rank, b_base;  // B: reserved slot (b_base on lane 0)
+  bool has_b;
+  __device__ __forceinline__ void init() {
+    a_nt = -1;
+    a_old = 1;
+    b_nt = -1;
+    b_rank = 0;
+    b_base = 0;
+    has_b = false;
+  }
+  __device__ __forceinline__ void issue(const TileGrid& tg, const phj_grid& g, int blk, bool ch,
+                                        int lane, int* flags) {
+    a_nt = -1;
+    if (ch && lane < (D == 2 ? 9 : 27)) {
+      const int nt = neighbour_block<D>(tg, g, blk, lane);
+      if (nt >= 0) {
+        a_nt = nt;
+        a_old = atomicExch(&flags[nt], 1);
+      }
+    }
+  }
+  __device__ __forceinline__ void reserve(int lane, int* cnt) {
+    const bool want = a_nt >= 0 && a_old == 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, want);
+    b_nt = want ? a_nt : -1;
+    b_rank = __popc(bal & ((1u << lane) - 1u));
+    if (bal != 0u && lane == 0) b_base = atomicAdd(cnt, __popc(bal));
+    has_b = bal != 0u;
+    a_nt = -1;
+  }
+  __device__ __forceinline__ void store(int* list) {
+    if (has_b) {
+      const int base = __shfl_sync(0xffffffffu, b_base, 0);
+      if (b_nt >= 0) list[base + b_rank] = b_nt;
+      has_b = false;
+      b_nt = -1;
+    }
+  }
+};
+
+template <int D, typename T>
+__host__ __device__ constexpr int64_t solve_tile_bytes() {
+  return (int64_t)kWarps * 2 * TileShape<D>::N * sizeof(T) +
+         (int64_t)kWarps * 2 * sizeof(NodeStage<D, T>);
 }
 
 template <int D, typename T, int RULE, int COST>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __grid_constant__ SolveParams p) {
+  constexpr int NB = Blk<D>::NB;
+  using S = TileShape<D>;
   extern __shared__ __align__(16) unsigned char smem[];
   cg::grid_group grid = cg::this_grid();
   StencilSmem<D, T> s = carve_stencil<D, T>(smem, p.n_classes, p.nc);
   int* s_done = (int*)(smem + StencilSmem<D, T>::bytes(p.n_classes, p.nc));
   unsigned long long* s_max = (unsigned long long*)(s_done + ((p.R + 1) / 2 * 2));
+  T* tiles = (T*)(smem + align_up(StencilSmem<D, T>::bytes(p.n_classes, p.nc) +
+                                      (int64_t)((p.R + 1) / 2 * 2) * 4 +
+                                      (int64_t)min(p.R, kSmemPatchReduce) * 8,
+                                  16));
+  T* wtile = tiles + (threadIdx.x >> 5) * 2 * S::N;
+  NodeStage<D, T>* wnodes =
+      (NodeStage<D, T>*)(tiles + kWarps * 2 * S::N) + (threadIdx.x >> 5) * 2;
   stage_stencil<D, T, RULE>(s, p.n_classes, p.nc, p.oct_start, p.nzmask, p.weights, p.cost);
   for (int i = threadIdx.x; i < p.R; i += blockDim.x)
     s_done[i] = (p.mine == nullptr || p.mine[i]) ? 0x7fffffff : 0;
   __syncthreads();
-
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
-  unsigned long long evals = 0;
+  unsigned long long evals = 0, exec = 0;
   int blocks_done = 0;
-  int sw = 0, buf = 0;
+  int sw = 0, buf = 0, stage = 0;
   const int nshared = min(p.R, kSmemPatchReduce);
+  const int gwarp = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const int nwarps = gridDim.x * kWarps;
+  // Work items of a sweep: the first is the warp's static index, later ones
+  // are claimed one ahead with an atomic (lane 0 keeps the raw ticket so the
+  // round trip is only waited for at the next item; the first dynamic claim
+  // of a sweep is issued before the previous sweep's barrier).  Block ids
+  // are read one ahead and the next block's tile / node inputs are loaded
+  // during the current block.
+  int ticket = 0;
+  if (lane == 0) ticket = atomicAdd(&p.ws.take[0], 1);
+  MarkQueue<D> mq;
+  mq.init();
+  PhaseTimer tm;
+  tm.start();
   for (;;) {
     const T* vin = (const T*)p.v[buf];
     T* vout = (T*)p.v[buf ^ 1];
@@ -577,28 +1003,42 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __gri
     unsigned long long* gmax_row = p.maxch + (int64_t)sw * p.R;
     for (int i = threadIdx.x; i < nshared; i += blockDim.x) s_max[i] = 0ull;
     __syncthreads();
-    // Work items are claimed two ahead and their block ids read one ahead, so
-    // the claim (atomic) and list-read round trips overlap a block's compute;
-    // the first claim of a warp is its static index.
-    const int gwarp = blockIdx.x * kWarps + (threadIdx.x >> 5);
-    const int nwarps = gridDim.x * kWarps;
     int item = gwarp;
     int blk = item < cnt ? __ldcg(&list[item]) : 0;
-    int nxt_l0 = 0;
-    if (lane == 0) nxt_l0 = nwarps + atomicAdd(take, 1);
+    if (item < cnt) stage_block<D, T, COST>(p, vin, blk, wtile + stage * S::N, wnodes + stage, lane);
+    PatchMax pm{-1, 0.0};
+    tm.mark(0);
     while (item < cnt) {
-      const int nxt = __shfl_sync(FULL, nxt_l0, 0);
+      const int nxt = nwarps + __shfl_sync(FULL, ticket, 0);
       const int nblk = nxt < cnt ? __ldcg(&list[nxt]) : 0;
-      if (lane == 0 && nxt < cnt) nxt_l0 = nwarps + atomicAdd(take, 1);
+      if (lane == 0 && nxt < cnt) ticket = atomicAdd(take, 1);
       if (lane == 0) cur_flags[blk] = 0;
-      const bool ch = sweep_block<D, T, RULE, COST>(p, s, blk, vin, vout, s_done, s_max, gmax_row,
-                                                    evals);
+      cp_async_wait_all();
+      __syncwarp();
+      auto hook = [&]() {
+        mq.store(nxt_list);
+        mq.reserve(lane, nxt_cnt);
+        if (nxt < cnt)
+          stage_block<D, T, COST>(p, vin, nblk, wtile + (stage ^ 1) * S::N, wnodes + (stage ^ 1),
+                                  lane);
+      };
+      tm.mark(1);
+      const bool ch = sweep_block<D, T, RULE, COST>(p, s, blk, wtile + stage * S::N, wnodes + stage,
+                                                    vout, s_done, s_max, gmax_row, evals, exec, pm,
+                                                    tm, hook);
       ++blocks_done;
-      if (ch && lane < (D == 2 ? 9 : 27))
-        mark_neighbour<D>(p.tg, p.g, blk, lane, nxt_flags, nxt_list, nxt_cnt);
+      mq.issue(p.tg, p.g, blk, ch, lane, nxt_flags);
+      tm.mark(6);
+      __syncwarp();  // the buffers of this block are refilled two blocks later
       item = nxt;
       blk = nblk;
+      stage ^= 1;
     }
+    if (lane == 0 && sw + 1 <= p.max_sweeps) ticket = atomicAdd(&p.ws.take[sw + 1], 1);
+    mq.store(nxt_list);
+    mq.reserve(lane, nxt_cnt);
+    mq.store(nxt_list);
+    flush_patch_max(p, pm, s_max, gmax_row);
     __syncthreads();
     for (int i = threadIdx.x; i < nshared; i += blockDim.x)
       if (s_max[i]) atomicMax(&gmax_row[i], s_max[i]);
@@ -614,8 +1054,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __gri
       }
     }
     const int any_pending = __syncthreads_or(pending);
+    tm.mark(7);
     if (!any_pending || sw >= p.max_sweeps) break;
   }
+#ifdef PHJ_TIMING
+  if (lane == 0)
+    for (int i = 0; i < 8; ++i) atomicAdd(&g_phase_cycles[i], tm.acc[i]);
+#endif
   if (blockIdx.x == 0) {
     for (int i = threadIdx.x; i < p.R; i += blockDim.x) {
       const int d = s_done[i];
@@ -626,18 +1071,21 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __gri
       p.info[1] = buf;
     }
   }
-  __shared__ unsigned long long s_ev;
+  __shared__ unsigned long long s_ev, s_ex;
   __shared__ int s_blk;
   if (threadIdx.x == 0) {
     s_ev = 0;
+    s_ex = 0;
     s_blk = 0;
   }
   __syncthreads();
   atomicAdd(&s_ev, evals);
+  atomicAdd(&s_ex, exec);
   if (lane == 0) atomicAdd(&s_blk, blocks_done);
   __syncthreads();
   if (threadIdx.x == 0) {
-    atomicAdd(p.evals, s_ev);
+    atomicAdd(&p.evals[0], s_ev);
+    atomicAdd(&p.evals[1], s_ex);
     atomicAdd(&p.info[2], s_blk);
   }
 }
@@ -997,7 +1445,8 @@ __global__ void __launch_bounds__(kThreads) feedback_kernel(const __grid_constan
       best[r] = big_value<T>();
       bidx[r] = 0x7fffffff;
     }
-    EvalAll<D, T, NB, RULE, COST, true, 1>::run(nb, s, os, fm, ncoef, s_ctrl, mn, best, bidx);
+    EvalAll<D, T, NB, RULE, COST, true, 1>::run(nb, s, os, fm, ncoef, s_ctrl, mn, best, bidx,
+                                                 NoHook());
 #pragma unroll
     for (int r = 0; r < NB; ++r) {
       if (!comp[r]) continue;
@@ -1139,15 +1588,18 @@ static int solve_impl(const phj_solve_args* a) {
   PHJ_CUDA(cudaMemsetAsync(a->workspace, 0, ws_bytes, stream));
   PHJ_CUDA(cudaMemsetAsync(a->maxch_hist, 0, sizeof(double) * (size_t)a->max_sweeps * a->n_patches,
                            stream));
-  PHJ_CUDA(cudaMemsetAsync(a->evals, 0, sizeof(unsigned long long), stream));
+  PHJ_CUDA(cudaMemsetAsync(a->evals, 0, 2 * sizeof(unsigned long long), stream));
   PHJ_CUDA(cudaMemsetAsync(a->info, 0, 4 * sizeof(int32_t), stream));
   build_list_kernel<D><<<(p.tg.total + kWarps - 1) / kWarps, kThreads, 0, stream>>>(
       p.g, p.tg, p.lab, p.mine, p.ws.flags[0], p.ws.list[0], p.ws.counts, 0, nullptr, nullptr,
       nullptr, 0ull);
   phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
-  size_t smem = (size_t)StencilSmem<D, T>::bytes(p.n_classes, p.nc) +
-                (size_t)((p.R + 1) / 2 * 2) * 4 + (size_t)std::min(p.R, kSmemPatchReduce) * 8 + 16;
+  size_t smem = (size_t)align_up(StencilSmem<D, T>::bytes(p.n_classes, p.nc) +
+                                     (int64_t)((p.R + 1) / 2 * 2) * 4 +
+                                     (int64_t)std::min(p.R, kSmemPatchReduce) * 8,
+                                 16) +
+                (size_t)solve_tile_bytes<D, T>();
   void* args[] = {(void*)&p};
   int launched = 0;
   int rc = coop_launch(solve_kernel<D, T, RULE, COST>, (p.tg.total + kWarps - 1) / kWarps, smem,
@@ -1157,6 +1609,16 @@ static int solve_impl(const phj_solve_args* a) {
   return PHJ_OK;
 }
 
+#ifdef PHJ_TIMING
+// diagnostic: summed per-warp cycles of the solve kernel phases since the last call
+extern "C" int phj_dbg_phase_cycles(unsigned long long* out) {
+  PHJ_CUDA(cudaMemcpyFromSymbol(out, g_phase_cycles, 8 * sizeof(unsigned long long)));
+  unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  PHJ_CUDA(cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z)));
+  return PHJ_OK;
+}
+#endif
+
 extern "C" int phj_solve(const phj_solve_args* a) {
   if (!a || (a->grid.dim != 2 && a->grid.dim != 3) || !a->v0 || !a->v1 || !a->lab || !a->fmask ||
       !a->workspace || !a->maxch_hist || !a->patch_sweeps || !a->evals || !a->info) {
@@ -1165,6 +1627,10 @@ extern "C" int phj_solve(const phj_solve_args* a) {
   }
   if (a->n_patches < 1 || a->n_patches > kMaxPatches || a->max_sweeps < 1) {
     phj_set_error("phj_solve: n_patches must be in [1, %d], max_sweeps >= 1", kMaxPatches);
+    return PHJ_ERR_ARG;
+  }
+  if (((uintptr_t)a->lab & 3) != 0) {
+    phj_set_error("phj_solve: lab must be 4-byte aligned (staged as 32-bit words)");
     return PHJ_ERR_ARG;
   }
   if (a->grid.periodic[1] || a->grid.periodic[2]) {

@@ -326,6 +326,7 @@ def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Te
     warnings = []
     stats = []
     performed = 0
+    executed = 0
     kernel_ms = 0.0
     sweeps_total = 0
     tiles_total = 0
@@ -336,6 +337,7 @@ def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Te
                            max_sweeps=cfg.sweep_limit(plan.grid), mine=mine)
         out = res.values
         performed = res.evals
+        executed = res.executed
         kernel_ms += res.device_ms
         sweeps_total = int(res.info[0])
         tiles_total = int(res.info[2])
@@ -374,6 +376,7 @@ def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Te
             oi = plan.interior_int(out)
             oi.copy_(torch.where(own, plan.interior_int(res.values), oi))
             performed += res.evals
+            executed += res.executed
             kernel_ms += res.device_ms
             sweeps_total += int(res.info[0])
             stats.append(stats_for_patch(res, 0, int(sizes[j]), plan.n_adm, cfg.tol))
@@ -390,7 +393,8 @@ def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Te
     blocked = (col3 < 0) & (col3 != TARGET)
     oi.copy_(torch.where(blocked, torch.full_like(oi, unr), oi))
     _sync_periodic(plan, out)
-    return out, stats, warnings, {"performed": performed, "kernel_ms": kernel_ms,
+    return out, stats, warnings, {"performed": performed, "executed": executed,
+                                  "kernel_ms": kernel_ms,
                                   "sweeps": sweeps_total, "tiles": tiles_total,
                                   "block_counts": block_counts}
 

@@ -375,6 +375,7 @@ class DeviceSolveResult:
     info: np.ndarray
     device_ms: float = 0.0
     block_counts: Optional[np.ndarray] = None
+    executed: int = 0              # stencil-entry evaluations run (after octant pruning)
 
 
 def device_solve(plan: StencilPlan, work: torch.Tensor, lab: torch.Tensor, fmask: torch.Tensor,
@@ -388,7 +389,7 @@ def device_solve(plan: StencilPlan, work: torch.Tensor, lab: torch.Tensor, fmask
     ws = torch.empty(int(wsb), dtype=torch.uint8, device=dev)
     ps = torch.zeros(n_patches, dtype=torch.int32, device=dev)
     mc = torch.zeros(max_sweeps * n_patches, dtype=torch.float64, device=dev)
-    ev = torch.zeros(1, dtype=torch.int64, device=dev)
+    ev = torch.zeros(2, dtype=torch.int64, device=dev)
     info = torch.zeros(4, dtype=torch.int32, device=dev)
     coef, coef0 = plan.coef(rule, dtype)
     a = _lib.SolveArgs()
@@ -419,8 +420,9 @@ def device_solve(plan: StencilPlan, work: torch.Tensor, lab: torch.Tensor, fmask
     e1.record()
     info_h = info.cpu().numpy()
     res = v1 if int(info_h[1]) == 1 else work
+    ev_h = ev.cpu().numpy()
     out = DeviceSolveResult(res, ps.cpu().numpy(), mc.view(max_sweeps, n_patches).cpu().numpy(),
-                            int(ev.item()), info_h)
+                            int(ev_h[0]), info_h, executed=int(ev_h[1]))
     out.device_ms = e0.elapsed_time(e1)
     out.block_counts = active_blocks_per_sweep(plan, ws, max_sweeps, int(info_h[0]))
     return out
