@@ -16,9 +16,11 @@ time-to-converge.  Units = candidate evaluations (node x control x sweep,
   host inputs (problem description -> device tables: H2D) to the value field
   on the host (D2H), all inside the timed region.
 * ``roofline`` -- dominant kernel = the fine patch solve launch; algorithmic
-  FP64 (FP32) flops per candidate 2*2^d + 1 x performed
-  candidates / its CUDA-event duration, against the FP pipe peak measured
-  here with ``phj_peak_flops`` (MEASURED_PEAKS.json has no FP64/FP32 figure).
+  FP64 (FP32) flops per candidate 2*2^d + 1 x candidates the
+  kernel executed (after exact octant pruning) / its CUDA-event duration,
+  against the FP pipe peak measured here with ``phj_peak_flops``
+  (MEASURED_PEAKS.json has no FP64/FP32 figure); ``logical_tflops`` counts
+  every admissible control of every swept node instead.
 * ``cpu_baseline`` -- the C oracle port (oracle/phj_oracle.c, reference
   update rule, OpenMP over all host cores) timed on Jacobi sweeps of the same
   fine grid (bounded sample), rank 0 at N=1.
@@ -242,6 +244,7 @@ def run_ours(args):
     clk.start()
     l0 = lib.phj_launch_count()
     tot_ms, perf, dense, kern_ms, kern_evals, patch_sweeps = 0.0, 0, 0, 0.0, 0, 0
+    kern_exec = 0
     res = None
     for _ in range(args.steps):
         res, ms = step(True)
@@ -251,6 +254,7 @@ def run_ours(args):
         k = res.stats.kernels.get("patch_solve", {})
         kern_ms += k.get("kernel_ms", 0.0)
         kern_evals += k.get("performed", 0)
+        kern_exec += k.get("executed", 0)
         patch_sweeps = k.get("sweeps", 0)
     launches = lib.phj_launch_count() - l0
     clocks = clk.stop()
@@ -260,9 +264,10 @@ def run_ours(args):
         t = torch.tensor([tot_ms, kern_ms], device="cuda", dtype=torch.float64)
         td.all_reduce(t, op=td.ReduceOp.MAX)
         tot_ms_max, kern_ms_max = t.tolist()
-        c = torch.tensor([perf, dense, kern_evals, launches], device="cuda", dtype=torch.float64)
+        c = torch.tensor([perf, dense, kern_evals, kern_exec, launches], device="cuda",
+                         dtype=torch.float64)
         td.all_reduce(c, op=td.ReduceOp.SUM)
-        perf, dense, kern_evals, launches = [int(x) for x in c.tolist()]
+        perf, dense, kern_evals, kern_exec, launches = [int(x) for x in c.tolist()]
     else:
         tot_ms_max, kern_ms_max = tot_ms, kern_ms
     value = perf / (tot_ms_max * 1e-3)
@@ -297,7 +302,11 @@ def run_ours(args):
         return
     peak = measure_peak(args.dtype)
     fl = _flops_per_candidate(dim)
-    achieved = kern_evals * fl / (kern_ms_max * 1e-3) / 1e12 if kern_ms_max > 0 else 0.0
+    # hardware work: stencil entries the kernel really evaluated (after octant
+    # pruning, incl. padding and masked lanes); the logical rate (every
+    # admissible control of every swept node) is reported beside it
+    achieved = kern_exec * fl / (kern_ms_max * 1e-3) / 1e12 if kern_ms_max > 0 else 0.0
+    logical = kern_evals * fl / (kern_ms_max * 1e-3) / 1e12 if kern_ms_max > 0 else 0.0
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
@@ -333,6 +342,9 @@ def run_ours(args):
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak if peak else None, "traffic": traffic,
                      "flops_per_candidate": fl,
+                     "executed_candidates": kern_exec // max(1, args.steps),
+                     "logical_candidates": kern_evals // max(1, args.steps),
+                     "logical_tflops": logical,
                      "peak_source": "measured here: phj_peak_flops FMA-chain probe"},
         "cpu_baseline": cpu,
         "clocks": clocks,

@@ -73,8 +73,11 @@ typedef struct phj_grid {
 } phj_grid;
 
 /* entries evaluated per inner-loop iteration; each octant group of a class
- * holds a multiple of this many entries */
-#define PHJ_UNROLL(dim) ((dim) == 2 ? 4 : 2)
+ * holds a multiple of this many entries (query a build with phj_unroll) */
+#ifndef PHJ_UNROLL3
+#define PHJ_UNROLL3 2
+#endif
+#define PHJ_UNROLL(dim) ((dim) == 2 ? 4 : PHJ_UNROLL3)
 
 /* Node-independent interpolation stencils, one set per class (class index =
  * interior index along internal axis 0 when n_classes > 1).  Entries of a
@@ -124,6 +127,8 @@ typedef struct phj_solve_args {
 } phj_solve_args;
 
 int64_t phj_solve_workspace_bytes(const phj_grid* g, int32_t n_patches, int32_t max_sweeps);
+/* PHJ_UNROLL(dim) this library was built with (octant-group padding) */
+int32_t phj_unroll(int32_t dim);
 /* number of warp blocks (work/activity units) of a grid (diagnostics) */
 int64_t phj_blocks_total(const phj_grid* g);
 int phj_solve(const phj_solve_args* a);

@@ -40,8 +40,12 @@ class Stencil(ctypes.Structure):
 
 
 def unroll(dim: int) -> int:
-    """PHJ_UNROLL(dim): octant groups are padded to a multiple of this."""
-    return 4 if dim == 2 else 2
+    """PHJ_UNROLL(dim) of the loaded build: octant groups are padded to a
+    multiple of this (header default when the library is not built)."""
+    try:
+        return int(load().phj_unroll(int(dim)))
+    except (PhjError, OSError):
+        return 4 if dim == 2 else 2
 
 
 class SolveArgs(ctypes.Structure):
@@ -72,7 +76,7 @@ class SpeedModel(ctypes.Structure):
 
 #: every symbol include/phj.h declares (checked by the CPU test suite)
 EXPORTS = (
-    "phj_solve_workspace_bytes", "phj_blocks_total", "phj_solve", "phj_fmask_from_labels",
+    "phj_solve_workspace_bytes", "phj_unroll", "phj_blocks_total", "phj_solve", "phj_fmask_from_labels",
     "phj_fmask_from_hard",
     "phj_feedback", "phj_transport", "phj_lift", "phj_argmax_update", "phj_argmax_colors",
     "phj_assemble_codes",
@@ -102,6 +106,7 @@ def load() -> ctypes.CDLL:
     sig = {
         "phj_solve_workspace_bytes": (I64, [P, I32, I32]),
         "phj_blocks_total": (I64, [P]),
+        "phj_unroll": (I32, [I32]),
         "phj_solve": (ctypes.c_int, [P]),
         "phj_fmask_from_labels": (ctypes.c_int, [P, P, P, P]),
         "phj_fmask_from_hard": (ctypes.c_int, [P, P, P, P]),

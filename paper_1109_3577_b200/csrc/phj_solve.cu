@@ -243,7 +243,7 @@ __device__ __forceinline__ T finish_cand(T acc, T ca, T cb, T ncoef, uint32_t fm
 // convex combinations of non-negative values plus non-negative costs), which
 // keeps the FP64 pipe for the interpolation FMAs; fp32 uses FMNMX.
 #ifndef PHJ_MIN_INT
-#define PHJ_MIN_INT 1
+#define PHJ_MIN_INT 0
 #endif
 #ifndef PHJ_KUNROLL2
 #define PHJ_KUNROLL2 4
@@ -253,6 +253,9 @@ __device__ __forceinline__ T finish_cand(T acc, T ca, T cb, T ncoef, uint32_t fm
 #endif
 #ifndef PHJ_WPIPE
 #define PHJ_WPIPE 0
+#endif
+#ifndef PHJ_MINU
+#define PHJ_MINU 0
 #endif
 template <typename T>
 struct MinAcc;
@@ -300,6 +303,15 @@ __device__ __forceinline__ void eval_octant(const Src& cell, int O, const Stenci
   constexpr int U = (D == 2) ? PHJ_KUNROLL2 : PHJ_UNROLL(D);  // divides the host padding
   const int e0 = os[O], e1 = os[O + 1];
   if (e0 >= e1) return;
+#if PHJ_MINU
+  // one running min per unrolled entry slot: no cross-slot compare chain
+  // inside the loop, merged into mn after the octant
+  MinAcc<T> mu[U][NB];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int r = 0; r < NB; ++r) mu[u][r].init();
+#endif
   // U entries from e: corner-major order -- U*NB independent FMA chains
   // advance one corner per step, so consecutive FP64 instructions never
   // depend on each other (DFMA latency ~8 cycles, 2-cycle issue per warp).
@@ -334,12 +346,17 @@ __device__ __forceinline__ void eval_octant(const Src& cell, int O, const Stenci
         x[u] = finish_cand<T, RULE, COST, SLOW, MODE>(acc[u][r], ca[u], cb[u], ncoef[r], fm[r],
                                                       nz[u]);
       if constexpr (MODE == 0) {
+#if PHJ_MINU
+#pragma unroll
+        for (int u = 0; u < U; ++u) mu[u][r].take(x[u]);
+#else
         // pairwise tree over the U candidates, one link into the running min
 #pragma unroll
         for (int st = 1; st < U; st <<= 1)
 #pragma unroll
           for (int u = 0; u + st < U; u += 2 * st) x[u] = x[u + st] < x[u] ? x[u + st] : x[u];
         mn[r].take(x[0]);
+#endif
       } else {
 #pragma unroll
         for (int u = 0; u < U; ++u) take_arg<T>(x[u], ci[u], best[r], bidx[r]);
@@ -368,6 +385,14 @@ __device__ __forceinline__ void eval_octant(const Src& cell, int O, const Stenci
     T w[U][NC];
     load(w, e);
     step(w, e);
+  }
+#endif
+#if PHJ_MINU
+  if constexpr (MODE == 0) {
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int r = 0; r < NB; ++r) mn[r].take(mu[u][r].get());
   }
 #endif
 }
@@ -635,79 +660,105 @@ struct NodeStage {
   uint32_t labw[B::BY * LW];
 };
 
-// ext index of the first node of row ly of the block at coordinates b
-template <int D>
-__device__ __forceinline__ int64_t block_row_ext(const phj_grid& g, const int (&b)[3], int ly) {
-  using B = Blk<D>;
-  if constexpr (D == 2) {
-    return (int64_t)(b[0] * B::BY + ly + 1) * g.strides[0] + b[1] * B::BX + 1;
-  } else {
-    return (int64_t)(b[0] + 1) * g.strides[0] + (int64_t)(b[1] * B::BY + ly + 1) * g.strides[1] +
-           b[2] * B::BX + 1;
-  }
-}
-
 // Stage block blk (halo tile of v + node inputs) into the warp's buffers as
-// one cp.async group.  Addresses are clamped into the arrays; lanes whose
-// nodes lie outside the grid are masked by the consumer.
+// one cp.async group.  Lanes own tile row segments (one base address each,
+// immediate column offsets); only blocks at the far grid edge (partial
+// blocks) clamp addresses into the arrays -- lanes whose nodes lie outside
+// the grid are masked by the consumer.
+template <int D>
+struct StagePlan {
+  using B = Blk<D>;
+  using S = TileShape<D>;
+  static constexpr int W = B::BX + 2;  // tile columns
+  static constexpr int seg() {
+    int s = 32 / S::R;
+    while (s > 1 && W % s != 0) --s;
+    return s < 1 ? 1 : s;
+  }
+  static constexpr int SEG = seg();      // lanes per tile row
+  static constexpr int SW = W / SEG;     // columns per lane
+  static constexpr int LPR = 32 / B::BY; // lanes per node row
+  static constexpr int NPL = B::BX / LPR;  // nodes per lane
+  static_assert(S::R * SEG <= 32, "tile rows exceed the warp");
+  static_assert(B::BX % LPR == 0, "node row split");
+};
+
 template <int D, typename T, int COST>
 __device__ __forceinline__ void stage_block(const SolveParams& p, const T* __restrict__ v, int blk,
                                             T* tile, NodeStage<D, T>* ns, int lane) {
   using B = Blk<D>;
   using S = TileShape<D>;
   using NS = NodeStage<D, T>;
+  using P = StagePlan<D>;
   const phj_grid& g = p.g;
-  const TileGrid& tg = p.tg;
   int b[3];
-  decode_block<D>(tg, blk, b);
+  decode_block<D>(p.tg, blk, b);
+  // ext flat index of the tile origin, row stride, extent checks
+  int64_t o, rs, s0x;
+  int row0, col0, rmax, cmax;
+  bool full;
   if constexpr (D == 2) {
-    const int row0 = b[0] * B::BY, col0 = b[1] * B::BX;
-    const int rmax = (int)g.ext[0] - 1, cmax = (int)g.ext[1] - 1;
-#pragma unroll
-    for (int i0 = 0; i0 < S::N; i0 += 32) {
-      const int i = i0 + lane;
-      if (i0 + 32 <= S::N || i < S::N) {
-        const int r = i / S::C, cc = i - r * S::C;
-        const int64_t off = (int64_t)min(row0 + r, rmax) * g.strides[0] + min(col0 + cc, cmax);
-        cp_async<sizeof(T)>(tile + i, v + off);
-      }
-    }
+    row0 = b[0] * B::BY;
+    col0 = b[1] * B::BX;
+    rs = g.strides[0];
+    s0x = 0;
+    o = (int64_t)row0 * rs + col0;
+    rmax = (int)g.ext[0] - 1;
+    cmax = (int)g.ext[1] - 1;
+    full = (b[0] + 1) * B::BY <= g.shape[0] && (b[1] + 1) * B::BX <= g.shape[1];
   } else {
-    const int bz = b[0], row0 = b[1] * B::BY, col0 = b[2] * B::BX;
-    const int pmax = (int)g.ext[0] - 1, rmax = (int)g.ext[1] - 1, cmax = (int)g.ext[2] - 1;
+    row0 = b[1] * B::BY;
+    col0 = b[2] * B::BX;
+    rs = g.strides[1];
+    s0x = g.strides[0];
+    o = (int64_t)b[0] * s0x + (int64_t)row0 * rs + col0;
+    rmax = (int)g.ext[1] - 1;
+    cmax = (int)g.ext[2] - 1;
+    full = (b[1] + 1) * B::BY <= g.shape[1] && (b[2] + 1) * B::BX <= g.shape[2];
+  }
+  // halo tile: lane -> (row, segment)
+  if (lane < S::R * P::SEG) {
+    const int r = lane / P::SEG, sg = lane - r * P::SEG;
+    int pl = 0, rr = r;
+    if constexpr (D == 3) {
+      pl = r / S::RB;
+      rr = r - pl * S::RB;
+    }
+    const int c0 = sg * P::SW;
+    T* dst = tile + r * S::C + c0;
+    if (full) {
+      const T* src = v + o + pl * s0x + (int64_t)rr * rs + c0;
 #pragma unroll
-    for (int i0 = 0; i0 < S::N; i0 += 32) {
-      const int i = i0 + lane;
-      if (i0 + 32 <= S::N || i < S::N) {
-        const int r = i / S::C, cc = i - r * S::C;
-        const int pl = r / S::RB, rr = r - pl * S::RB;
-        const int64_t off = (int64_t)min(bz + pl, pmax) * g.strides[0] +
-                            (int64_t)min(row0 + rr, rmax) * g.strides[1] + min(col0 + cc, cmax);
-        cp_async<sizeof(T)>(tile + i, v + off);
-      }
+      for (int j = 0; j < P::SW; ++j) cp_async<sizeof(T)>(dst + j, src + j);
+    } else {
+      const int rc = min(row0 + rr, rmax) - row0;
+      const T* src = v + o + pl * s0x + (int64_t)rc * rs;
+#pragma unroll
+      for (int j = 0; j < P::SW; ++j)
+        cp_async<sizeof(T)>(dst + j, src + (min(col0 + c0 + j, cmax) - col0));
     }
   }
-  const int64_t nlast = (int64_t)g.ext[0] * g.strides[0] - 1;
-  const bool stage_coef = COST == PHJ_COST_NODE && p.coef != nullptr;
+  // node inputs: lane -> (node row, NPL consecutive nodes, label words)
+  {
+    const int ly = lane / P::LPR, q = lane - ly * P::LPR;
+    const int64_t nlast = (int64_t)g.ext[0] * g.strides[0] - 1;
+    const int64_t fr = o + s0x + rs + 1 + (int64_t)ly * rs;  // ext index of the row's node 0
+    const bool stage_coef = COST == PHJ_COST_NODE && p.coef != nullptr;
+    const int j0 = q * P::NPL;
 #pragma unroll
-  for (int i0 = 0; i0 < NS::NN; i0 += 32) {
-    const int i = i0 + lane;
-    if (i0 + 32 <= NS::NN || i < NS::NN) {
-      const int ly = i / B::BX, j = i - ly * B::BX;
-      const int64_t f = min(block_row_ext<D>(g, b, ly) + j, nlast);
-      cp_async<4>(&ns->fm[i], p.fmask + f);
-      if (stage_coef) cp_async<sizeof(T)>(&ns->coef[i], (const T*)p.coef + f);
+    for (int k = 0; k < P::NPL; ++k) {
+      const int j = j0 + k;
+      const int64_t f = full ? fr + j : min(fr + j, nlast);
+      cp_async<4>(&ns->fm[ly * B::BX + j], p.fmask + f);
+      if (stage_coef) cp_async<sizeof(T)>(&ns->coef[ly * B::BX + j], (const T*)p.coef + f);
     }
-  }
-  const int64_t wmax = (nlast - 1) >> 1;  // last whole 32-bit word of the label array
-  const uint32_t* labw = (const uint32_t*)p.lab;
+    const int64_t wmax = (nlast - 1) >> 1;  // last whole 32-bit word of the label array
+    const uint32_t* labw = (const uint32_t*)p.lab;
+    const int64_t w0 = fr >> 1;
 #pragma unroll
-  for (int i0 = 0; i0 < B::BY * NS::LW; i0 += 32) {
-    const int i = i0 + lane;
-    if (i0 + 32 <= B::BY * NS::LW || i < B::BY * NS::LW) {
-      const int ly = i / NS::LW, w = i - ly * NS::LW;
-      const int64_t wi = min((block_row_ext<D>(g, b, ly) >> 1) + w, wmax);
-      cp_async<4>(&ns->labw[i], labw + wi);
+    for (int w = q; w < NS::LW; w += P::LPR) {
+      const int64_t wi = full ? w0 + w : min(w0 + w, wmax);
+      cp_async<4>(&ns->labw[ly * NS::LW + w], labw + wi);
     }
   }
   cp_async_commit();
@@ -1526,6 +1577,8 @@ extern "C" int64_t phj_blocks_total(const phj_grid* g) {
   if (!g) return -1;
   return g->dim == 2 ? make_tile_grid<2>(*g).total : make_tile_grid<3>(*g).total;
 }
+
+extern "C" int32_t phj_unroll(int32_t dim) { return PHJ_UNROLL(dim); }
 
 extern "C" int64_t phj_solve_workspace_bytes(const phj_grid* g, int32_t n_patches,
                                              int32_t max_sweeps) {

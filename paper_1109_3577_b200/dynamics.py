@@ -159,8 +159,11 @@ def _weights_for(disp: np.ndarray):
 
 
 def unroll(dim: int) -> int:
-    """Entries per kernel inner-loop iteration (PHJ_UNROLL in include/phj.h)."""
-    return 4 if dim == 2 else 2
+    """Entries per kernel inner-loop iteration (PHJ_UNROLL of the built
+    library, include/phj.h)."""
+    from . import _lib
+
+    return _lib.unroll(dim)
 
 
 def build_stencil(disp: np.ndarray, cost: Optional[np.ndarray], admissible: np.ndarray,
