@@ -976,6 +976,20 @@ struct MarkQueue {
       }
     }
   }
+  // transport: OR the changed colours into the neighbours' next masks; the
+  // first setter (old mask 0) appends the block
+  __device__ __forceinline__ void issue_mask(const TileGrid& tg, const phj_grid& g, int blk,
+                                             unsigned long long bits, int lane,
+                                             unsigned long long* masks) {
+    a_nt = -1;
+    if (bits != 0ull && lane < (D == 2 ? 9 : 27)) {
+      const int nt = neighbour_block<D>(tg, g, blk, lane);
+      if (nt >= 0) {
+        a_nt = nt;
+        a_old = atomicOr(&masks[nt], bits) != 0ull;
+      }
+    }
+  }
   __device__ __forceinline__ void reserve(int lane, int* cnt) {
     const bool want = a_nt >= 0 && a_old == 0;
     const unsigned bal = __ballot_sync(0xffffffffu, want);
@@ -1210,8 +1224,11 @@ struct TransportParams {
   unsigned long long* updates;
 };
 
+#ifndef PHJ_TRANSPORT_CTAS
+#define PHJ_TRANSPORT_CTAS 2
+#endif
 template <int D>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm) transport_kernel(const __grid_constant__ TransportParams p) {
+__global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel(const __grid_constant__ TransportParams p) {
   using B = Blk<D>;
   constexpr int NC = 1 << D;
   constexpr int NB = B::NB;
@@ -1256,6 +1273,20 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) transport_kernel(const _
   }
   unsigned long long upd = 0;
   int sw = 0, buf = 0;
+  const int gwarp = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const int nwarps = gridDim.x * kWarps;
+  // Items are claimed two ahead (raw tickets on lane 0, first dynamic claims
+  // of a sweep issued before the previous barrier), block ids read one
+  // ahead, and a block's colour mask and mover entries are loaded while the
+  // previous block is processed: an item's own work is a few FMAs per colour,
+  // so without the lookahead each item would wait on 3 dependent round trips.
+  int ticket = 0, ticket2 = 0;
+  if (lane == 0) {
+    ticket = atomicAdd(&p.ws.take[0], 1);
+    ticket2 = atomicAdd(&p.ws.take[0], 1);
+  }
+  MarkQueue<D> mq;
+  mq.init();
   for (;;) {
     const double* pin = p.phi[buf];
     double* pout = p.phi[buf ^ 1];
@@ -1263,37 +1294,62 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) transport_kernel(const _
     const int* list = p.ws.list[sw & 1];
     int* cur_flags = p.ws.flags[sw & 1];
     unsigned long long* cur_mask = p.ws.cmask[sw & 1];
+    unsigned long long* nxt_mask = p.ws.cmask[(sw + 1) & 1];
+    int* nxt_list = p.ws.list[(sw + 1) & 1];
+    int* nxt_cnt = &p.ws.counts[sw + 1];
     int* take = &p.ws.take[sw];
     for (int i = threadIdx.x; i < R; i += blockDim.x) s_max[i] = 0ull;
     __syncthreads();
-    const int gwarp = blockIdx.x * kWarps + (threadIdx.x >> 5);
-    const int nwarps = gridDim.x * kWarps;
+    // prefetch of one item: its colour mask (lane 0) and mover entries
+    auto prefetch = [&](int b, unsigned long long& pcm, int (&pe)[NB]) {
+      int cc[3];
+      const bool rok = lane_nodes<D>(g, p.tg, b, lane, cc);
+      const int64_t ss = serial_of<D>(g, cc);
+      pcm = 0ull;
+      if (lane == 0) {
+        pcm = __ldcg(&cur_mask[b]);
+        cur_mask[b] = 0ull;
+        cur_flags[b] = 0;
+      }
+#pragma unroll
+      for (int r = 0; r < NB; ++r) {
+        const bool in = rok && cc[last] + r < g.shape[last];
+        pe[r] = in ? __ldg(&p.ent[ss + r]) : -1;
+      }
+    };
     int item = gwarp;
+    int blk = item < cnt ? __ldcg(&list[item]) : 0;
+    int nxt = nwarps + __shfl_sync(FULL, ticket, 0);
+    int nblk = (item < cnt && nxt < cnt) ? __ldcg(&list[nxt]) : 0;
+    if (lane == 0) ticket = ticket2;
+    unsigned long long cm_l0 = 0ull;
+    int e[NB];
+    if (item < cnt) prefetch(blk, cm_l0, e);
     while (item < cnt) {
-      int nxt_l0 = 0;
-      if (lane == 0) nxt_l0 = nwarps + atomicAdd(take, 1);
-      const int blk = __ldcg(&list[item]);
+      // lookahead: ticket of the item after next, next block's inputs
+      const int nn = nwarps + __shfl_sync(FULL, ticket, 0);
+      const int nnblk = (nxt < cnt && nn < cnt) ? __ldcg(&list[nn]) : 0;
+      if (lane == 0 && nxt < cnt && nn < cnt) ticket = atomicAdd(take, 1);
+      unsigned long long ncm_l0 = 0ull;
+      int ne[NB];
+#pragma unroll
+      for (int r = 0; r < NB; ++r) ne[r] = -1;
+      if (nxt < cnt) prefetch(nblk, ncm_l0, ne);
+      mq.store(nxt_list);
+      mq.reserve(lane, nxt_cnt);
+
       // colours active in this block: those a neighbour block changed in the
       // previous sweep (exact per colour, like the block skipping)
-      unsigned long long cm = 0;
-      if (lane == 0) {
-        cm = __ldcg(&cur_mask[blk]);
-        cur_mask[blk] = 0ull;
-        cur_flags[blk] = 0;
-      }
-      cm = __shfl_sync(FULL, cm, 0);
+      const unsigned long long cm = __shfl_sync(FULL, cm_l0, 0);
       int c[3];
       const bool row_ok = lane_nodes<D>(g, p.tg, blk, lane, c);
       const int64_t f0 = ext_flat<D>(g, c);
-      const int64_t s0 = serial_of<D>(g, c);
-      int e[NB];
       int64_t base[NB];
       double w[NB][NC];
       bool any = false;
+      (void)row_ok;
 #pragma unroll
       for (int r = 0; r < NB; ++r) {
-        const bool in = row_ok && c[last] + r < g.shape[last];
-        e[r] = in ? __ldg(&p.ent[s0 + r]) : -1;
         base[r] = f0 + r;
         if (e[r] >= 0) {
           const int oc = s_oct[e[r]];
@@ -1352,11 +1408,23 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) transport_kernel(const _
           }
         }
       }
-      if (changed && lane < (D == 2 ? 9 : 27))
-        mark_neighbour_mask<D>(p.tg, g, blk, lane, changed, p.ws.cmask[(sw + 1) & 1],
-                               p.ws.list[(sw + 1) & 1], &p.ws.counts[sw + 1]);
-      item = __shfl_sync(FULL, nxt_l0, 0);
+      mq.issue_mask(p.tg, g, blk, changed, lane, nxt_mask);
+      item = nxt;
+      blk = nblk;
+      nxt = nn;
+      nblk = nnblk;
+      cm_l0 = ncm_l0;
+#pragma unroll
+      for (int r = 0; r < NB; ++r) e[r] = ne[r];
     }
+    if (lane == 0 && sw + 1 <= p.max_sweeps) {
+      // the two leading claims of the next sweep
+      ticket = atomicAdd(&p.ws.take[sw + 1], 1);
+      ticket2 = atomicAdd(&p.ws.take[sw + 1], 1);
+    }
+    mq.store(nxt_list);
+    mq.reserve(lane, nxt_cnt);
+    mq.store(nxt_list);
     __syncthreads();
     unsigned long long* grow = p.maxch + (int64_t)sw * R;
     for (int i = threadIdx.x; i < R; i += blockDim.x)
