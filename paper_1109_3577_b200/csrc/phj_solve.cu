@@ -1345,7 +1345,6 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
       const bool row_ok = lane_nodes<D>(g, p.tg, blk, lane, c);
       const int64_t f0 = ext_flat<D>(g, c);
       int64_t base[NB];
-      double w[NB][NC];
       bool any = false;
       (void)row_ok;
 #pragma unroll
@@ -1356,55 +1355,89 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
 #pragma unroll
           for (int ax = 0; ax < D; ++ax)
             if (!((oc >> ax) & 1)) base[r] -= g.strides[ax];
-#pragma unroll
-          for (int k = 0; k < NC; ++k) w[r][k] = s_w[k * wpitch + e[r]];
           any = true;
           ++upd;
         }
       }
       unsigned long long changed = 0;
       if (__any_sync(FULL, any)) {
+        // the node itself is corner kself of its foot cell (feet lie in one of
+        // the 2^D cells around the node): its old value comes with the corners
+        int kself[NB];
+#pragma unroll
+        for (int r = 0; r < NB; ++r) kself[r] = e[r] >= 0 ? (~s_oct[e[r]]) & (NC - 1) : 0;
+        // colours in batches of CB: all corner loads of a batch are in flight
+        // together (the sweep is latency-bound on these gathers)
+#ifndef PHJ_TCB2
+#define PHJ_TCB2 1
+#endif
+        constexpr int CB = (D == 2) ? PHJ_TCB2 : 2;
         const bool masked = R <= 64;
-        unsigned long long todo = cm;
-        for (int jj = 0; masked ? (todo != 0ull) : (jj < R); ++jj) {
-          int j = jj;
-          if (masked) {
-            j = __ffsll((long long)todo) - 1;
-            todo &= todo - 1;
+        unsigned long long todo = masked ? cm : 0ull;
+        int jnext = 0;  // unmasked (R > 64): every colour in order
+        for (;;) {
+          int js[CB];
+          bool anyj = false;
+#pragma unroll
+          for (int q = 0; q < CB; ++q) {
+            if (masked) {
+              js[q] = todo ? __ffsll((long long)todo) - 1 : -1;
+              todo &= todo ? todo - 1 : 0ull;
+            } else {
+              js[q] = jnext < R ? jnext : -1;
+              ++jnext;
+            }
+            anyj |= js[q] >= 0;
           }
-          const bool live = s_done[j] == 0x7fffffff;
-          const double* pj = pin + (int64_t)j * p.plane;
-          double* qj = pout + (int64_t)j * p.plane;
-          double lmax = 0.0;
-          double acc[NB], old[NB];
+          if (!anyj) break;
+          double cv[CB][NB][NC];
 #pragma unroll
-          for (int r = 0; r < NB; ++r) {
-            acc[r] = 0.0;
-            old[r] = 0.0;
-            if (e[r] >= 0) {
-              old[r] = pj[f0 + r];
+          for (int q = 0; q < CB; ++q) {
+            const double* pj = pin + (int64_t)max(js[q], 0) * p.plane;
 #pragma unroll
-              for (int k = 0; k < NC; ++k) acc[r] = fma(w[r][k], pj[base[r] + coff[k]], acc[r]);
+            for (int r = 0; r < NB; ++r)
+#pragma unroll
+              for (int k = 0; k < NC; ++k)
+                cv[q][r][k] = (js[q] >= 0 && e[r] >= 0) ? pj[base[r] + coff[k]] : 0.0;
+          }
+          double lmax[CB];
+#pragma unroll
+          for (int q = 0; q < CB; ++q) {
+            lmax[q] = 0.0;
+            if (js[q] < 0) continue;
+            const int j = js[q];
+            const bool live = s_done[j] == 0x7fffffff;
+            double* qj = pout + (int64_t)j * p.plane;
+#pragma unroll
+            for (int r = 0; r < NB; ++r) {
+              if (e[r] < 0) continue;
+              double acc = 0.0, old = cv[q][r][0];
+#pragma unroll
+              for (int k = 0; k < NC; ++k) {
+                acc = fma(s_w[k * wpitch + e[r]], cv[q][r][k], acc);
+                if (k > 0 && k == kself[r]) old = cv[q][r][k];
+              }
+              const double nv = live ? acc : old;
+              lmax[q] = fmax(lmax[q], fabs(old - nv));
+              qj[f0 + r] = nv;
+              if (per0) {
+                if (c[0] == 0) qj[f0 + r + ghost_shift] = nv;
+                else if (c[0] == M0 - 1) qj[f0 + r - ghost_shift] = nv;
+              }
             }
           }
 #pragma unroll
-          for (int r = 0; r < NB; ++r) {
-            if (e[r] < 0) continue;
-            const double nv = live ? acc[r] : old[r];
-            lmax = fmax(lmax, fabs(old[r] - nv));
-            qj[f0 + r] = nv;
-            if (per0) {
-              if (c[0] == 0) qj[f0 + r + ghost_shift] = nv;
-              else if (c[0] == M0 - 1) qj[f0 + r - ghost_shift] = nv;
-            }
-          }
-          if (__any_sync(FULL, lmax > 0.0)) {
+          for (int off = 16; off > 0; off >>= 1)
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) lmax = fmax(lmax, __shfl_xor_sync(FULL, lmax, off));
-            if (lane == 0) atomicMax(&s_max[j], dbits(lmax));
+            for (int q = 0; q < CB; ++q) lmax[q] = fmax(lmax[q], __shfl_xor_sync(FULL, lmax[q], off));
+#pragma unroll
+          for (int q = 0; q < CB; ++q) {
+            if (js[q] < 0 || !(lmax[q] > 0.0)) continue;
+            const int j = js[q];
+            if (lane == 0) atomicMax(&s_max[j], dbits(lmax[q]));
             // activity threshold: changes <= act_eps (a small fraction of the
             // stopping tolerance) do not re-activate the neighbourhood
-            if (lmax > p.act_eps) changed |= (j < 64) ? (1ull << j) : ~0ull;
+            if (lmax[q] > p.act_eps) changed |= (j < 64) ? (1ull << j) : ~0ull;
           }
         }
       }
