@@ -33,12 +33,12 @@ namespace phj {
 
 // Optional per-phase cycle accounting (diagnostic builds only, -DPHJ_TIMING).
 #ifdef PHJ_TIMING
-__device__ unsigned long long g_phase_cycles[8];
+__device__ unsigned long long g_phase_cycles[12];
 struct PhaseTimer {
-  unsigned long long acc[8];
+  unsigned long long acc[12];
   long long prev;
   __device__ void start() {
-    for (int i = 0; i < 8; ++i) acc[i] = 0;
+    for (int i = 0; i < 12; ++i) acc[i] = 0;
     prev = clock64();
   }
   __device__ void mark(int i) {
@@ -1104,10 +1104,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __gri
     mq.reserve(lane, nxt_cnt);
     mq.store(nxt_list);
     flush_patch_max(p, pm, s_max, gmax_row);
+    tm.mark(8);
     __syncthreads();
+    tm.mark(9);
     for (int i = threadIdx.x; i < nshared; i += blockDim.x)
       if (s_max[i]) atomicMax(&gmax_row[i], s_max[i]);
     grid.sync();
+    tm.mark(10);
     ++sw;
     buf ^= 1;
     int pending = 0;
@@ -1124,7 +1127,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __gri
   }
 #ifdef PHJ_TIMING
   if (lane == 0)
-    for (int i = 0; i < 8; ++i) atomicAdd(&g_phase_cycles[i], tm.acc[i]);
+    for (int i = 0; i < 12; ++i) atomicAdd(&g_phase_cycles[i], tm.acc[i]);
 #endif
   if (blockIdx.x == 0) {
     for (int i = threadIdx.x; i < p.R; i += blockDim.x) {
@@ -1766,8 +1769,8 @@ static int solve_impl(const phj_solve_args* a) {
 #ifdef PHJ_TIMING
 // diagnostic: summed per-warp cycles of the solve kernel phases since the last call
 extern "C" int phj_dbg_phase_cycles(unsigned long long* out) {
-  PHJ_CUDA(cudaMemcpyFromSymbol(out, g_phase_cycles, 8 * sizeof(unsigned long long)));
-  unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  PHJ_CUDA(cudaMemcpyFromSymbol(out, g_phase_cycles, 12 * sizeof(unsigned long long)));
+  unsigned long long z[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   PHJ_CUDA(cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z)));
   return PHJ_OK;
 }

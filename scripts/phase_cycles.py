@@ -23,8 +23,9 @@ plans = patchy.make_plans(w.spec, w.pcfg)
 lib = _lib.load()
 fn = lib.phj_dbg_phase_cycles
 fn.argtypes = [ctypes.c_void_p]
-buf = (ctypes.c_ulonglong * 8)()
-names = ["sweep_prologue", "fetch", "labels", "eval", "store", "maxch", "mark", "barrier"]
+buf = (ctypes.c_ulonglong * 12)()
+names = ["sweep_prologue", "fetch", "labels", "eval", "store", "maxch", "mark", "post_sweep",
+         "sweep_flush", "cta_wait", "grid_sync", "-"]
 for i in range(2):
     fn(buf)
     phj.run_patchy(w.spec, w.pcfg, w.cfg, plans=plans, outputs=False)
