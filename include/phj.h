@@ -123,8 +123,14 @@ typedef struct phj_solve_args {
                                  evaluations executed (incl. padding, after pruning) */
   int32_t* info;              /* out [4]: total sweeps, index of result buffer,
                                  tiles processed, launches */
+  int32_t options;            /* PHJ_SOLVE_* bits, 0 = defaults */
+  int32_t pad_;
   void* stream;               /* cudaStream_t */
 } phj_solve_args;
+
+/* phj_solve_args.options: evaluate every octant (disable the exact octant
+ * pruning; for verification -- results are bit-identical either way) */
+#define PHJ_SOLVE_NO_PRUNE 1
 
 int64_t phj_solve_workspace_bytes(const phj_grid* g, int32_t n_patches, int32_t max_sweeps);
 /* PHJ_UNROLL(dim) this library was built with (octant-group padding) */

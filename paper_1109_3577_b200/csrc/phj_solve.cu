@@ -76,6 +76,7 @@ struct SolveParams {
   int32_t* patch_sweeps;
   unsigned long long* evals;
   int32_t* info;
+  int prune;  // exact octant pruning on (PHJ_SOLVE_NO_PRUNE clears it)
 };
 
 template <int D, typename T>
@@ -569,13 +570,14 @@ __device__ __forceinline__ int preferred_octant(const T* lt) {
 // per-control costs every octant in order.  `hook` runs once, after the
 // first octant.  Returns the stencil entries evaluated per node.
 template <int D, typename T, int NB, int RULE, int COST, bool SLOW, typename Hook>
-__device__ __forceinline__ int eval_sweep(const T* lt, const StencilSmem<D, T>& s,
+__device__ __forceinline__ int eval_sweep(const T* lt, bool prune_on, const StencilSmem<D, T>& s,
                                           const int* os, const uint32_t (&fm)[NB],
                                           const T (&ncoef)[NB], const bool (&comp)[NB],
                                           MinAcc<T> (&mn)[NB], T (&best)[NB], int (&bidx)[NB],
                                           const Hook& hook) {
-  constexpr bool PRUNE = COST == PHJ_COST_NODE && PHJ_PRUNE;
-  const int first = PRUNE ? preferred_octant<D, T>(lt) : 0;
+  constexpr bool CAN_PRUNE = COST == PHJ_COST_NODE && PHJ_PRUNE;
+  const bool prune = CAN_PRUNE && prune_on;
+  const int first = prune ? preferred_octant<D, T>(lt) : 0;
   OctNb<D, T, NB> cell;
   cell.load(lt, first);
   eval_octant<D, T, NB, RULE, COST, SLOW, 0>(cell, first, s, os, fm, ncoef, nullptr, mn, best,
@@ -586,7 +588,7 @@ __device__ __forceinline__ int eval_sweep(const T* lt, const StencilSmem<D, T>& 
   for (int O = 0; O < (1 << D); ++O) {
     if (O == first) continue;
     cell.load(lt, O);
-    if (PRUNE && !__any_sync(0xffffffffu, octant_needed<D, T, NB>(cell, comp, mn))) continue;
+    if (prune && !__any_sync(0xffffffffu, octant_needed<D, T, NB>(cell, comp, mn))) continue;
     eval_octant<D, T, NB, RULE, COST, SLOW, 0>(cell, O, s, os, fm, ncoef, nullptr, mn, best, bidx);
     n_ent += os[O + 1] - os[O];
   }
@@ -864,11 +866,11 @@ __device__ __forceinline__ bool sweep_block(const SolveParams& p, const StencilS
     for (int r = 0; r < NB; ++r) fmo |= fm[r];
     int n_ent;
     if (__any_sync(FULL, fmo != 0))
-      n_ent = eval_sweep<D, T, NB, RULE, COST, true>(lt, s, os, fm, ncoef, comp, mn, best, bidx,
-                                                     hook);
+      n_ent = eval_sweep<D, T, NB, RULE, COST, true>(lt, p.prune != 0, s, os, fm, ncoef, comp, mn,
+                                                     best, bidx, hook);
     else
-      n_ent = eval_sweep<D, T, NB, RULE, COST, false>(lt, s, os, fm, ncoef, comp, mn, best, bidx,
-                                                      hook);
+      n_ent = eval_sweep<D, T, NB, RULE, COST, false>(lt, p.prune != 0, s, os, fm, ncoef, comp, mn,
+                                                      best, bidx, hook);
     exec += (unsigned long long)n_ent * NB;
 #pragma unroll
     for (int r = 0; r < NB; ++r) best[r] = mn[r].get();
@@ -1741,6 +1743,7 @@ static int solve_impl(const phj_solve_args* a) {
   p.patch_sweeps = a->patch_sweeps;
   p.evals = a->evals;
   p.info = a->info;
+  p.prune = (a->options & PHJ_SOLVE_NO_PRUNE) ? 0 : 1;
   const int64_t ws_bytes = workspace_bytes<D>(a->grid, a->max_sweeps);
   PHJ_CUDA(cudaMemsetAsync(a->workspace, 0, ws_bytes, stream));
   PHJ_CUDA(cudaMemsetAsync(a->maxch_hist, 0, sizeof(double) * (size_t)a->max_sweeps * a->n_patches,

@@ -380,7 +380,8 @@ class DeviceSolveResult:
 
 def device_solve(plan: StencilPlan, work: torch.Tensor, lab: torch.Tensor, fmask: torch.Tensor,
                  n_patches: int, *, rule: str, dtype: str, tol: float, max_sweeps: int,
-                 mine: Optional[torch.Tensor] = None, sync: bool = True) -> DeviceSolveResult:
+                 mine: Optional[torch.Tensor] = None, sync: bool = True,
+                 prune: bool = True) -> DeviceSolveResult:
     """One phj_solve launch: all patches of `lab`, to per-patch convergence."""
     lib = _lib.load()
     dev = plan.device
@@ -412,6 +413,7 @@ def device_solve(plan: StencilPlan, work: torch.Tensor, lab: torch.Tensor, fmask
     a.maxch_hist = _lib.ptr(mc)
     a.evals = _lib.ptr(ev)
     a.info = _lib.ptr(info)
+    a.options = 0 if prune else _lib.SOLVE_NO_PRUNE
     a.stream = _lib.stream_handle()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
