@@ -1,11 +1,19 @@
-"""Multi-GPU patch scheduling.
+"""Multi-GPU scheduling.
 
 Patches are invariant under the optimal dynamics and need no transmission
 conditions, so ranks solve disjoint patch sets with no halo exchange; the
-only collective is the final gather of v, an element-wise MIN all-reduce
-(every rank's non-owned nodes still hold the unreached value, which is >=
-the owner's result; target nodes are 0 everywhere).  Patches are placed by
-LPT (longest processing time first) on node counts, as north_star asks.
+final gather of v is an element-wise MIN all-reduce (every rank's non-owned
+nodes still hold the unreached value, which is >= the owner's result; target
+nodes are 0 everywhere).  Patches are placed by LPT (longest processing time
+first) on node counts, as north_star asks.
+
+The colour transport (the labelling stage, a third of a step on one GPU) is
+split by colour: colours are independent linear fixed points with their own
+stopping rule, so each rank transports a disjoint colour set and the
+per-node argmax is merged exactly with two all-reduces (MAX of the fp64
+value bits -- phi >= 0, so the bit order is the value order -- then MIN of
+the colour index among the ranks holding that maximum: the lowest colour
+wins ties, as in the single-device running argmax, src/patchy.py:251-256).
 """
 
 from __future__ import annotations
@@ -64,4 +72,43 @@ def gather_min(t: torch.Tensor) -> torch.Tensor:
 
     if td.is_available() and td.is_initialized() and td.get_world_size() > 1:
         td.all_reduce(t, op=td.ReduceOp.MIN)
+    return t
+
+
+def colour_owner(n_colors: int, n_ranks: int) -> np.ndarray:
+    """Owner rank per colour (round robin: colour costs are not known in
+    advance and part sizes say little about them)."""
+    return np.arange(n_colors, dtype=np.int64) % max(1, n_ranks)
+
+
+def my_colours(n_colors: int, rank: int, n_ranks: int) -> np.ndarray:
+    """Global indices of the colours this rank transports, ascending."""
+    return np.nonzero(colour_owner(n_colors, n_ranks) == rank)[0]
+
+
+def merge_argmax(best_val: torch.Tensor, best_idx: torch.Tensor, n_colors: int):
+    """Exact cross-rank running argmax: per node the maximum value over all
+    ranks' colours and the LOWEST global colour index attaining it.
+    ``best_val`` (fp64, >= 0) / ``best_idx`` (global colour ids) are this
+    rank's local argmax; both are replaced in place."""
+    import torch.distributed as td
+
+    if not (td.is_available() and td.is_initialized() and td.get_world_size() > 1):
+        return best_val, best_idx
+    bits = best_val.view(torch.int64)
+    gbits = bits.clone()
+    td.all_reduce(gbits, op=td.ReduceOp.MAX)
+    cand = torch.where(bits == gbits, best_idx.to(torch.int64),
+                       torch.full_like(bits, n_colors))
+    td.all_reduce(cand, op=td.ReduceOp.MIN)
+    best_val.copy_(gbits.view(torch.float64))
+    best_idx.copy_(torch.clamp(cand, max=n_colors - 1).to(best_idx.dtype))
+    return best_val, best_idx
+
+
+def sum_over_ranks(t: torch.Tensor) -> torch.Tensor:
+    import torch.distributed as td
+
+    if td.is_available() and td.is_initialized() and td.get_world_size() > 1:
+        td.all_reduce(t, op=td.ReduceOp.SUM)
     return t

@@ -243,6 +243,38 @@ def transport_internal(plan: StencilPlan, fb_int: torch.Tensor, parts_flat: Sequ
     return phi, R, [int(x) for x in csw.cpu().tolist()], int(upd.item())
 
 
+def _transport_and_argmax(fplan: StencilPlan, fb: torch.Tensor, parts, color_tol: float,
+                          limit: int):
+    """Transport of every colour + running argmax (patchy.py:183-219,
+    251-256).  With several ranks each rank transports its own colours
+    (dist.my_colours) and the argmax is merged exactly across ranks.
+    Returns (best_val, best_idx, per-colour sweeps, updates)."""
+    R = len(parts)
+    rank, world = dist.world()
+    mine = dist.my_colours(R, rank, world) if world > 1 else np.arange(R)
+    n = fplan.grid.n_interior
+    dev = fplan.device
+    csw_all = torch.zeros(R, dtype=torch.int64, device=dev)
+    upd = 0
+    if len(mine):
+        parts_flat = [fplan.user_serials_to_internal_flat(parts[j]) for j in mine]
+        phi, _, csw, upd = transport_internal(fplan, fb, parts_flat, color_tol, limit)
+        best_val, best_idx = argmax_batched(fplan.gs, phi, len(mine), n, dev)
+        del phi
+        csw_all[torch.as_tensor(mine, device=dev)] = torch.as_tensor(csw, device=dev)
+        if world > 1:
+            best_idx = torch.as_tensor(mine, device=dev, dtype=torch.int32)[best_idx.long()]
+    else:
+        best_val = torch.zeros(n, dtype=torch.float64, device=dev)
+        best_idx = torch.full((n,), R - 1, dtype=torch.int32, device=dev)
+    if world > 1:
+        dist.merge_argmax(best_val, best_idx, R)
+        dist.sum_over_ranks(csw_all)
+        u = dist.sum_over_ranks(torch.tensor([upd], dtype=torch.int64, device=dev))
+        upd = int(u.item())
+    return best_val, best_idx, [int(x) for x in csw_all.tolist()], upd
+
+
 def argmax_stream(gs, phis, n_serial: int, device):
     """Running argmax over streamed single-colour fields (patchy.py:251-256)."""
     lib = _lib.load()
@@ -556,18 +588,15 @@ def run_patchy(spec: ProblemSpec, pcfg: PatchyConfig, cfg: Optional[SolverConfig
             mask = plan_interior_serial(fplan, vf) >= thr
         parts = _resolve_parts(pcfg, spec, fine_grid, fplan)
         limit = pcfg.transport_max_sweeps or 10 * max(fine_grid.shape)
-        parts_flat = [fplan.user_serials_to_internal_flat(p) for p in parts]
-        phi, _, csw, upd = transport_internal(fplan, fb, parts_flat, pcfg.color_tol, limit)
+        n_colors = len(parts)
+        best_val, best_idx, csw, upd = _transport_and_argmax(fplan, fb, parts, pcfg.color_tol,
+                                                             limit)
         stats.transport_updates += upd
         transport_sweeps = [abs(x) for x in csw]
         for j, x in enumerate(csw):
             if x <= 0:
                 stats.warnings.append(f"color {j}: color transport: no convergence after "
                                       f"{abs(x)} sweeps (color_tol {pcfg.color_tol:.1e})")
-        n_colors = len(parts)
-        best_val, best_idx = argmax_batched(fplan.gs, phi, n_colors, fine_grid.n_interior,
-                                            fplan.device)
-        del phi
         color, n_unc, boundary, lab = assemble_internal(
             fplan.gs, best_val, best_idx, n_colors, mask, fplan.kind, fine_grid.n_interior,
             fplan.device, stats.warnings)

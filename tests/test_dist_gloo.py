@@ -62,3 +62,62 @@ def test_lpt_ownership_and_min_gather_world2():
     want = color + 0.5
     for _, _, v in out:
         assert np.array_equal(np.array(v), want)  # identical gathered field on every rank
+
+
+def _argmax_worker(rank, world, port, phi, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    td.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        R, n = phi.shape
+        mine = dist.my_colours(R, rank, world)
+        # local running argmax over this rank's colours (strict >, from (0, 0))
+        bv = torch.zeros(n, dtype=torch.float64)
+        bi = torch.zeros(n, dtype=torch.int32)
+        first = True
+        for j in mine:
+            x = torch.as_tensor(phi[j])
+            take = x > bv
+            if first:
+                bi[:] = int(j)
+                first = False
+            bv = torch.where(take, x, bv)
+            bi = torch.where(take, torch.full_like(bi, int(j)), bi)
+        if len(mine) == 0:
+            bi[:] = R - 1
+        dist.merge_argmax(bv, bi, R)
+        q.put((rank, bv.numpy().tolist(), bi.numpy().tolist()))
+    finally:
+        td.destroy_process_group()
+
+
+def test_colour_split_argmax_merge_world2():
+    """Colours split round-robin over 2 ranks; the merged argmax equals the
+    single-device running argmax (lowest colour on ties, (0, 0) when all
+    colours are 0) on every rank."""
+    rng = np.random.default_rng(7)
+    R, n = 5, 400
+    phi = rng.choice([0.0, 0.25, 0.5, 1.0], size=(R, n)) * (rng.random((R, n)) < 0.6)
+    phi[:, :20] = 0.0            # all-zero nodes
+    phi[1:4, 20:40] = 0.75        # exact ties across ranks
+    # reference: strict > scan over all colours
+    want_v = np.zeros(n)
+    want_i = np.zeros(n, dtype=np.int64)
+    for j in range(R):
+        t = phi[j] > want_v
+        want_v = np.where(t, phi[j], want_v)
+        want_i = np.where(t, j, want_i)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_argmax_worker, args=(r, 2, port, phi, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    pos = want_v > 0
+    for _, v, i in out:
+        assert np.array_equal(np.array(v), want_v)
+        assert np.array_equal(np.array(i)[pos], want_i[pos])  # index only matters where v > 0
