@@ -109,40 +109,71 @@ __device__ inline StencilSmem<D, T> carve_stencil(unsigned char* base, int ncls,
   return s;
 }
 
+// Entries [src0, src0 + n) of the global stencil into entries [dst0, ...) of
+// a staged copy, threads t0, t0 + tstride, ...
 template <int D, typename T, int RULE>
-__device__ inline void stage_stencil(const StencilSmem<D, T>& s, int ncls, int nc,
-                                     const int32_t* oct_start, const uint32_t* nzmask,
+__device__ inline void stage_entries(const StencilSmem<D, T>& s, int dst0, int src0, int n,
+                                     int t0, int tstride, const uint32_t* nzmask,
                                      const double* weights, const double* cost) {
-  const int nent = ncls * nc;
   constexpr int NC = 1 << D;
-  for (int i = threadIdx.x; i < nent; i += blockDim.x) {
+  for (int i = t0; i < n; i += tstride) {
+    const int src = src0 + i, dst = dst0 + i;
     // weights in T with the last nonzero one set so that their sequential
     // sum in T is exactly 1 (I[1] == 1, see dynamics._weights_for)
     T w[NC];
     int last = 0;
     for (int k = 0; k < NC; ++k) {
-      w[k] = (T)weights[(int64_t)i * NC + k];
+      w[k] = (T)weights[(int64_t)src * NC + k];
       if (w[k] != T(0)) last = k;
     }
     T sum = T(0);
     for (int k = 0; k < last; ++k) sum = sum + w[k];
     w[last] = T(1) - sum;
-    for (int k = 0; k < NC; ++k) s.w[(int64_t)i * NC + k] = w[k];
-  }
-  for (int i = threadIdx.x; i < nent; i += blockDim.x) {
-    s.nz[i] = nzmask[i];
-    double c = cost ? cost[i] : 0.0;
+    for (int k = 0; k < NC; ++k) s.w[(int64_t)dst * NC + k] = w[k];
+    s.nz[dst] = nzmask[src];
+    const double c = cost ? cost[src] : 0.0;
     if (RULE == PHJ_RULE_KRUZKOV) {
       // 1 - beta is exact in T (Sterbenz), so beta * 1 + (1 - beta) == 1
       const T beta = (T)exp(-c);
-      s.a[i] = beta;
-      s.b[i] = T(1) - beta;
+      s.a[dst] = beta;
+      s.b[dst] = T(1) - beta;
     } else {
-      s.a[i] = (T)c;
-      s.b[i] = (T)0;
+      s.a[dst] = (T)c;
+      s.b[dst] = (T)0;
     }
   }
+}
+
+// Shared-memory stencil area of the solve kernel: the whole stencil for a
+// single class, else one private single-class slot per warp (multi-class
+// stencils -- one class per heading -- are too big to stage per CTA and a
+// warp block lies in one class).
+template <int D, typename T>
+__host__ __device__ inline int64_t solve_stencil_slot(int nc) {
+  return align_up(StencilSmem<D, T>::bytes(1, nc), 16);
+}
+template <int D, typename T>
+__host__ __device__ inline int64_t solve_stencil_bytes(int ncls, int nc) {
+  return ncls > 1 ? kWarps * solve_stencil_slot<D, T>(nc) : StencilSmem<D, T>::bytes(ncls, nc);
+}
+
+template <int D, typename T, int RULE>
+__device__ inline void stage_stencil(const StencilSmem<D, T>& s, int ncls, int nc,
+                                     const int32_t* oct_start, const uint32_t* nzmask,
+                                     const double* weights, const double* cost) {
+  stage_entries<D, T, RULE>(s, 0, 0, ncls * nc, threadIdx.x, blockDim.x, nzmask, weights, cost);
   for (int i = threadIdx.x; i < ncls * ((1 << D) + 1); i += blockDim.x) s.oct[i] = oct_start[i];
+}
+
+// One class of a multi-class stencil (Dubins: one per heading) into a
+// warp's private staged copy (class index 0 there), by the warp's lanes.
+template <int D, typename T, int RULE>
+__device__ inline void stage_class(const StencilSmem<D, T>& s, int cls, int nc, int lane,
+                                   const int32_t* oct_start, const uint32_t* nzmask,
+                                   const double* weights, const double* cost) {
+  constexpr int NC = 1 << D;
+  stage_entries<D, T, RULE>(s, 0, cls * nc, nc, lane, 32, nzmask, weights, cost);
+  if (lane <= NC) s.oct[lane] = oct_start[cls * (NC + 1) + lane] - cls * nc;
 }
 
 // Neighbourhood sources.  Evaluation code asks a source for corner K of
@@ -257,6 +288,9 @@ __device__ __forceinline__ T finish_cand(T acc, T ca, T cb, T ncoef, uint32_t fm
 #endif
 #ifndef PHJ_MINU
 #define PHJ_MINU 0
+#endif
+#ifndef PHJ_CTRL_REGNB
+#define PHJ_CTRL_REGNB 0
 #endif
 template <typename T>
 struct MinAcc;
@@ -575,6 +609,29 @@ __device__ __forceinline__ int eval_sweep(const T* lt, bool prune_on, const Sten
                                           const T (&ncoef)[NB], const bool (&comp)[NB],
                                           MinAcc<T> (&mn)[NB], T (&best)[NB], int (&bidx)[NB],
                                           const Hook& hook) {
+#if PHJ_CTRL_REGNB
+  if constexpr (COST == PHJ_COST_CTRL) {
+    // per-control costs (no pruning), few controls: the whole neighbourhood
+    // in registers, compile-time octants
+    Nbhd<D, T, NB> nb;
+    using S = TileShape<D>;
+    if constexpr (D == 2) {
+#pragma unroll
+      for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < NB + 2; ++dx) nb.v[dy][dx] = lt[dy * S::C + dx];
+    } else {
+#pragma unroll
+      for (int dz = 0; dz < 3; ++dz)
+#pragma unroll
+        for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+          for (int dx = 0; dx < NB + 2; ++dx) nb.v[dz * 3 + dy][dx] = lt[(dz * S::RB + dy) * S::C + dx];
+    }
+    EvalAll<D, T, NB, RULE, COST, SLOW, 0>::run(nb, s, os, fm, ncoef, nullptr, mn, best, bidx, hook);
+    return os[1 << D] - os[0];
+  }
+#endif
   constexpr bool CAN_PRUNE = COST == PHJ_COST_NODE && PHJ_PRUNE;
   const bool prune = CAN_PRUNE && prune_on;
   const int first = prune ? preferred_octant<D, T>(lt) : 0;
@@ -586,7 +643,7 @@ __device__ __forceinline__ int eval_sweep(const T* lt, bool prune_on, const Sten
   hook();
 #pragma unroll 1
   for (int O = 0; O < (1 << D); ++O) {
-    if (O == first) continue;
+    if (O == first || os[O] == os[O + 1]) continue;
     cell.load(lt, O);
     if (prune && !__any_sync(0xffffffffu, octant_needed<D, T, NB>(cell, comp, mn))) continue;
     eval_octant<D, T, NB, RULE, COST, SLOW, 0>(cell, O, s, os, fm, ncoef, nullptr, mn, best, bidx);
@@ -805,8 +862,9 @@ __device__ __forceinline__ bool sweep_block(const SolveParams& p, const StencilS
   int c[3];
   const bool row_ok = lane_nodes<D>(g, p.tg, blk, lane, c);
   const int64_t f0 = ext_flat<D>(g, c);
-  const int cls = p.n_classes > 1 ? c[0] : 0;
-  const int* os = s.oct + cls * ((1 << D) + 1);
+  // the solve kernel's staged stencil holds this block's class at index 0
+  // (single-class stencils, or the warp's private class slot)
+  const int* os = s.oct;
   const int nadm = p.n_real;
   const int ly = lane / B::LX, lx = lane % B::LX;
   const int lshift = (int)((f0 - lx * NB) & 1);  // label half-word offset of the row
@@ -1023,17 +1081,23 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __gri
   using S = TileShape<D>;
   extern __shared__ __align__(16) unsigned char smem[];
   cg::grid_group grid = cg::this_grid();
-  StencilSmem<D, T> s = carve_stencil<D, T>(smem, p.n_classes, p.nc);
-  int* s_done = (int*)(smem + StencilSmem<D, T>::bytes(p.n_classes, p.nc));
+  const bool warp_cls = p.n_classes > 1;
+  const int64_t sbytes = solve_stencil_bytes<D, T>(p.n_classes, p.nc);
+  StencilSmem<D, T> s =
+      warp_cls ? carve_stencil<D, T>(smem + (threadIdx.x >> 5) * solve_stencil_slot<D, T>(p.nc), 1,
+                                     p.nc)
+               : carve_stencil<D, T>(smem, p.n_classes, p.nc);
+  int* s_done = (int*)(smem + sbytes);
   unsigned long long* s_max = (unsigned long long*)(s_done + ((p.R + 1) / 2 * 2));
-  T* tiles = (T*)(smem + align_up(StencilSmem<D, T>::bytes(p.n_classes, p.nc) +
-                                      (int64_t)((p.R + 1) / 2 * 2) * 4 +
+  T* tiles = (T*)(smem + align_up(sbytes + (int64_t)((p.R + 1) / 2 * 2) * 4 +
                                       (int64_t)min(p.R, kSmemPatchReduce) * 8,
                                   16));
   T* wtile = tiles + (threadIdx.x >> 5) * 2 * S::N;
   NodeStage<D, T>* wnodes =
       (NodeStage<D, T>*)(tiles + kWarps * 2 * S::N) + (threadIdx.x >> 5) * 2;
-  stage_stencil<D, T, RULE>(s, p.n_classes, p.nc, p.oct_start, p.nzmask, p.weights, p.cost);
+  if (!warp_cls)
+    stage_stencil<D, T, RULE>(s, p.n_classes, p.nc, p.oct_start, p.nzmask, p.weights, p.cost);
+  int wcls = -1;  // class held by this warp's slot
   for (int i = threadIdx.x; i < p.R; i += blockDim.x)
     s_done[i] = (p.mine == nullptr || p.mine[i]) ? 0x7fffffff : 0;
   __syncthreads();
@@ -1080,6 +1144,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __gri
       const int nblk = nxt < cnt ? __ldcg(&list[nxt]) : 0;
       if (lane == 0 && nxt < cnt) ticket = atomicAdd(take, 1);
       if (lane == 0) cur_flags[blk] = 0;
+      if (warp_cls) {
+        int bc[3];
+        decode_block<D>(p.tg, blk, bc);
+        if (bc[0] != wcls) {
+          __syncwarp();
+          stage_class<D, T, RULE>(s, bc[0], p.nc, lane, p.oct_start, p.nzmask, p.weights, p.cost);
+          wcls = bc[0];
+        }
+      }
       cp_async_wait_all();
       __syncwarp();
       auto hook = [&]() {
@@ -1755,7 +1828,7 @@ static int solve_impl(const phj_solve_args* a) {
       nullptr, 0ull);
   phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
-  size_t smem = (size_t)align_up(StencilSmem<D, T>::bytes(p.n_classes, p.nc) +
+  size_t smem = (size_t)align_up(solve_stencil_bytes<D, T>(p.n_classes, p.nc) +
                                      (int64_t)((p.R + 1) / 2 * 2) * 4 +
                                      (int64_t)std::min(p.R, kSmemPatchReduce) * 8,
                                  16) +
