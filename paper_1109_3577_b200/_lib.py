@@ -14,6 +14,9 @@ from typing import Optional
 HERE = os.path.dirname(os.path.abspath(__file__))
 # PHJ_LIB_PATH selects an alternative in-tree build (kernel variant A/B runs)
 LIB_PATH = os.environ.get("PHJ_LIB_PATH") or os.path.join(HERE, "_lib", "libphj.so")
+#: read back per-sweep diagnostics (active blocks per sweep) after each
+#: launch -- extra device->host traffic, off unless PHJ_DIAG=1 or set here
+DIAG = os.environ.get("PHJ_DIAG", "0") == "1"
 
 PHJ_OK = 0
 F64, F32 = 0, 1

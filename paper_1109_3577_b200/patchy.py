@@ -239,7 +239,8 @@ def transport_internal(plan: StencilPlan, fb_int: torch.Tensor, parts_flat: Sequ
     from .solver import active_blocks_per_sweep
 
     TRANSPORT_DIAG["kernel_ms"] = e0.elapsed_time(e1)
-    TRANSPORT_DIAG["block_counts"] = active_blocks_per_sweep(plan, ws, max_sweeps, int(ih[0]))
+    if _lib.DIAG:
+        TRANSPORT_DIAG["block_counts"] = active_blocks_per_sweep(plan, ws, max_sweeps, int(ih[0]))
     return phi, R, [int(x) for x in csw.cpu().tolist()], int(upd.item())
 
 

@@ -426,7 +426,8 @@ def device_solve(plan: StencilPlan, work: torch.Tensor, lab: torch.Tensor, fmask
     out = DeviceSolveResult(res, ps.cpu().numpy(), mc.view(max_sweeps, n_patches).cpu().numpy(),
                             int(ev_h[0]), info_h, executed=int(ev_h[1]))
     out.device_ms = e0.elapsed_time(e1)
-    out.block_counts = active_blocks_per_sweep(plan, ws, max_sweeps, int(info_h[0]))
+    if _lib.DIAG:
+        out.block_counts = active_blocks_per_sweep(plan, ws, max_sweeps, int(info_h[0]))
     return out
 
 

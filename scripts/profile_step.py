@@ -13,7 +13,9 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import paper_1109_3577_b200 as phj  # noqa: E402
-from paper_1109_3577_b200 import configs, patchy  # noqa: E402
+from paper_1109_3577_b200 import _lib, configs, patchy  # noqa: E402
+
+_lib.DIAG = True
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 dtype = sys.argv[2] if len(sys.argv) > 2 else "float64"
