@@ -21,6 +21,7 @@ constexpr int kWarps = kThreads / 32;
 #endif
 constexpr int kCtasPerSm = PHJ_MIN_CTAS;
 constexpr int kMaxPatches = 1024;
+constexpr int kMaxColors = 4096;  // transport colours (>= kMaxPatches)
 constexpr int kSmemPatchReduce = 64;  // per-CTA patch max reduction when R <= 64
 
 // Work/activity unit = one warp "block" of nodes: LY rows x (LX lanes * NB
@@ -158,7 +159,15 @@ struct Workspace {
   int* counts;  // [max_sweeps + 2] active blocks per sweep
   int* take;    // [max_sweeps + 2] dynamic work counters
   unsigned long long* cmask[2];  // transport: per-block active-colour masks
+  // per-sweep max change per patch / colour, one 128-byte line per entry
+  // (all CTAs reduce into these with atomics right before the grid barrier
+  // and read them right after it: packed into one line, those requests
+  // serialise on one L2 slice), triple-buffered by sweep so the entries of
+  // sweep k+1 can be zeroed during sweep k
+  unsigned long long* pmax;  // [3][kMaxColors * kMaxPad]
 };
+
+constexpr int kMaxPad = 16;  // u64 per entry = 128 B
 
 __host__ __device__ inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
@@ -169,6 +178,7 @@ inline int64_t workspace_bytes(const phj_grid& g, int max_sweeps) {
   b += 4 * align_up((int64_t)tg.total * 4, 256);
   b += 2 * align_up((int64_t)(max_sweeps + 2) * 4, 256);
   b += 2 * align_up((int64_t)tg.total * 8, 256);
+  b += 3 * (int64_t)kMaxColors * kMaxPad * 8;
   return b;
 }
 
@@ -185,8 +195,14 @@ inline Workspace carve(const phj_grid& g, void* base, int max_sweeps) {
   w.counts = (int*)p; p += align_up((int64_t)(max_sweeps + 2) * 4, 256);
   w.take = (int*)p; p += align_up((int64_t)(max_sweeps + 2) * 4, 256);
   w.cmask[0] = (unsigned long long*)p; p += align_up((int64_t)tg.total * 8, 256);
-  w.cmask[1] = (unsigned long long*)p;
+  w.cmask[1] = (unsigned long long*)p; p += align_up((int64_t)tg.total * 8, 256);
+  w.pmax = (unsigned long long*)p;
   return w;
+}
+
+// the padded max-change entries of sweep sw
+__device__ __forceinline__ unsigned long long* sweep_max_slots(const Workspace& w, int sw) {
+  return w.pmax + (int64_t)(sw % 3) * kMaxColors * kMaxPad;
 }
 
 __device__ inline unsigned long long dbits(double x) {

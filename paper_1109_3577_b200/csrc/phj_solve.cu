@@ -292,6 +292,9 @@ __device__ __forceinline__ T finish_cand(T acc, T ca, T cb, T ncoef, uint32_t fm
 #ifndef PHJ_CTRL_REGNB
 #define PHJ_CTRL_REGNB 0
 #endif
+#ifndef PHJ_SKIP_EMPTY_OCT
+#define PHJ_SKIP_EMPTY_OCT 1
+#endif
 template <typename T>
 struct MinAcc;
 template <>
@@ -643,7 +646,11 @@ __device__ __forceinline__ int eval_sweep(const T* lt, bool prune_on, const Sten
   hook();
 #pragma unroll 1
   for (int O = 0; O < (1 << D); ++O) {
+#if PHJ_SKIP_EMPTY_OCT
     if (O == first || os[O] == os[O + 1]) continue;
+#else
+    if (O == first) continue;
+#endif
     cell.load(lt, O);
     if (prune && !__any_sync(0xffffffffu, octant_needed<D, T, NB>(cell, comp, mn))) continue;
     eval_octant<D, T, NB, RULE, COST, SLOW, 0>(cell, O, s, os, fm, ncoef, nullptr, mn, best, bidx);
@@ -836,7 +843,7 @@ __device__ __forceinline__ void flush_patch_max(const SolveParams& p, PatchMax& 
                                                 unsigned long long* gmax_row) {
   if (pm.lab >= 0 && (threadIdx.x & 31) == 0) {
     if (p.R <= kSmemPatchReduce) atomicMax(&s_max[pm.lab], dbits(pm.m));
-    else atomicMax(&gmax_row[pm.lab], dbits(pm.m));
+    else atomicMax(&gmax_row[pm.lab * kMaxPad], dbits(pm.m));
   }
   pm.lab = -1;
   pm.m = 0.0;
@@ -999,7 +1006,7 @@ __device__ __forceinline__ bool sweep_block(const SolveParams& p, const StencilS
       for (int r = 0; r < NB; ++r) {
         if (mych[r] > T(0)) {
           if (p.R <= kSmemPatchReduce) atomic_max_change(&s_max[labv[r]], mych[r]);
-          else atomic_max_change(&gmax_row[labv[r]], mych[r]);
+          else atomic_max_change(&gmax_row[labv[r] * kMaxPad], mych[r]);
         }
       }
     }
@@ -1075,18 +1082,20 @@ __host__ __device__ constexpr int64_t solve_tile_bytes() {
          (int64_t)kWarps * 2 * sizeof(NodeStage<D, T>);
 }
 
-template <int D, typename T, int RULE, int COST>
+// WCLS: multi-class stencil staged per warp (compile-time, so single-class
+// launches keep fixed shared-memory addressing)
+template <int D, typename T, int RULE, int COST, bool WCLS>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __grid_constant__ SolveParams p) {
   constexpr int NB = Blk<D>::NB;
   using S = TileShape<D>;
   extern __shared__ __align__(16) unsigned char smem[];
   cg::grid_group grid = cg::this_grid();
-  const bool warp_cls = p.n_classes > 1;
-  const int64_t sbytes = solve_stencil_bytes<D, T>(p.n_classes, p.nc);
+  constexpr bool warp_cls = WCLS;
+  const int64_t sbytes = solve_stencil_bytes<D, T>(WCLS ? 2 : 1, p.nc);
   StencilSmem<D, T> s =
-      warp_cls ? carve_stencil<D, T>(smem + (threadIdx.x >> 5) * solve_stencil_slot<D, T>(p.nc), 1,
-                                     p.nc)
-               : carve_stencil<D, T>(smem, p.n_classes, p.nc);
+      WCLS ? carve_stencil<D, T>(smem + (threadIdx.x >> 5) * solve_stencil_slot<D, T>(p.nc), 1,
+                                 p.nc)
+           : carve_stencil<D, T>(smem, 1, p.nc);
   int* s_done = (int*)(smem + sbytes);
   unsigned long long* s_max = (unsigned long long*)(s_done + ((p.R + 1) / 2 * 2));
   T* tiles = (T*)(smem + align_up(sbytes + (int64_t)((p.R + 1) / 2 * 2) * 4 +
@@ -1131,7 +1140,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __gri
     int* nxt_list = p.ws.list[(sw + 1) & 1];
     int* nxt_cnt = &p.ws.counts[sw + 1];
     int* take = &p.ws.take[sw];
-    unsigned long long* gmax_row = p.maxch + (int64_t)sw * p.R;
+    unsigned long long* gmax_row = sweep_max_slots(p.ws, sw);  // padded: entry i at i * kMaxPad
+    if (blockIdx.x == 0) {
+      unsigned long long* z = sweep_max_slots(p.ws, sw + 1);
+      for (int i = threadIdx.x; i < p.R; i += blockDim.x) z[i * kMaxPad] = 0ull;
+    }
     for (int i = threadIdx.x; i < nshared; i += blockDim.x) s_max[i] = 0ull;
     __syncthreads();
     int item = gwarp;
@@ -1183,7 +1196,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __gri
     __syncthreads();
     tm.mark(9);
     for (int i = threadIdx.x; i < nshared; i += blockDim.x)
-      if (s_max[i]) atomicMax(&gmax_row[i], s_max[i]);
+      if (s_max[i]) atomicMax(&gmax_row[i * kMaxPad], s_max[i]);
     grid.sync();
     tm.mark(10);
     ++sw;
@@ -1191,7 +1204,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __gri
     int pending = 0;
     for (int i = threadIdx.x; i < p.R; i += blockDim.x) {
       if (s_done[i] == 0x7fffffff) {
-        const double mc = __longlong_as_double((long long)ld_cg(&gmax_row[i]));
+        const unsigned long long mb = ld_cg(&gmax_row[i * kMaxPad]);
+        if (blockIdx.x == 0) p.maxch[(int64_t)(sw - 1) * p.R + i] = mb;
+        const double mc = __longlong_as_double((long long)mb);
         if (mc <= p.tol) s_done[i] = sw;
         else pending = 1;
       }
@@ -1377,6 +1392,10 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
     int* nxt_cnt = &p.ws.counts[sw + 1];
     int* take = &p.ws.take[sw];
     for (int i = threadIdx.x; i < R; i += blockDim.x) s_max[i] = 0ull;
+    if (blockIdx.x == 0) {
+      unsigned long long* z = sweep_max_slots(p.ws, sw + 1);
+      for (int i = threadIdx.x; i < R; i += blockDim.x) z[i * kMaxPad] = 0ull;
+    }
     __syncthreads();
     // prefetch of one item: its colour mask (lane 0) and mover entries
     auto prefetch = [&](int b, unsigned long long& pcm, int (&pe)[NB]) {
@@ -1537,16 +1556,18 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
     mq.reserve(lane, nxt_cnt);
     mq.store(nxt_list);
     __syncthreads();
-    unsigned long long* grow = p.maxch + (int64_t)sw * R;
+    unsigned long long* grow = sweep_max_slots(p.ws, sw);  // padded: entry i at i * kMaxPad
     for (int i = threadIdx.x; i < R; i += blockDim.x)
-      if (s_max[i]) atomicMax(&grow[i], s_max[i]);
+      if (s_max[i]) atomicMax(&grow[i * kMaxPad], s_max[i]);
     grid.sync();
     ++sw;
     buf ^= 1;
     int pending = 0;
     for (int i = threadIdx.x; i < R; i += blockDim.x) {
       if (s_done[i] == 0x7fffffff) {
-        const double mc = __longlong_as_double((long long)ld_cg(&grow[i]));
+        const unsigned long long mb = ld_cg(&grow[i * kMaxPad]);
+        if (blockIdx.x == 0) p.maxch[(int64_t)(sw - 1) * R + i] = mb;
+        const double mc = __longlong_as_double((long long)mb);
         if (mc <= p.tol) s_done[i] = sw;
         else pending = 1;
       }
@@ -1835,8 +1856,11 @@ static int solve_impl(const phj_solve_args* a) {
                 (size_t)solve_tile_bytes<D, T>();
   void* args[] = {(void*)&p};
   int launched = 0;
-  int rc = coop_launch(solve_kernel<D, T, RULE, COST>, (p.tg.total + kWarps - 1) / kWarps, smem,
-                       args, stream, &launched);
+  int rc = (D == 3 && p.n_classes > 1)
+               ? coop_launch(solve_kernel<D, T, RULE, COST, D == 3>,
+                             (p.tg.total + kWarps - 1) / kWarps, smem, args, stream, &launched)
+               : coop_launch(solve_kernel<D, T, RULE, COST, false>,
+                             (p.tg.total + kWarps - 1) / kWarps, smem, args, stream, &launched);
   if (rc) return rc;
   PHJ_CUDA(cudaGetLastError());
   return PHJ_OK;
@@ -1964,8 +1988,8 @@ extern "C" int phj_transport(const phj_transport_args* a) {
     phj_set_error("phj_transport: only internal axis 0 may be periodic");
     return PHJ_ERR_UNSUPPORTED;
   }
-  if (a->n_colors < 1 || a->n_colors > 4096 || !a->maxch_hist || !a->color_sweeps) {
-    phj_set_error("phj_transport: n_colors must be in [1, 4096]");
+  if (a->n_colors < 1 || a->n_colors > kMaxColors || !a->maxch_hist || !a->color_sweeps) {
+    phj_set_error("phj_transport: n_colors must be in [1, %d]", kMaxColors);
     return PHJ_ERR_ARG;
   }
   return a->grid.dim == 2 ? transport_impl<2>(a) : transport_impl<3>(a);
