@@ -207,5 +207,42 @@ def main():
           "transport", tsweeps)
 
 
+def main_ao3():
+    """G7: conical control reduction (AO3, solver.py:446-476, patchy.py:353-356)
+    on the config-1 patch map of G3: state-constrained patch solves with
+    ``reduction`` r = 3 and 6 (reference rule, GS, tol 1e-8)."""
+    phj = import_reference()
+    spec1 = phj.ProblemSpec(name="c1", dim=2, box_lo=(-2.0, -2.0), box_hi=(2.0, 2.0),
+                            dynamics=eikonal_dyn,
+                            control_set=phj.discretize_circle(32),
+                            target=phj.TargetSpec.ball((0.0, 0.0), 0.1))
+    g1 = phj.Grid(spec1.box_lo, spec1.box_hi, (101, 101))
+    t1 = phj.CandidateTable(g1, spec1)
+    cfg = phj.SolverConfig(tol=1e-8)
+    c = np.load(os.path.join(OUT, "c1_patchy.npz"))
+    lifted = phj.NodeField(g1, c["lifted"].copy(), sentinel=1e9)
+    fbl = phj.FeedbackField(g1, spec1.control_set, c["feedback"].copy())
+    mask = phj.mask_unreachable(lifted)
+    pm = phj.assemble_patches(list(enumerate([phj.NodeField(g1, p.copy()) for p in c["phi"]])),
+                              mask, g1, kind=t1.kind)
+    assert np.array_equal(pm.color, c["color"])
+    out = {}
+    for r in (3.0, 6.0):
+        pcfg = phj.PatchyConfig(n_patches=4, coarse_nodes=26, fine_nodes=101, reduction=r)
+        val, pst, _ = phj.solve_patches(spec1, g1, pm, lifted, pcfg, cfg, table=t1,
+                                        feedback=fbl)
+        key = f"r{int(r)}"
+        out[f"value_{key}"] = val.values
+        out[f"sweeps_{key}"] = np.array([s.sweeps for s in pst])
+        out[f"evals_{key}"] = np.array([s.candidate_evals for s in pst])
+        print("ao3", r, "sweeps", [s.sweeps for s in pst], "evals",
+              [s.candidate_evals for s in pst])
+    np.savez_compressed(os.path.join(OUT, "c1_patchy_ao3.npz"), **out)
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "ao3":
+        main_ao3()
+    else:
+        main()
+        main_ao3()

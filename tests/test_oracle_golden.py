@@ -159,3 +159,19 @@ def test_kruzkov_rule_is_monotone_transform_of_reference_at_one_sweep():
     P.sweep(u, pr, np.array([s]), rule="kruzkov", mode="jacobi")
     beta = np.exp(-g.k_step)
     assert g.interior(u)[75, 50] == pytest.approx(beta * 0.25 + 1.0 - beta, abs=1e-15)
+
+
+def test_c1_patch_solves_with_conical_reduction_bit_exact():
+    """AO3 (solver.py:446-476, patchy.py:353-356): the oracle's reduced patch
+    solves reproduce the reference's (r = 3 and 6) bit for bit, with the same
+    sweep and candidate-evaluation counts."""
+    c = golden("c1_patchy.npz")
+    a = golden("c1_patchy_ao3.npz")
+    pr = C.c1_fine()
+    for r in (3, 6):
+        allowed = P.allowed_mask(pr.controls, c["feedback"], float(r))
+        val, pst = P.solve_patches(pr, c["color"], 4, rule="reference", mode="gs", tol=1e-8,
+                                   allowed=allowed)
+        assert np.array_equal(val, _flat(a[f"value_r{r}"]))
+        assert [s.sweeps for s in pst] == [int(x) for x in a[f"sweeps_r{r}"]]
+        assert [s.candidate_evals for s in pst] == [int(x) for x in a[f"evals_r{r}"]]
