@@ -123,8 +123,16 @@ typedef struct phj_solve_args {
                                  evaluations executed (incl. padding, after pruning) */
   int32_t* info;              /* out [4]: total sweeps, index of result buffer,
                                  tiles processed, launches */
+  /* AO3 conical control reduction (solver.py:446-476; NULL ao3_fb = off):
+   * a node with feedback control f >= 0 only evaluates the stencil entries
+   * whose bits are set in ao3_mask[f * ao3_words ...] (entry index order of
+   * the class-0 stencil, 64 entries per word) and counts ao3_count[f]
+   * candidate evaluations; f < 0 keeps every entry. */
+  const int32_t* ao3_fb;                /* ext layout, feedback control per node or -1 */
+  const unsigned long long* ao3_mask;   /* [n_controls][ao3_words] */
+  const int32_t* ao3_count;             /* [n_controls] */
+  int32_t ao3_words;                    /* 1 or 2 */
   int32_t options;            /* PHJ_SOLVE_* bits, 0 = defaults */
-  int32_t pad_;
   void* stream;               /* cudaStream_t */
 } phj_solve_args;
 

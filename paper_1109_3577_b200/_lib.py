@@ -56,7 +56,8 @@ class SolveArgs(ctypes.Structure):
                 ("v0", P), ("v1", P), ("lab", P), ("fmask", P), ("coef", P), ("coef0", D),
                 ("n_patches", I32), ("max_sweeps", I32), ("mine", P), ("tol", D),
                 ("workspace", P), ("patch_sweeps", P), ("maxch_hist", P), ("evals", P),
-                ("info", P), ("options", I32), ("pad_", I32), ("stream", P)]
+                ("info", P), ("ao3_fb", P), ("ao3_mask", P), ("ao3_count", P),
+                ("ao3_words", I32), ("options", I32), ("stream", P)]
 
 
 SOLVE_NO_PRUNE = 1  # PHJ_SOLVE_NO_PRUNE

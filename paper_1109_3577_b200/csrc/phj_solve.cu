@@ -77,6 +77,11 @@ struct SolveParams {
   unsigned long long* evals;
   int32_t* info;
   int prune;  // exact octant pruning on (PHJ_SOLVE_NO_PRUNE clears it)
+  // AO3 conical reduction (NULL ao3_fb = off)
+  const int32_t* ao3_fb;
+  const unsigned long long* ao3_mask;
+  const int32_t* ao3_count;
+  int ao3_words;
 };
 
 template <int D, typename T>
@@ -257,7 +262,8 @@ __device__ __forceinline__ void load_weights(const T* src, T* w) {
 // Candidate post-processing: per-entry cost (COST_CTRL), the per-candidate
 // rule in feedback mode, and state-constraint rejection.
 template <typename T, int RULE, int COST, bool SLOW, int MODE>
-__device__ __forceinline__ T finish_cand(T acc, T ca, T cb, T ncoef, uint32_t fm, uint32_t nz) {
+__device__ __forceinline__ T finish_cand(T acc, T ca, T cb, T ncoef, uint32_t fm, uint32_t nz,
+                                         bool ok = true) {
   if constexpr (COST == PHJ_COST_CTRL) {
     acc = (RULE == PHJ_RULE_KRUZKOV) ? fma(ca, acc, cb) : acc + ca;
   } else if constexpr (MODE == 1) {
@@ -265,7 +271,7 @@ __device__ __forceinline__ T finish_cand(T acc, T ca, T cb, T ncoef, uint32_t fm
     acc = (RULE == PHJ_RULE_KRUZKOV) ? fma(ncoef, acc, T(1) - ncoef) : acc + ncoef;
   }
   if constexpr (SLOW) {
-    if (fm & nz) acc = big_value<T>();
+    if ((fm & nz) || !ok) acc = big_value<T>();
   }
   return acc;
 }
@@ -332,11 +338,22 @@ __device__ __forceinline__ void take_arg(T acc, int cidx, T& best, int& bidx) {
 // per iteration (the host pads every octant group to a multiple of U).
 // MODE 0: min (sweep, into mn); MODE 1: argmin with the lowest original
 // index on ties (feedback, into best/bidx).
-template <int D, typename T, int NB, int RULE, int COST, bool SLOW, int MODE, typename Src>
+// AO3 conical control reduction (solver.py:446-476): per node, the stencil
+// entries allowed by its feedback control, as a bitmask over entry index
+// (up to 128 entries).
+template <int NB>
+struct Allowed {
+  unsigned long long w[NB][2];
+};
+
+template <int D, typename T, int NB, int RULE, int COST, bool SLOW, int MODE, typename Src,
+          bool AO3 = false>
 __device__ __forceinline__ void eval_octant(const Src& cell, int O, const StencilSmem<D, T>& s,
                                             const int* os, const uint32_t (&fm)[NB],
                                             const T (&ncoef)[NB], const int32_t* ctrl_map,
-                                            MinAcc<T> (&mn)[NB], T (&best)[NB], int (&bidx)[NB]) {
+                                            MinAcc<T> (&mn)[NB], T (&best)[NB], int (&bidx)[NB],
+                                            const Allowed<NB>* al = nullptr) {
+  static_assert(!AO3 || SLOW, "AO3 rejects candidates on the SLOW path");
   constexpr int NC = 1 << D;
   constexpr int U = (D == 2) ? PHJ_KUNROLL2 : PHJ_UNROLL(D);  // divides the host padding
   const int e0 = os[O], e1 = os[O + 1];
@@ -379,10 +396,15 @@ __device__ __forceinline__ void eval_octant(const Src& cell, int O, const Stenci
 #pragma unroll
     for (int r = 0; r < NB; ++r) {
       T x[U];
+      unsigned long long aw = 0ull;
+      if constexpr (AO3) aw = (e >> 6) ? al->w[r][1] : al->w[r][0];  // U | 64: one word
 #pragma unroll
-      for (int u = 0; u < U; ++u)
+      for (int u = 0; u < U; ++u) {
+        bool ok = true;
+        if constexpr (AO3) ok = (aw >> ((e + u) & 63)) & 1ull;
         x[u] = finish_cand<T, RULE, COST, SLOW, MODE>(acc[u][r], ca[u], cb[u], ncoef[r], fm[r],
-                                                      nz[u]);
+                                                      nz[u], ok);
+      }
       if constexpr (MODE == 0) {
 #if PHJ_MINU
 #pragma unroll
@@ -606,12 +628,13 @@ __device__ __forceinline__ int preferred_octant(const T* lt) {
 // the warp's preferred octant first, then the others unless pruned; with
 // per-control costs every octant in order.  `hook` runs once, after the
 // first octant.  Returns the stencil entries evaluated per node.
-template <int D, typename T, int NB, int RULE, int COST, bool SLOW, typename Hook>
+template <int D, typename T, int NB, int RULE, int COST, bool SLOW, typename Hook,
+          bool AO3 = false>
 __device__ __forceinline__ int eval_sweep(const T* lt, bool prune_on, const StencilSmem<D, T>& s,
                                           const int* os, const uint32_t (&fm)[NB],
                                           const T (&ncoef)[NB], const bool (&comp)[NB],
                                           MinAcc<T> (&mn)[NB], T (&best)[NB], int (&bidx)[NB],
-                                          const Hook& hook) {
+                                          const Hook& hook, const Allowed<NB>* al = nullptr) {
 #if PHJ_CTRL_REGNB
   if constexpr (COST == PHJ_COST_CTRL) {
     // per-control costs (no pruning), few controls: the whole neighbourhood
@@ -640,8 +663,8 @@ __device__ __forceinline__ int eval_sweep(const T* lt, bool prune_on, const Sten
   const int first = prune ? preferred_octant<D, T>(lt) : 0;
   OctNb<D, T, NB> cell;
   cell.load(lt, first);
-  eval_octant<D, T, NB, RULE, COST, SLOW, 0>(cell, first, s, os, fm, ncoef, nullptr, mn, best,
-                                             bidx);
+  eval_octant<D, T, NB, RULE, COST, SLOW, 0, OctNb<D, T, NB>, AO3>(cell, first, s, os, fm, ncoef,
+                                                                   nullptr, mn, best, bidx, al);
   int n_ent = os[first + 1] - os[first];
   hook();
 #pragma unroll 1
@@ -653,7 +676,8 @@ __device__ __forceinline__ int eval_sweep(const T* lt, bool prune_on, const Sten
 #endif
     cell.load(lt, O);
     if (prune && !__any_sync(0xffffffffu, octant_needed<D, T, NB>(cell, comp, mn))) continue;
-    eval_octant<D, T, NB, RULE, COST, SLOW, 0>(cell, O, s, os, fm, ncoef, nullptr, mn, best, bidx);
+    eval_octant<D, T, NB, RULE, COST, SLOW, 0, OctNb<D, T, NB>, AO3>(cell, O, s, os, fm, ncoef,
+                                                                     nullptr, mn, best, bidx, al);
     n_ent += os[O + 1] - os[O];
   }
   return n_ent;
@@ -723,6 +747,7 @@ struct NodeStage {
   static constexpr int LW = B::BX / 2 + 1;  // label words per row
   T coef[NN];
   uint32_t fm[NN];
+  int32_t fb[NN];  // AO3: feedback control per node
   uint32_t labw[B::BY * LW];
 };
 
@@ -817,6 +842,7 @@ __device__ __forceinline__ void stage_block(const SolveParams& p, const T* __res
       const int64_t f = full ? fr + j : min(fr + j, nlast);
       cp_async<4>(&ns->fm[ly * B::BX + j], p.fmask + f);
       if (stage_coef) cp_async<sizeof(T)>(&ns->coef[ly * B::BX + j], (const T*)p.coef + f);
+      if (p.ao3_fb) cp_async<4>(&ns->fb[ly * B::BX + j], p.ao3_fb + f);
     }
     const int64_t wmax = (nlast - 1) >> 1;  // last whole 32-bit word of the label array
     const uint32_t* labw = (const uint32_t*)p.lab;
@@ -930,12 +956,27 @@ __device__ __forceinline__ bool sweep_block(const SolveParams& p, const StencilS
 #pragma unroll
     for (int r = 0; r < NB; ++r) fmo |= fm[r];
     int n_ent;
-    if (__any_sync(FULL, fmo != 0))
+    if (p.ao3_fb) {
+      // AO3: the node's allowed stencil entries (all for nodes without feedback)
+      Allowed<NB> al;
+#pragma unroll
+      for (int r = 0; r < NB; ++r) {
+        const int f = comp[r] ? ns->fb[ly * B::BX + lx * NB + r] : -1;
+#pragma unroll
+        for (int w = 0; w < 2; ++w)
+          al.w[r][w] = (f >= 0 && w < p.ao3_words) ? __ldg(&p.ao3_mask[f * p.ao3_words + w])
+                                                   : ~0ull;
+      }
+      n_ent = eval_sweep<D, T, NB, RULE, COST, true, Hook, true>(lt, p.prune != 0, s, os, fm,
+                                                                 ncoef, comp, mn, best, bidx, hook,
+                                                                 &al);
+    } else if (__any_sync(FULL, fmo != 0)) {
       n_ent = eval_sweep<D, T, NB, RULE, COST, true>(lt, p.prune != 0, s, os, fm, ncoef, comp, mn,
                                                      best, bidx, hook);
-    else
+    } else {
       n_ent = eval_sweep<D, T, NB, RULE, COST, false>(lt, p.prune != 0, s, os, fm, ncoef, comp, mn,
                                                       best, bidx, hook);
+    }
     exec += (unsigned long long)n_ent * NB;
 #pragma unroll
     for (int r = 0; r < NB; ++r) best[r] = mn[r].get();
@@ -946,7 +987,12 @@ __device__ __forceinline__ bool sweep_block(const SolveParams& p, const StencilS
       const T old = (D == 2) ? tile_at<D>(lt, 0, r) : tile_at<D>(lt, 0, 0, r);
       T nv = old;
       if (comp[r]) {
-        evals += (unsigned long long)nadm;
+        int fcnt = nadm;
+        if (p.ao3_fb) {
+          const int f = ns->fb[ly * B::BX + lx * NB + r];
+          if (f >= 0) fcnt = __ldg(&p.ao3_count[f]);
+        }
+        evals += (unsigned long long)fcnt;
         T cand = best[r];
         if constexpr (COST == PHJ_COST_NODE) {
           cand = (RULE == PHJ_RULE_KRUZKOV) ? fma(ncoef[r], best[r], T(1) - ncoef[r])
@@ -1838,6 +1884,10 @@ static int solve_impl(const phj_solve_args* a) {
   p.evals = a->evals;
   p.info = a->info;
   p.prune = (a->options & PHJ_SOLVE_NO_PRUNE) ? 0 : 1;
+  p.ao3_fb = a->ao3_fb;
+  p.ao3_mask = a->ao3_mask;
+  p.ao3_count = a->ao3_count;
+  p.ao3_words = a->ao3_words;
   const int64_t ws_bytes = workspace_bytes<D>(a->grid, a->max_sweeps);
   PHJ_CUDA(cudaMemsetAsync(a->workspace, 0, ws_bytes, stream));
   PHJ_CUDA(cudaMemsetAsync(a->maxch_hist, 0, sizeof(double) * (size_t)a->max_sweeps * a->n_patches,
@@ -1884,6 +1934,12 @@ extern "C" int phj_solve(const phj_solve_args* a) {
   }
   if (a->n_patches < 1 || a->n_patches > kMaxPatches || a->max_sweeps < 1) {
     phj_set_error("phj_solve: n_patches must be in [1, %d], max_sweeps >= 1", kMaxPatches);
+    return PHJ_ERR_ARG;
+  }
+  if (a->ao3_fb && (!a->ao3_mask || !a->ao3_count || a->ao3_words < 1 || a->ao3_words > 2 ||
+                    a->st.n_classes != 1)) {
+    phj_set_error("phj_solve: AO3 needs masks/counts, 1..2 mask words (<= 128 stencil entries) "
+                  "and a single-class stencil");
     return PHJ_ERR_ARG;
   }
   if (((uintptr_t)a->lab & 3) != 0) {

@@ -334,10 +334,47 @@ def assemble_internal(gs, best_val: torch.Tensor, best_idx: torch.Tensor, n_colo
     return color, n_unc, boundary, lab
 
 
+def ao3_tables(plan: StencilPlan, spec: ProblemSpec, fb_int: torch.Tensor, r: float):
+    """Device tables of the conical control reduction AO3 (solver.py:446-476,
+    patchy.py:353-356) for the patch solves: per node its feedback control
+    (ext layout), per feedback control the allowed stencil entries (bitmask
+    over the class-0 entry order, padding included) and the number of allowed
+    admissible controls (candidate-evaluation count).  None when the control
+    geometry is not unit-norm (the reference then keeps every control)."""
+    cs = spec.control_set
+    if not cs.is_unit:
+        return None
+    st = plan.stencils
+    if st.n_classes != 1:
+        raise ConfigurationError("conical reduction needs a single-class stencil")
+    controls = np.asarray(cs.controls, dtype=float)
+    thresh = np.cos(np.pi / r) - 1.0e-12
+    pair_ok = controls @ controls.T >= thresh                      # [nc, nc]
+    ctrl = st.ctrl[:st.nc].astype(np.int64)
+    noct = st.oct_start.shape[1] - 1
+    e0, e1 = int(st.oct_start[0, 0]), int(st.oct_start[0, noct])
+    if e1 > 128:
+        raise ConfigurationError("conical reduction supports at most 128 stencil entries")
+    words = 1 if e1 <= 64 else 2
+    adm = np.unique(ctrl[e0:e1])
+    nc = controls.shape[0]
+    mask = np.zeros((nc, words), dtype=np.uint64)
+    for e in range(e0, e1):
+        ok = pair_ok[:, ctrl[e]]
+        mask[ok, e >> 6] |= np.uint64(1) << np.uint64(e & 63)
+    count = pair_ok[:, adm].sum(axis=1).astype(np.int32)
+    dev = plan.device
+    fbx = torch.full(plan.int_ext, -1, dtype=torch.int32, device=dev)
+    plan.interior_int(fbx).copy_(fb_int.to(dev, torch.int32).view(plan.int_shape))
+    _sync_periodic(plan, fbx)
+    return (fbx, torch.as_tensor(mask.view(np.int64), device=dev),
+            torch.as_tensor(count, device=dev), words)
+
+
 def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Tensor,
                            n_patches: int, pcfg: PatchyConfig, cfg: SolverConfig,
                            lifted_work: Optional[torch.Tensor] = None,
-                           work: Optional[torch.Tensor] = None):
+                           work: Optional[torch.Tensor] = None, ao3=None):
     """All patches on the device (patchy.py:304-389).  `color` per internal
     serial.  Returns (working result, [SweepStats], warnings, performed)."""
     rule, dtype = cfg.rule, cfg.dtype
@@ -354,6 +391,15 @@ def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Te
         inner_w.copy_(torch.where(col3 >= 0, seed, inner_w))
         _sync_periodic(plan, work)
     sizes = torch.bincount(color[color >= 0].long(), minlength=n_patches)[:n_patches].cpu().numpy()
+    cands = None  # AO3: candidates per sweep per patch (reduced control sets)
+    if ao3 is not None:
+        fbx, _, acount, _ = ao3
+        fser = plan.interior_int(fbx).reshape(-1)
+        per = torch.where(fser >= 0, acount[fser.clamp(min=0).long()],
+                          torch.full_like(fser, plan.n_adm)).to(torch.float64)
+        sel = color >= 0
+        cands = torch.bincount(color[sel].long(), weights=per[sel],
+                               minlength=n_patches)[:n_patches].cpu().numpy()
     rank, world = dist.world()
     mine = dist.mine_mask(sizes, rank, world, dev)
     warnings = []
@@ -367,6 +413,7 @@ def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Te
     if pcfg.bc_mode == STATE_CONSTRAINT:
         fmask = plan.fmask_from_labels(lab)
         res = device_solve(plan, work, lab, fmask, n_patches, rule=rule, dtype=dtype, tol=cfg.tol,
+                           ao3=ao3,
                            max_sweeps=cfg.sweep_limit(plan.grid), mine=mine)
         out = res.values
         performed = res.evals
@@ -379,7 +426,8 @@ def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Te
             if mine is not None and not bool(mine[j]):
                 stats.append(SweepStats())
                 continue
-            stats.append(stats_for_patch(res, j, int(sizes[j]), plan.n_adm, cfg.tol))
+            stats.append(stats_for_patch(res, j, int(sizes[j]), plan.n_adm, cfg.tol,
+                                         cands_per_sweep=None if cands is None else cands[j]))
     else:
         # Dirichlet: out-of-patch reads see the frozen lifted field with
         # UNREACHABLE forced to the sentinel (patchy.py:340-347); one launch per
@@ -404,7 +452,7 @@ def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Te
             li = plan.interior_int(labj)
             li.copy_(torch.where(own, torch.zeros_like(li), li))
             _sync_periodic(plan, labj)
-            res = device_solve(plan, w, labj, plan.fmask_hard, 1, rule=rule, dtype=dtype,
+            res = device_solve(plan, w, labj, plan.fmask_hard, 1, rule=rule, dtype=dtype, ao3=ao3,
                                tol=cfg.tol, max_sweeps=cfg.sweep_limit(plan.grid))
             oi = plan.interior_int(out)
             oi.copy_(torch.where(own, plan.interior_int(res.values), oi))
@@ -412,7 +460,8 @@ def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Te
             executed += res.executed
             kernel_ms += res.device_ms
             sweeps_total += int(res.info[0])
-            stats.append(stats_for_patch(res, 0, int(sizes[j]), plan.n_adm, cfg.tol))
+            stats.append(stats_for_patch(res, 0, int(sizes[j]), plan.n_adm, cfg.tol,
+                                         cands_per_sweep=None if cands is None else cands[j]))
         _sync_periodic(plan, out)
     if world > 1:
         dist.gather_min(out)
@@ -526,11 +575,15 @@ def solve_patches(spec: ProblemSpec, grid: Grid, patch_map: PatchMap, lifted: No
     """Independent patch solves merged into one field (patchy.py:304-389).
     Returns (NodeField, list[SweepStats], warnings)."""
     cfg = cfg or SolverConfig()
-    if pcfg.reduction is not None:
-        if feedback is None:
-            raise ConfigurationError("conical reduction needs a feedback field")
-        raise ConfigurationError("conical reduction (AO3) is not on the device path")
+    if pcfg.reduction is not None and feedback is None:
+        raise ConfigurationError("conical reduction needs a feedback field")
     plan = table if table is not None else StencilPlan(grid, spec)
+    ao3 = None
+    if pcfg.reduction is not None:
+        fi = feedback.indices
+        fi = fi if isinstance(fi, torch.Tensor) else torch.as_tensor(np.asarray(fi))
+        fb_int = plan.serial_to_internal(fi.to(plan.device, torch.int32)).contiguous()
+        ao3 = ao3_tables(plan, spec, fb_int, float(pcfg.reduction))
     color_int = plan.serial_to_internal(patch_map.color.to(plan.device)).contiguous()
     lab = torch.full(plan.int_ext, _lib.LAB_HARD, dtype=torch.int16, device=plan.device)
     li = plan.interior_int(lab)
@@ -542,7 +595,7 @@ def solve_patches(spec: ProblemSpec, grid: Grid, patch_map: PatchMap, lifted: No
     lw = plan.working_from_user(lifted.values, cfg.rule, cfg.dtype)
     work = None if field is None else plan.working_from_user(field.values, cfg.rule, cfg.dtype)
     out, stats, warnings, _ = solve_patches_internal(plan, color_int, lab, patch_map.n_patches,
-                                                     pcfg, cfg, lw, work)
+                                                     pcfg, cfg, lw, work, ao3=ao3)
     res = NodeField(grid, plan.user_from_working(out, cfg.rule, cfg.dtype))
     if field is not None:
         field.values.copy_(res.values)
@@ -602,8 +655,10 @@ def run_patchy(spec: ProblemSpec, pcfg: PatchyConfig, cfg: Optional[SolverConfig
             fplan.gs, best_val, best_idx, n_colors, mask, fplan.kind, fine_grid.n_interior,
             fplan.device, stats.warnings)
     with stats.phase("patch_solve"):
+        ao3 = (ao3_tables(fplan, spec, fb, float(pcfg.reduction))
+               if pcfg.reduction is not None else None)
         out, pstats, warnings, pinfo = solve_patches_internal(
-            fplan, color, lab, n_colors, pcfg, cfg, vf)
+            fplan, color, lab, n_colors, pcfg, cfg, vf, ao3=ao3)
         stats.warnings.extend(warnings)
         for st in pstats:
             stats.merge_counts(st)

@@ -381,7 +381,7 @@ class DeviceSolveResult:
 def device_solve(plan: StencilPlan, work: torch.Tensor, lab: torch.Tensor, fmask: torch.Tensor,
                  n_patches: int, *, rule: str, dtype: str, tol: float, max_sweeps: int,
                  mine: Optional[torch.Tensor] = None, sync: bool = True,
-                 prune: bool = True) -> DeviceSolveResult:
+                 prune: bool = True, ao3=None) -> DeviceSolveResult:
     """One phj_solve launch: all patches of `lab`, to per-patch convergence."""
     lib = _lib.load()
     dev = plan.device
@@ -414,6 +414,12 @@ def device_solve(plan: StencilPlan, work: torch.Tensor, lab: torch.Tensor, fmask
     a.evals = _lib.ptr(ev)
     a.info = _lib.ptr(info)
     a.options = 0 if prune else _lib.SOLVE_NO_PRUNE
+    if ao3 is not None:
+        fbx, amask, acount, words = ao3
+        a.ao3_fb = _lib.ptr(fbx)
+        a.ao3_mask = _lib.ptr(amask)
+        a.ao3_count = _lib.ptr(acount)
+        a.ao3_words = int(words)
     a.stream = _lib.stream_handle()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -442,7 +448,7 @@ def active_blocks_per_sweep(plan: StencilPlan, ws: torch.Tensor, max_sweeps: int
 
 
 def stats_for_patch(res: DeviceSolveResult, p: int, n_nodes: int, n_adm: int, tol: float,
-                    label: str = "") -> SweepStats:
+                    label: str = "", cands_per_sweep: Optional[int] = None) -> SweepStats:
     s = int(res.patch_sweeps[p])
     st = SweepStats()
     if n_nodes == 0:
@@ -451,7 +457,8 @@ def stats_for_patch(res: DeviceSolveResult, p: int, n_nodes: int, n_adm: int, to
     st.converged = s > 0
     st.max_change = float(res.maxch[st.sweeps - 1, p]) if st.sweeps > 0 else 0.0
     st.node_relaxations = n_nodes * st.sweeps
-    st.candidate_evals = n_nodes * n_adm * st.sweeps
+    st.candidate_evals = (n_nodes * n_adm if cands_per_sweep is None
+                          else int(cands_per_sweep)) * st.sweeps
     if not st.converged:
         st.warning = (f"{label}no convergence after {st.sweeps} sweeps "
                       f"(max change {st.max_change:.3e} > tol {tol:.1e})")

@@ -336,3 +336,36 @@ def test_dubins_small_matches_oracle():
     got = _to_v(_flat(u.numpy()))
     inner = og.interior_flat()
     assert np.abs(got[inner] - v[inner]).max() <= 1e-8
+
+
+@pytest.mark.parametrize("r", [3, 6])
+def test_c1_patch_solves_with_conical_reduction(r):
+    """AO3 (solver.py:446-476, patchy.py:353-356) on the config-1 patch map:
+    device patch solves with reduction r match the reference's reduced GS
+    solves (golden) within the fixed-point bar, and the oracle's reduced
+    Jacobi solves; the candidate-evaluation counts follow the reduced
+    control sets (fewer than the full solve)."""
+    c = golden("c1_patchy.npz")
+    a = golden("c1_patchy_ao3.npz")
+    spec = _eik_spec((-2.0, -2.0), (2.0, 2.0), C.circle(32), 0.1)
+    g = phj.Grid(spec.box_lo, spec.box_hi, (101, 101))
+    lifted = phj.NodeField(g, c["lifted"])
+    fb, _ = phj.extract_feedback(lifted, spec)
+    pm = phj.PatchMap(g, 4, torch.as_tensor(c["color"]))
+    cfg = phj.SolverConfig(tol=1e-8)
+    val, pst, _ = phj.solve_patches(spec, g, pm, lifted,
+                                    phj.PatchyConfig(n_patches=4, reduction=float(r)), cfg,
+                                    feedback=fb)
+    got = _flat(val.numpy())
+    assert _live_close(got, _flat(a[f"value_r{r}"]), 1e-8) <= 1e-8
+    pr = C.c1_fine()
+    allowed = O.allowed_mask(pr.controls, c["feedback"], float(r))
+    ov, _ = O.solve_patches(pr, c["color"], 4, rule="reference", mode="jacobi", tol=1e-8,
+                            allowed=allowed)
+    assert _live_close(got, ov, 1e-8) <= 1e-8
+    # candidate counts follow the reduced control sets: the reference's GS
+    # counts are (its sweeps) x (allowed candidates per sweep); ours use our
+    # Jacobi sweep counts, so compare the per-sweep figure
+    for j, s in enumerate(pst):
+        ref_per_sweep = int(a[f"evals_r{r}"][j]) / int(a[f"sweeps_r{r}"][j])
+        assert s.candidate_evals / s.sweeps == ref_per_sweep
