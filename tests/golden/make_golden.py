@@ -239,6 +239,19 @@ def main_ao3():
               [s.candidate_evals for s in pst])
     np.savez_compressed(os.path.join(OUT, "c1_patchy_ao3.npz"), **out)
 
+    # -- G8: Dirichlet patch boundary condition and AO1 warm start
+    #        (patchy.py:334-347) on the same patch map
+    out = {}
+    for key, kw in (("dirichlet", dict(bc_mode="dirichlet")),
+                    ("warm", dict(warm_start=True)),
+                    ("dirichlet_warm", dict(bc_mode="dirichlet", warm_start=True))):
+        pcfg = phj.PatchyConfig(n_patches=4, coarse_nodes=26, fine_nodes=101, **kw)
+        val, pst, _ = phj.solve_patches(spec1, g1, pm, lifted, pcfg, cfg, table=t1)
+        out[f"value_{key}"] = val.values
+        out[f"sweeps_{key}"] = np.array([s.sweeps for s in pst])
+        print(key, "sweeps", [s.sweeps for s in pst])
+    np.savez_compressed(os.path.join(OUT, "c1_patchy_bc.npz"), **out)
+
 
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "ao3":

@@ -369,3 +369,26 @@ def test_c1_patch_solves_with_conical_reduction(r):
     for j, s in enumerate(pst):
         ref_per_sweep = int(a[f"evals_r{r}"][j]) / int(a[f"sweeps_r{r}"][j])
         assert s.candidate_evals / s.sweeps == ref_per_sweep
+
+
+@pytest.mark.parametrize("key,kw", [("dirichlet", dict(bc_mode="dirichlet")),
+                                    ("warm", dict(warm_start=True)),
+                                    ("dirichlet_warm", dict(bc_mode="dirichlet",
+                                                            warm_start=True))])
+def test_c1_patch_solves_dirichlet_and_warm_start(key, kw):
+    """Dirichlet patch BC / AO1 warm start (patchy.py:334-347): device patch
+    solves match the reference's (golden, GS) and the oracle's Jacobi solves
+    within the fixed-point bar."""
+    c = golden("c1_patchy.npz")
+    b = golden("c1_patchy_bc.npz")
+    spec = _eik_spec((-2.0, -2.0), (2.0, 2.0), C.circle(32), 0.1)
+    g = phj.Grid(spec.box_lo, spec.box_hi, (101, 101))
+    lifted = phj.NodeField(g, c["lifted"])
+    pm = phj.PatchMap(g, 4, torch.as_tensor(c["color"]))
+    val, pst, _ = phj.solve_patches(spec, g, pm, lifted, phj.PatchyConfig(n_patches=4, **kw),
+                                    phj.SolverConfig(tol=1e-8))
+    got = _flat(val.numpy())
+    assert _live_close(got, _flat(b[f"value_{key}"]), 1e-8) <= 1e-8
+    ov, _ = O.solve_patches(C.c1_fine(), c["color"], 4, rule="reference", mode="jacobi",
+                            tol=1e-8, lifted=_flat(c["lifted"]), **kw)
+    assert _live_close(got, ov, 1e-8) <= 1e-8

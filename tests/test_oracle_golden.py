@@ -175,3 +175,19 @@ def test_c1_patch_solves_with_conical_reduction_bit_exact():
         assert np.array_equal(val, _flat(a[f"value_r{r}"]))
         assert [s.sweeps for s in pst] == [int(x) for x in a[f"sweeps_r{r}"]]
         assert [s.candidate_evals for s in pst] == [int(x) for x in a[f"evals_r{r}"]]
+
+
+def test_c1_patch_solves_dirichlet_and_warm_start_bit_exact():
+    """Dirichlet patch boundary condition and AO1 warm start
+    (patchy.py:334-347) on the config-1 patch map: bit-exact with the
+    reference, same sweep counts."""
+    c = golden("c1_patchy.npz")
+    b = golden("c1_patchy_bc.npz")
+    pr = C.c1_fine()
+    lifted = _flat(c["lifted"])
+    for key, kw in (("dirichlet", dict(bc_mode="dirichlet")), ("warm", dict(warm_start=True)),
+                    ("dirichlet_warm", dict(bc_mode="dirichlet", warm_start=True))):
+        val, pst = P.solve_patches(pr, c["color"], 4, rule="reference", mode="gs", tol=1e-8,
+                                   lifted=lifted, **kw)
+        assert np.array_equal(val, _flat(b[f"value_{key}"])), key
+        assert [s.sweeps for s in pst] == [int(x) for x in b[f"sweeps_{key}"]], key
