@@ -1637,6 +1637,451 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
   if (threadIdx.x == 0) atomicAdd(p.updates, s_up);
 }
 
+// ---------------------------------------------------------------------------
+// Two Jacobi sweeps per grid barrier (default transport; PHJ_TRANSPORT_T1=1
+// selects the one-sweep kernel above).
+//
+// The transport is a linear map with fixed feet, so an active block can run
+// sweeps k and k+1 back to back: it stages its 2-ring halo of colour j,
+// computes sweep k on the block plus a 1-node ring (the ring values are the
+// same Jacobi images the neighbour blocks compute; recomputing them costs a
+// few FMAs per node), then sweep k+1 on its own nodes from shared memory.
+// Only the sweep-(k+1) values are written, into the other buffer, so no
+// block ever reads a value another block overwrites in the same pass.
+// Activity: a block is swept for colour j in pass m if colour j changed (by
+// more than act_eps) in pass m-1 within its neighbourhood -- 3x3 blocks in
+// 2D, and +-2 planes along internal axis 0 in 3D (blocks are one plane
+// thick there, and a change reaches two planes in one pass).  Per-colour
+// stopping is decided per sweep exactly as in the one-sweep kernel (max
+// change over the swept nodes of each of the two sweeps); a colour that
+// stops after the first sweep of a pass gets that sweep recomputed densely
+// from the pass's input buffer at the end.
+template <int D>
+struct T2Shape {
+  using B = Blk<D>;
+  static constexpr int PL = (D == 2) ? 1 : 5;         // axis-0 planes in the tile (3D)
+  static constexpr int RB = B::BY + 4;                // rows per plane
+  static constexpr int W = B::BX + 4;                 // columns
+  static constexpr int C = W + (W % 2 == 0);          // row pitch (odd: banks)
+  static constexpr int N = PL * RB * C;
+  static constexpr int RPL = (D == 2) ? 1 : 3;        // ring planes
+  static constexpr int RRB = B::BY + 2;               // ring rows per plane
+  static constexpr int RW = B::BX + 2;                // ring columns
+  static constexpr int RN = RPL * RRB * RW;
+  static constexpr int NNB = (D == 2) ? 9 : 45;       // neighbour blocks marked
+};
+
+template <int D>
+struct T2Warp {  // per-warp shared memory
+  double tile[T2Shape<D>::N];
+  double ring[T2Shape<D>::RN];
+  int rent[T2Shape<D>::RN];  // stencil entry of each ring node (-1: holds its value)
+};
+
+// neighbour nid of block t for the two-sweep transport (-1 outside)
+template <int D>
+__device__ inline int t2_neighbour(const TileGrid& tg, const phj_grid& g, int t, int nid) {
+  if (D == 2) return neighbour_block<D>(tg, g, t, nid);
+  const int* n = tg.n;
+  int b[3];
+  decode_block<D>(tg, t, b);
+  int a = b[0] + nid / 9 - 2, c = b[1] + (nid / 3) % 3 - 1, e = b[2] + nid % 3 - 1;
+  if (g.periodic[0]) a = ((a % n[0]) + n[0]) % n[0];
+  if (a < 0 || a >= n[0] || c < 0 || c >= n[1] || e < 0 || e >= n[2]) return -1;
+  return (a * n[1] + c) * n[2] + e;
+}
+
+// interior index along internal axis 0 -> ext index, wrapped on a periodic
+// axis and clamped otherwise (clamped values only feed non-movers)
+__device__ __forceinline__ int t2_axis0_ext(const phj_grid& g, int q) {
+  const int n0 = (int)g.shape[0];
+  if (g.periodic[0]) q = ((q % n0) + n0) % n0;
+  else q = max(-1, min(q, n0));
+  return q + 1;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS)
+    transport_kernel2(const __grid_constant__ TransportParams p) {
+  using B = Blk<D>;
+  using S = T2Shape<D>;
+  constexpr int NC = 1 << D;
+  constexpr int NB = B::NB;
+  extern __shared__ __align__(16) unsigned char smem[];
+  cg::grid_group grid = cg::this_grid();
+  const int nent = p.n_classes * p.nc;
+  const int R = p.R;
+  // weights corner-major with an odd pitch (as in transport_kernel)
+  const int wpitch = nent | 1;
+  double* s_w = (double*)smem;                                                   // [NC][wpitch]
+  unsigned long long* s_max = (unsigned long long*)(s_w + (int64_t)wpitch * NC);  // [2][R]
+  int* s_done = (int*)(s_max + 2 * R);                      // [R] sweeps done (0x7fffffff running)
+  signed char* s_oct = (signed char*)(s_done + R);          // [nent]
+  T2Warp<D>* wsm =
+      (T2Warp<D>*)(smem + align_up((int64_t)wpitch * NC * 8 + 16 * R + 4 * R + nent, 16)) +
+      (threadIdx.x >> 5);
+  for (int i = threadIdx.x; i < nent * NC; i += blockDim.x)
+    s_w[(i % NC) * wpitch + i / NC] = p.weights[i];
+  for (int i = threadIdx.x; i < R; i += blockDim.x) s_done[i] = 0x7fffffff;
+  for (int cls = 0; cls < p.n_classes; ++cls) {
+    const int32_t* os = p.oct_start + cls * (NC + 1);
+    for (int e = os[0] + threadIdx.x; e < os[NC]; e += blockDim.x) {
+      int oc = 0;
+      while (oc < NC - 1 && e >= os[oc + 1]) ++oc;
+      s_oct[e] = (signed char)oc;
+    }
+  }
+  __syncthreads();
+  const unsigned FULL = 0xffffffffu;
+  const phj_grid& g = p.g;
+  const int lane = threadIdx.x & 31;
+  const int ly = lane / B::LX, lx = lane % B::LX;
+  const int64_t M0 = g.shape[0];
+  const bool per0 = g.periodic[0] != 0;
+  const int64_t ghost_shift = M0 * g.strides[0];
+  // corner offsets (bit ax = +1 along axis ax) in tile and ring coordinates
+  int toff[NC], roff[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    int t = 0, r = 0;
+    if (D == 2) {
+      t = ((k & 1) ? S::C : 0) + ((k >> 1) & 1);
+      r = ((k & 1) ? S::RW : 0) + ((k >> 1) & 1);
+    } else {
+      t = ((k & 1) ? S::RB * S::C : 0) + (((k >> 1) & 1) ? S::C : 0) + ((k >> 2) & 1);
+      r = ((k & 1) ? S::RRB * S::RW : 0) + (((k >> 1) & 1) ? S::RW : 0) + ((k >> 2) & 1);
+    }
+    toff[k] = t;
+    roff[k] = r;
+  }
+  unsigned long long upd = 0;
+  int m = 0, buf = 0;
+  const int gwarp = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const int nwarps = gridDim.x * kWarps;
+  int ticket = 0;
+  if (lane == 0) ticket = atomicAdd(&p.ws.take[0], 1);
+  for (;;) {
+    const double* pin = p.phi[buf];
+    double* pout = p.phi[buf ^ 1];
+    const int cnt = ld_cg(&p.ws.counts[m]);
+    const int* list = p.ws.list[m & 1];
+    int* cur_flags = p.ws.flags[m & 1];
+    unsigned long long* cur_mask = p.ws.cmask[m & 1];
+    unsigned long long* nxt_mask = p.ws.cmask[(m + 1) & 1];
+    int* nxt_list = p.ws.list[(m + 1) & 1];
+    int* nxt_cnt = &p.ws.counts[m + 1];
+    int* take = &p.ws.take[m];
+    for (int i = threadIdx.x; i < 2 * R; i += blockDim.x) s_max[i] = 0ull;
+    if (blockIdx.x == 0) {
+      unsigned long long* z0 = sweep_max_slots(p.ws, 2 * m + 2);
+      unsigned long long* z1 = sweep_max_slots(p.ws, 2 * m + 3);
+      for (int i = threadIdx.x; i < R; i += blockDim.x) {
+        z0[i * kMaxPad] = 0ull;
+        z1[i * kMaxPad] = 0ull;
+      }
+    }
+    __syncthreads();
+    int item = gwarp;
+    while (item < cnt) {
+      const int blk = __ldcg(&list[item]);
+      const int nxt = nwarps + __shfl_sync(FULL, ticket, 0);
+      if (lane == 0 && nxt < cnt) ticket = atomicAdd(take, 1);
+      unsigned long long cm = 0ull;
+      if (lane == 0) {
+        cm = __ldcg(&cur_mask[blk]);
+        cur_mask[blk] = 0ull;
+        cur_flags[blk] = 0;
+      }
+      cm = __shfl_sync(FULL, cm, 0);
+      int bc[3];
+      decode_block<D>(p.tg, blk, bc);
+      // block origin: interior coordinates of its first node
+      const int o0 = (D == 2) ? bc[0] * B::BY : bc[0];
+      const int o1 = (D == 2) ? bc[1] * B::BX : bc[1] * B::BY;
+      const int o2 = (D == 2) ? 0 : bc[2] * B::BX;
+      // ring entries (stencil entry of each ring node's feedback, -1 = holds)
+      for (int q = lane; q < S::RN; q += 32) {
+        int i0, i1, i2 = 0;
+        if (D == 2) {
+          i0 = o0 - 1 + q / S::RW;
+          i1 = o1 - 1 + q % S::RW;
+        } else {
+          const int pl = q / (S::RRB * S::RW), rem = q - pl * S::RRB * S::RW;
+          i0 = o0 - 1 + pl;
+          i1 = o1 - 1 + rem / S::RW;
+          i2 = o2 - 1 + rem % S::RW;
+        }
+        if (per0) i0 = ((i0 % (int)M0) + (int)M0) % (int)M0;
+        int e = -1;
+        const bool inside = i0 >= 0 && i0 < M0 && i1 >= 0 && i1 < g.shape[1] &&
+                            (D == 2 || (i2 >= 0 && i2 < g.shape[2]));
+        if (inside) {
+          const int64_t sidx = (D == 2) ? (int64_t)i0 * g.shape[1] + i1
+                                        : ((int64_t)i0 * g.shape[1] + i1) * g.shape[2] + i2;
+          e = __ldg(&p.ent[sidx]);
+        }
+        wsm->rent[q] = e;
+      }
+      __syncwarp();
+      // own nodes: ring position and interior validity
+      int rpos[NB];
+      bool own_in[NB];
+#pragma unroll
+      for (int r = 0; r < NB; ++r) {
+        const int rr = ly + 1, rc = lx * NB + r + 1;
+        rpos[r] = (D == 2) ? rr * S::RW + rc : (1 * S::RRB + rr) * S::RW + rc;
+        const int i1 = (D == 2) ? o0 + ly : o1 + ly;
+        const int ilast = (D == 2) ? o1 + lx * NB + r : o2 + lx * NB + r;
+        own_in[r] = (D == 2) ? (i1 < M0 && ilast < g.shape[1])
+                             : (i1 < g.shape[1] && ilast < g.shape[2]);
+        if (own_in[r] && wsm->rent[rpos[r]] >= 0) upd += 2;  // two sweeps
+      }
+      unsigned long long changed = 0ull;
+      const bool masked = R <= 64;
+      unsigned long long todo = masked ? cm : 0ull;
+      int jnext = 0;
+      for (;;) {
+        int j;
+        if (masked) {
+          if (!todo) break;
+          j = __ffsll((long long)todo) - 1;
+          todo &= todo - 1;
+        } else {
+          if (jnext >= R) break;
+          j = jnext++;
+        }
+        if (s_done[j] != 0x7fffffff) continue;  // stopped colours are never touched again
+        const double* pj = pin + (int64_t)j * p.plane;
+        double* qj = pout + (int64_t)j * p.plane;
+        // stage the 2-ring tile of colour j (rows wrapped / clamped on axis 0)
+        for (int rrow = lane; rrow < S::PL * S::RB; rrow += 32) {
+          int64_t rbase;
+          if (D == 2) {
+            const int e0 = t2_axis0_ext(g, o0 - 2 + rrow);
+            rbase = (int64_t)e0 * g.strides[0];
+          } else {
+            const int pl = rrow / S::RB, rr = rrow - pl * S::RB;
+            const int e0 = t2_axis0_ext(g, o0 - 2 + pl);
+            const int e1 = max(0, min(o1 - 1 + rr, (int)g.ext[1] - 1));
+            rbase = (int64_t)e0 * g.strides[0] + (int64_t)e1 * g.strides[1];
+          }
+          const int cmax = (int)g.ext[D - 1] - 1;
+          const int c0 = (D == 2) ? o1 - 1 : o2 - 1;
+#pragma unroll
+          for (int c = 0; c < S::W; ++c)
+            cp_async<8>(&wsm->tile[rrow * S::C + c], pj + rbase + max(0, min(c0 + c, cmax)));
+        }
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncwarp();
+        // sweep k on the block + 1-node ring
+        for (int q = lane; q < S::RN; q += 32) {
+          int tp;
+          if (D == 2) tp = (q / S::RW + 1) * S::C + q % S::RW + 1;
+          else {
+            const int pl = q / (S::RRB * S::RW), rem = q - pl * S::RRB * S::RW;
+            tp = ((pl + 1) * S::RB + rem / S::RW + 1) * S::C + rem % S::RW + 1;
+          }
+          const int e = wsm->rent[q];
+          double v = wsm->tile[tp];
+          if (e >= 0) {
+            const int oc = s_oct[e];
+            int lo = tp;  // lower corner of the foot cell
+            if (D == 2) {
+              if (!(oc & 1)) lo -= S::C;
+              if (!((oc >> 1) & 1)) lo -= 1;
+            } else {
+              if (!(oc & 1)) lo -= S::RB * S::C;
+              if (!((oc >> 1) & 1)) lo -= S::C;
+              if (!((oc >> 2) & 1)) lo -= 1;
+            }
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < NC; ++k) acc = fma(s_w[k * wpitch + e], wsm->tile[lo + toff[k]], acc);
+            v = acc;
+          }
+          wsm->ring[q] = v;
+        }
+        __syncwarp();
+        // sweep k + 1 on the own nodes
+        double l0 = 0.0, l1 = 0.0;
+#pragma unroll
+        for (int r = 0; r < NB; ++r) {
+          if (!own_in[r]) continue;
+          const int q = rpos[r];
+          const int e = wsm->rent[q];
+          if (e < 0) continue;
+          int tp;
+          if (D == 2) tp = (q / S::RW + 1) * S::C + q % S::RW + 1;
+          else {
+            const int pl = q / (S::RRB * S::RW), rem = q - pl * S::RRB * S::RW;
+            tp = ((pl + 1) * S::RB + rem / S::RW + 1) * S::C + rem % S::RW + 1;
+          }
+          const double vk = wsm->ring[q];
+          l0 = fmax(l0, fabs(wsm->tile[tp] - vk));
+          const int oc = s_oct[e];
+          int lo = q;
+          if (D == 2) {
+            if (!(oc & 1)) lo -= S::RW;
+            if (!((oc >> 1) & 1)) lo -= 1;
+          } else {
+            if (!(oc & 1)) lo -= S::RRB * S::RW;
+            if (!((oc >> 1) & 1)) lo -= S::RW;
+            if (!((oc >> 2) & 1)) lo -= 1;
+          }
+          double acc = 0.0;
+#pragma unroll
+          for (int k = 0; k < NC; ++k) acc = fma(s_w[k * wpitch + e], wsm->ring[lo + roff[k]], acc);
+          l1 = fmax(l1, fabs(vk - acc));
+          int c[3];
+          if (D == 2) {
+            c[0] = o0 + ly;
+            c[1] = o1 + lx * NB + r;
+          } else {
+            c[0] = o0;
+            c[1] = o1 + ly;
+            c[2] = o2 + lx * NB + r;
+          }
+          const int64_t f = ext_flat<D>(g, c);
+          qj[f] = acc;
+          if (per0) {
+            if (c[0] == 0) qj[f + ghost_shift] = acc;
+            else if (c[0] == M0 - 1) qj[f - ghost_shift] = acc;
+          }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          l0 = fmax(l0, __shfl_xor_sync(FULL, l0, off));
+          l1 = fmax(l1, __shfl_xor_sync(FULL, l1, off));
+        }
+        if (lane == 0) {
+          if (l0 > 0.0) atomicMax(&s_max[j], dbits(l0));
+          if (l1 > 0.0) atomicMax(&s_max[R + j], dbits(l1));
+        }
+        if (fmax(l0, l1) > p.act_eps) changed |= (j < 64) ? (1ull << j) : ~0ull;
+        __syncwarp();
+      }
+      // mark the neighbourhood for the next pass
+      for (int base = 0; base < S::NNB; base += 32) {
+        const int nid = base + lane;
+        int want = 0, nt = -1;
+        if (changed && nid < S::NNB) {
+          nt = t2_neighbour<D>(p.tg, g, blk, nid);
+          if (nt >= 0 && atomicOr(&nxt_mask[nt], changed) == 0ull) want = 1;
+        }
+        const unsigned bal = __ballot_sync(FULL, want);
+        if (bal) {
+          int b0 = 0;
+          if (lane == 0) b0 = atomicAdd(nxt_cnt, __popc(bal));
+          b0 = __shfl_sync(FULL, b0, 0);
+          if (want) nxt_list[b0 + __popc(bal & ((1u << lane) - 1u))] = nt;
+        }
+      }
+      item = nxt;
+    }
+    if (lane == 0 && 2 * m + 2 < p.max_sweeps) ticket = atomicAdd(&p.ws.take[m + 1], 1);
+    __syncthreads();
+    unsigned long long* g0 = sweep_max_slots(p.ws, 2 * m);
+    unsigned long long* g1 = sweep_max_slots(p.ws, 2 * m + 1);
+    for (int i = threadIdx.x; i < R; i += blockDim.x) {
+      if (s_max[i]) atomicMax(&g0[i * kMaxPad], s_max[i]);
+      if (s_max[R + i]) atomicMax(&g1[i * kMaxPad], s_max[R + i]);
+    }
+    grid.sync();
+    ++m;
+    buf ^= 1;
+    int pending = 0;
+    for (int i = threadIdx.x; i < R; i += blockDim.x) {
+      if (s_done[i] == 0x7fffffff) {
+        const unsigned long long b0 = ld_cg(&g0[i * kMaxPad]), b1 = ld_cg(&g1[i * kMaxPad]);
+        if (blockIdx.x == 0) {
+          p.maxch[(int64_t)(2 * m - 2) * R + i] = b0;
+          if (2 * m - 1 < p.max_sweeps) p.maxch[(int64_t)(2 * m - 1) * R + i] = b1;
+        }
+        if (__longlong_as_double((long long)b0) <= p.tol) s_done[i] = 2 * m - 1;
+        else if (__longlong_as_double((long long)b1) <= p.tol) s_done[i] = 2 * m;
+        else pending = 1;
+      }
+    }
+    const int any_pending = __syncthreads_or(pending);
+    if (!any_pending || 2 * m >= p.max_sweeps) break;
+  }
+  // colours that stopped after the first sweep of their last pass: that sweep
+  // again, densely over the movers, from the pass's input buffer into its
+  // output buffer (which then holds every colour's result)
+  grid.sync();
+  const int64_t N = g.shape[0] * g.shape[1] * (D == 3 ? g.shape[2] : 1);
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  for (int j = 0; j < R; ++j) {
+    const int d = s_done[j];
+    if (d == 0x7fffffff || !(d & 1)) continue;
+    const int mj = (d - 1) / 2;  // pass that held the stop
+    const double* rj = p.phi[mj & 1] + (int64_t)j * p.plane;
+    double* wj = p.phi[(mj + 1) & 1] + (int64_t)j * p.plane;
+    for (int64_t sidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; sidx < N; sidx += gstride) {
+      const int e = __ldg(&p.ent[sidx]);
+      if (e < 0) continue;
+      int c[3];
+      if (D == 2) {
+        c[0] = (int)(sidx / g.shape[1]);
+        c[1] = (int)(sidx % g.shape[1]);
+        c[2] = 0;
+      } else {
+        c[2] = (int)(sidx % g.shape[2]);
+        const int64_t r2 = sidx / g.shape[2];
+        c[1] = (int)(r2 % g.shape[1]);
+        c[0] = (int)(r2 / g.shape[1]);
+      }
+      const int64_t f = ext_flat<D>(g, c);
+      const int oc = s_oct[e];
+      int64_t lo = f;
+#pragma unroll
+      for (int ax = 0; ax < D; ++ax)
+        if (!((oc >> ax) & 1)) lo -= g.strides[ax];
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        int64_t o = 0;
+#pragma unroll
+        for (int ax = 0; ax < D; ++ax)
+          if ((k >> ax) & 1) o += g.strides[ax];
+        acc = fma(__ldg(&p.weights[(int64_t)e * NC + k]), rj[lo + o], acc);
+      }
+      wj[f] = acc;
+      if (per0) {
+        if (c[0] == 0) wj[f + ghost_shift] = acc;
+        else if (c[0] == M0 - 1) wj[f - ghost_shift] = acc;
+      }
+    }
+  }
+  grid.sync();
+  // every colour's result into buffer 0 (the output buffer of its last pass)
+  const int mfin = m;  // passes run
+  for (int j = 0; j < R; ++j) {
+    const int d = s_done[j];
+    const int mj = (d == 0x7fffffff) ? mfin - 1 : (d - 1) / 2;
+    if (((mj + 1) & 1) == 0) continue;
+    const double* src = p.phi[1] + (int64_t)j * p.plane;
+    double* dst = p.phi[0] + (int64_t)j * p.plane;
+    for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < p.plane; f += gstride)
+      dst[f] = src[f];
+  }
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i < R; i += blockDim.x)
+      p.color_sweeps[i] = (s_done[i] == 0x7fffffff) ? -(2 * mfin) : s_done[i];
+    if (threadIdx.x == 0) {
+      p.info[0] = 2 * mfin;
+      p.info[1] = 0;
+    }
+  }
+  __shared__ unsigned long long s_up;
+  if (threadIdx.x == 0) s_up = 0;
+  __syncthreads();
+  atomicAdd(&s_up, upd);
+  __syncthreads();
+  if (threadIdx.x == 0) atomicAdd(p.updates, s_up);
+}
+
 // Mover -> stencil entry of its feedback control (patchy.py:165-180: movers
 // are free nodes with a defined feedback and an admissible foot).
 template <int D>
@@ -2028,9 +2473,20 @@ static int transport_impl(const phj_transport_args* a) {
   phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   const int nent = p.n_classes * p.nc;
-  size_t smem = (size_t)(nent | 1) * (1 << D) * 8 + (size_t)p.R * 12 + (size_t)nent + 16;
   void* args[] = {(void*)&p};
-  return coop_launch(transport_kernel<D>, (p.tg.total + kWarps - 1) / kWarps, smem, args, stream,
+  // two sweeps per barrier pay in 2D only (3D: the 2-ring halo is 5 planes
+  // deep and the activity must reach +-2 planes -- measured 2x slower)
+  static const bool one_sweep = getenv("PHJ_TRANSPORT_T1") && atoi(getenv("PHJ_TRANSPORT_T1"));
+  if (one_sweep || D == 3) {
+    size_t smem = (size_t)(nent | 1) * (1 << D) * 8 + (size_t)p.R * 12 + (size_t)nent + 16;
+    return coop_launch(transport_kernel<D>, (p.tg.total + kWarps - 1) / kWarps, smem, args,
+                       stream, nullptr);
+  }
+  size_t smem = (size_t)align_up((int64_t)(nent | 1) * (1 << D) * 8 + 16 * (int64_t)p.R +
+                                     4 * (int64_t)p.R + nent,
+                                 16) +
+                (size_t)kWarps * sizeof(T2Warp<D>);
+  return coop_launch(transport_kernel2<D>, (p.tg.total + kWarps - 1) / kWarps, smem, args, stream,
                      nullptr);
 }
 
