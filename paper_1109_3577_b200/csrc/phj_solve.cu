@@ -301,6 +301,9 @@ __device__ __forceinline__ T finish_cand(T acc, T ca, T cb, T ncoef, uint32_t fm
 #ifndef PHJ_SKIP_EMPTY_OCT
 #define PHJ_SKIP_EMPTY_OCT 1
 #endif
+#ifndef PHJ_EARLY_STAGE
+#define PHJ_EARLY_STAGE 0
+#endif
 template <typename T>
 struct MinAcc;
 template <>
@@ -1197,11 +1200,24 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __gri
     int blk = item < cnt ? __ldcg(&list[item]) : 0;
     if (item < cnt) stage_block<D, T, COST>(p, vin, blk, wtile + stage * S::N, wnodes + stage, lane);
     PatchMax pm{-1, 0.0};
+#if PHJ_EARLY_STAGE
+    // block ids are read two ahead so the next block's staging can start as
+    // soon as the current block's tile has landed
+    int nxt = nwarps + __shfl_sync(FULL, ticket, 0);
+    int nblk = (item < cnt && nxt < cnt) ? __ldcg(&list[nxt]) : 0;
+    if (lane == 0 && item < cnt && nxt < cnt) ticket = atomicAdd(take, 1);
+#endif
     tm.mark(0);
     while (item < cnt) {
+#if PHJ_EARLY_STAGE
+      const int nn = nwarps + __shfl_sync(FULL, ticket, 0);
+      const int nnblk = (nxt < cnt && nn < cnt) ? __ldcg(&list[nn]) : 0;
+      if (lane == 0 && nxt < cnt && nn < cnt) ticket = atomicAdd(take, 1);
+#else
       const int nxt = nwarps + __shfl_sync(FULL, ticket, 0);
       const int nblk = nxt < cnt ? __ldcg(&list[nxt]) : 0;
       if (lane == 0 && nxt < cnt) ticket = atomicAdd(take, 1);
+#endif
       if (lane == 0) cur_flags[blk] = 0;
       if (warp_cls) {
         int bc[3];
@@ -1214,6 +1230,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __gri
       }
       cp_async_wait_all();
       __syncwarp();
+#if PHJ_EARLY_STAGE
+      mq.store(nxt_list);
+      mq.reserve(lane, nxt_cnt);
+      if (nxt < cnt)
+        stage_block<D, T, COST>(p, vin, nblk, wtile + (stage ^ 1) * S::N, wnodes + (stage ^ 1),
+                                lane);
+      auto hook = []() {};
+#else
       auto hook = [&]() {
         mq.store(nxt_list);
         mq.reserve(lane, nxt_cnt);
@@ -1221,6 +1245,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __gri
           stage_block<D, T, COST>(p, vin, nblk, wtile + (stage ^ 1) * S::N, wnodes + (stage ^ 1),
                                   lane);
       };
+#endif
       tm.mark(1);
       const bool ch = sweep_block<D, T, RULE, COST>(p, s, blk, wtile + stage * S::N, wnodes + stage,
                                                     vout, s_done, s_max, gmax_row, evals, exec, pm,
@@ -1231,6 +1256,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __gri
       __syncwarp();  // the buffers of this block are refilled two blocks later
       item = nxt;
       blk = nblk;
+#if PHJ_EARLY_STAGE
+      nxt = nn;
+      nblk = nnblk;
+#endif
       stage ^= 1;
     }
     if (lane == 0 && sw + 1 <= p.max_sweeps) ticket = atomicAdd(&p.ws.take[sw + 1], 1);
