@@ -133,12 +133,27 @@ typedef struct phj_solve_args {
   const int32_t* ao3_count;             /* [n_controls] */
   int32_t ao3_words;                    /* 1 or 2 */
   int32_t options;            /* PHJ_SOLVE_* bits, 0 = defaults */
+  /* activity threshold: a node change re-activates the neighbour blocks only
+   * if it exceeds act_tol in time units (KRUZKOV: dv > act_tol * (1 - v),
+   * REF: du > act_tol * max(1, u)); smaller changes re-sweep their own block
+   * once.  0 = exact Jacobi activity. */
+  double act_tol;
+  /* block-local relaxations per sweep (<= 1: one, plain Jacobi): the block's
+   * nodes are relaxed up to this many times from the staged tile with the
+   * halo ring held at the sweep's input -- block-Jacobi with inner
+   * iterations, same fixed point, schedule-independent */
+  int32_t inner_sweeps;
   void* stream;               /* cudaStream_t */
 } phj_solve_args;
 
 /* phj_solve_args.options: evaluate every octant (disable the exact octant
  * pruning; for verification -- results are bit-identical either way) */
 #define PHJ_SOLVE_NO_PRUNE 1
+/* asynchronous (chaotic) relaxation in one buffer instead of barrier-separated
+ * Jacobi sweeps: same fixed point, to within act_tol (> 0 required); result
+ * in v0, patch_sweeps = equivalent sweeps (blocks swept / initial blocks),
+ * maxch_hist untouched */
+#define PHJ_SOLVE_ASYNC 2
 
 int64_t phj_solve_workspace_bytes(const phj_grid* g, int32_t n_patches, int32_t max_sweeps);
 /* PHJ_UNROLL(dim) this library was built with (octant-group padding) */

@@ -42,7 +42,7 @@ def _eikonal_dyn(X, a):
     return np.tile(np.asarray(a, dtype=float), (X.shape[0], 1))
 
 
-def c1(rule: str = "kruzkov", dtype: str = "float64", scale: int = 1) -> Workload:
+def c1(rule: str = "kruzkov", dtype: str = "float64", schedule: str = "async", scale: int = 1) -> Workload:
     """2D eikonal, 32 circle controls, [-2,2]^2 at 101^2, ball r=0.1, coarse
     26^2, 4 angular pieces, tol 1e-8 (CPU-runnable oracle case)."""
     n = 100 * scale + 1
@@ -54,14 +54,14 @@ def c1(rule: str = "kruzkov", dtype: str = "float64", scale: int = 1) -> Workloa
     pcfg = PatchyConfig(n_patches=4, coarse_nodes=nc_, fine_nodes=n,
                         coarse_target=TargetSpec.ball((0.0, 0.0), max(0.1, kc * np.sqrt(2.0))))
     return Workload("c1", "2D eikonal 101^2, 32 controls, 4 patches", spec, pcfg,
-                    SolverConfig(tol=1e-8, rule=rule, dtype=dtype), (n, n), (nc_, nc_))
+                    SolverConfig(schedule=schedule, tol=1e-8, rule=rule, dtype=dtype), (n, n), (nc_, nc_))
 
 
 def c2_centres(seed: int = SEED_C2) -> np.ndarray:
     return np.random.default_rng(seed).uniform(-0.95, 0.95, (4, 2))
 
 
-def c2(rule: str = "kruzkov", dtype: str = "float64", n: int = 2049, nc_: Optional[int] = None,
+def c2(rule: str = "kruzkov", dtype: str = "float64", schedule: str = "async", n: int = 2049, nc_: Optional[int] = None,
        seed: int = SEED_C2) -> Workload:
     """2D variable speed c = 1 + 0.5 sin(2 pi x) sin(2 pi y), 64 controls,
     [-1,1]^2 at 2049^2, 4 seeded disks r=0.05 -> 8 patches, coarse 513^2."""
@@ -73,11 +73,11 @@ def c2(rule: str = "kruzkov", dtype: str = "float64", n: int = 2049, nc_: Option
     pcfg = PatchyConfig(n_patches=8, coarse_nodes=nc_, fine_nodes=n,
                         parts=partition_balls_halves)
     return Workload("c2", f"2D variable speed {n}^2, 64 controls, 8 patches", spec, pcfg,
-                    SolverConfig(tol=1e-8 if dtype == "float64" else 1e-6, rule=rule,
+                    SolverConfig(schedule=schedule, tol=1e-8 if dtype == "float64" else 1e-6, rule=rule,
                                  dtype=dtype), (n, n), (nc_, nc_))
 
 
-def c3(rule: str = "kruzkov", dtype: str = "float64", n: int = 257,
+def c3(rule: str = "kruzkov", dtype: str = "float64", schedule: str = "async", n: int = 257,
        nc_: Optional[int] = None) -> Workload:
     """3D eikonal, 48 Fibonacci controls, [-1,1]^3 at 257^3, ball r=0.1 in 8
     octant pieces, coarse 65^3."""
@@ -87,7 +87,7 @@ def c3(rule: str = "kruzkov", dtype: str = "float64", n: int = 257,
                        target=TargetSpec.ball((0.0, 0.0, 0.0), 0.1), model=ScaledSpeed(1.0))
     pcfg = PatchyConfig(n_patches=8, coarse_nodes=nc_, fine_nodes=n, parts=partition_octants)
     return Workload("c3", f"3D eikonal {n}^3, 48 controls, 8 patches", spec, pcfg,
-                    SolverConfig(tol=1e-8 if dtype == "float64" else 1e-6, rule=rule,
+                    SolverConfig(schedule=schedule, tol=1e-8 if dtype == "float64" else 1e-6, rule=rule,
                                  dtype=dtype), (n,) * 3, (nc_,) * 3)
 
 
@@ -101,7 +101,7 @@ def theta_slabs(n_parts: int) -> Callable:
     return parts
 
 
-def c4(rule: str = "kruzkov", dtype: str = "float64", nxy: int = 257, nth: int = 128,
+def c4(rule: str = "kruzkov", dtype: str = "float64", schedule: str = "async", nxy: int = 257, nth: int = 128,
        cxy: Optional[int] = None, cth: Optional[int] = None) -> Workload:
     """3D Dubins (x, y, th), f = (cos th, sin th, a), a in {-1,-.5,0,.5,1},
     [-2,2]^2 x [0, 2 pi) at 257x257x128 with periodic th, target disk r=0.2
@@ -117,11 +117,11 @@ def c4(rule: str = "kruzkov", dtype: str = "float64", nxy: int = 257, nth: int =
     pcfg = PatchyConfig(n_patches=16, coarse_nodes=(cxy, cxy, cth), fine_nodes=(nxy, nxy, nth),
                         parts=theta_slabs(16))
     return Workload("c4", f"3D Dubins {nxy}x{nxy}x{nth}, 5 controls, 16 patches", spec, pcfg,
-                    SolverConfig(tol=1e-8 if dtype == "float64" else 1e-6, rule=rule,
+                    SolverConfig(schedule=schedule, tol=1e-8 if dtype == "float64" else 1e-6, rule=rule,
                                  dtype=dtype), (nxy, nxy, nth), (cxy, cxy, cth))
 
 
-def c5(rule: str = "kruzkov", dtype: str = "float32", n: int = 513,
+def c5(rule: str = "kruzkov", dtype: str = "float32", schedule: str = "async", n: int = 513,
        nc_: Optional[int] = None, seed: int = SEED_C5) -> Workload:
     """3D variable speed c = 1 + 0.3 sin(pi x) sin(pi y) sin(pi z), 96
     Fibonacci controls, [-1,1]^3 at 513^3, ball r=0.15 split into 32 seeded
@@ -135,7 +135,7 @@ def c5(rule: str = "kruzkov", dtype: str = "float32", n: int = 513,
                         parts=lambda t, g, serials=None: partition_random_directions(
                             t, g, 32, seed, serials=serials))
     return Workload("c5", f"3D variable speed {n}^3, 96 controls, 32 patches", spec, pcfg,
-                    SolverConfig(tol=1e-8 if dtype == "float64" else 1e-6, rule=rule,
+                    SolverConfig(schedule=schedule, tol=1e-8 if dtype == "float64" else 1e-6, rule=rule,
                                  dtype=dtype), (n,) * 3, (nc_,) * 3)
 
 

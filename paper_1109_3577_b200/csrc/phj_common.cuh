@@ -165,7 +165,12 @@ struct Workspace {
   // serialise on one L2 slice), triple-buffered by sweep so the entries of
   // sweep k+1 can be zeroed during sweep k
   unsigned long long* pmax;  // [3][kMaxColors * kMaxPad]
+  // asynchronous solve: FIFO ring of block ids, capacity blocks + warps
+  // (at most one queued entry per block and one waiting ticket per warp)
+  int* ring;  // [total + kRingExtra]
 };
+
+constexpr int kRingExtra = 1 << 16;  // >= resident warps of any launch
 
 constexpr int kMaxPad = 16;  // u64 per entry = 128 B
 
@@ -179,6 +184,7 @@ inline int64_t workspace_bytes(const phj_grid& g, int max_sweeps) {
   b += 2 * align_up((int64_t)(max_sweeps + 2) * 4, 256);
   b += 2 * align_up((int64_t)tg.total * 8, 256);
   b += 3 * (int64_t)kMaxColors * kMaxPad * 8;
+  b += align_up(((int64_t)tg.total + kRingExtra) * 4, 256);
   return b;
 }
 
@@ -197,6 +203,8 @@ inline Workspace carve(const phj_grid& g, void* base, int max_sweeps) {
   w.cmask[0] = (unsigned long long*)p; p += align_up((int64_t)tg.total * 8, 256);
   w.cmask[1] = (unsigned long long*)p; p += align_up((int64_t)tg.total * 8, 256);
   w.pmax = (unsigned long long*)p;
+  p += 3 * (int64_t)kMaxColors * kMaxPad * 8;
+  w.ring = (int*)p;
   return w;
 }
 

@@ -77,6 +77,8 @@ struct SolveParams {
   unsigned long long* evals;
   int32_t* info;
   int prune;  // exact octant pruning on (PHJ_SOLVE_NO_PRUNE clears it)
+  double act;  // a node change marks the neighbour blocks only if > act (0 = exact)
+  int inner;   // block-local relaxations per sweep (>= 1)
   // AO3 conical reduction (NULL ao3_fb = off)
   const int32_t* ao3_fb;
   const unsigned long long* ao3_mask;
@@ -882,13 +884,14 @@ __device__ __forceinline__ void flush_patch_max(const SolveParams& p, PatchMax& 
 // tile and node inputs.  `hook` (the next block's loads, deferred marks)
 // runs exactly once.  Returns (warp-uniform) whether any node changed.
 template <int D, typename T, int RULE, int COST, typename Hook>
-__device__ __forceinline__ bool sweep_block(const SolveParams& p, const StencilSmem<D, T>& s,
+__device__ __forceinline__ int sweep_block(const SolveParams& p, const StencilSmem<D, T>& s,
                                             int blk, const T* tile, const NodeStage<D, T>* ns,
                                             T* __restrict__ vout, const int* s_done,
                                             unsigned long long* s_max, unsigned long long* gmax_row,
                                             unsigned long long& evals, unsigned long long& exec,
                                             PatchMax& pm, PhaseTimer& tm, const Hook& hook) {
   using B = Blk<D>;
+  using S = TileShape<D>;
   using NS = NodeStage<D, T>;
   constexpr int NB = B::NB;
   constexpr int last = D - 1;
@@ -935,7 +938,7 @@ __device__ __forceinline__ bool sweep_block(const SolveParams& p, const StencilS
     if (!comp[r]) fm[r] = 0;
     any_copy |= copy[r];
   }
-  bool changed = false;
+  bool changed = false, big = false;
   T mych[NB];
 #pragma unroll
   for (int r = 0; r < NB; ++r) mych[r] = T(0);
@@ -946,22 +949,13 @@ __device__ __forceinline__ bool sweep_block(const SolveParams& p, const StencilS
   const bool warp_comp = __any_sync(FULL, any_comp);
   tm.mark(2);
   if (warp_comp) {
-    MinAcc<T> mn[NB];
-    T best[NB];
-    int bidx[NB];
-#pragma unroll
-    for (int r = 0; r < NB; ++r) {
-      mn[r].init();
-      best[r] = big_value<T>();
-      bidx[r] = 0;
-    }
     uint32_t fmo = 0;
 #pragma unroll
     for (int r = 0; r < NB; ++r) fmo |= fm[r];
-    int n_ent;
+    const bool slow = __any_sync(FULL, fmo != 0);
+    // per-node AO3 masks (loaded once per block)
+    Allowed<NB> al;
     if (p.ao3_fb) {
-      // AO3: the node's allowed stencil entries (all for nodes without feedback)
-      Allowed<NB> al;
 #pragma unroll
       for (int r = 0; r < NB; ++r) {
         const int f = comp[r] ? ns->fb[ly * B::BX + lx * NB + r] : -1;
@@ -970,42 +964,95 @@ __device__ __forceinline__ bool sweep_block(const SolveParams& p, const StencilS
           al.w[r][w] = (f >= 0 && w < p.ao3_words) ? __ldg(&p.ao3_mask[f * p.ao3_words + w])
                                                    : ~0ull;
       }
-      n_ent = eval_sweep<D, T, NB, RULE, COST, true, Hook, true>(lt, p.prune != 0, s, os, fm,
-                                                                 ncoef, comp, mn, best, bidx, hook,
-                                                                 &al);
-    } else if (__any_sync(FULL, fmo != 0)) {
-      n_ent = eval_sweep<D, T, NB, RULE, COST, true>(lt, p.prune != 0, s, os, fm, ncoef, comp, mn,
-                                                     best, bidx, hook);
-    } else {
-      n_ent = eval_sweep<D, T, NB, RULE, COST, false>(lt, p.prune != 0, s, os, fm, ncoef, comp, mn,
-                                                      best, bidx, hook);
     }
-    exec += (unsigned long long)n_ent * NB;
+    unsigned long long fcnt_sum = 0;
 #pragma unroll
-    for (int r = 0; r < NB; ++r) best[r] = mn[r].get();
+    for (int r = 0; r < NB; ++r) {
+      if (!comp[r]) continue;
+      int fcnt = nadm;
+      if (p.ao3_fb) {
+        const int f = ns->fb[ly * B::BX + lx * NB + r];
+        if (f >= 0) fcnt = __ldg(&p.ao3_count[f]);
+      }
+      fcnt_sum += (unsigned long long)fcnt;
+    }
+    // old values, then up to p.inner block-local relaxations: the halo ring
+    // stays at the sweep's input, the block's own nodes are relaxed in the
+    // staged tile (deterministic: independent of the schedule)
+    T old[NB], cur[NB];
+#pragma unroll
+    for (int r = 0; r < NB; ++r) {
+      old[r] = (D == 2) ? tile_at<D>(lt, 0, r) : tile_at<D>(lt, 0, 0, r);
+      cur[r] = old[r];
+    }
+    bool hooked = false;
+    auto once = [&]() {
+      if (!hooked) {
+        hooked = true;
+        hook();
+      }
+    };
+    for (int it = 0;;) {
+      MinAcc<T> mn[NB];
+      T best[NB];
+      int bidx[NB];
+#pragma unroll
+      for (int r = 0; r < NB; ++r) {
+        mn[r].init();
+        best[r] = big_value<T>();
+        bidx[r] = 0;
+      }
+      int n_ent;
+      if (p.ao3_fb) {
+        n_ent = eval_sweep<D, T, NB, RULE, COST, true, decltype(once), true>(
+            lt, p.prune != 0, s, os, fm, ncoef, comp, mn, best, bidx, once, &al);
+      } else if (slow) {
+        n_ent = eval_sweep<D, T, NB, RULE, COST, true>(lt, p.prune != 0, s, os, fm, ncoef, comp,
+                                                       mn, best, bidx, once);
+      } else {
+        n_ent = eval_sweep<D, T, NB, RULE, COST, false>(lt, p.prune != 0, s, os, fm, ncoef, comp,
+                                                        mn, best, bidx, once);
+      }
+      exec += (unsigned long long)n_ent * NB;
+      evals += fcnt_sum;
+      bool moved = false;
+#pragma unroll
+      for (int r = 0; r < NB; ++r) {
+        if (!comp[r]) continue;
+        const T b = mn[r].get();
+        T cand = b;
+        if constexpr (COST == PHJ_COST_NODE) {
+          cand = (RULE == PHJ_RULE_KRUZKOV) ? fma(ncoef[r], b, T(1) - ncoef[r]) : b + ncoef[r];
+        }
+        if (cand < cur[r]) {
+          // another block-local relaxation only for changes above the
+          // activity threshold (the same test as the neighbour marking)
+          if constexpr (RULE == PHJ_RULE_KRUZKOV) moved |= cur[r] - cand > T(p.act) * (T(1) - cand);
+          else moved |= cur[r] - cand > T(p.act) * max(T(1), cand);
+          cur[r] = cand;
+        }
+      }
+      if (++it >= p.inner || !__any_sync(FULL, moved)) break;
+      // publish the relaxed values to the lanes whose neighbourhoods hold them
+      T* ltw = const_cast<T*>(lt);
+#pragma unroll
+      for (int r = 0; r < NB; ++r) {
+        if (D == 2) ltw[S::C + 1 + r] = cur[r];
+        else ltw[(S::RB + 1) * S::C + 1 + r] = cur[r];
+      }
+      __syncwarp();
+    }
     tm.mark(3);
 #pragma unroll
     for (int r = 0; r < NB; ++r) {
       if (!(comp[r] || copy[r])) continue;
-      const T old = (D == 2) ? tile_at<D>(lt, 0, r) : tile_at<D>(lt, 0, 0, r);
-      T nv = old;
-      if (comp[r]) {
-        int fcnt = nadm;
-        if (p.ao3_fb) {
-          const int f = ns->fb[ly * B::BX + lx * NB + r];
-          if (f >= 0) fcnt = __ldg(&p.ao3_count[f]);
-        }
-        evals += (unsigned long long)fcnt;
-        T cand = best[r];
-        if constexpr (COST == PHJ_COST_NODE) {
-          cand = (RULE == PHJ_RULE_KRUZKOV) ? fma(ncoef[r], best[r], T(1) - ncoef[r])
-                                            : best[r] + ncoef[r];
-        }
-        if (cand < old) {
-          nv = cand;
-          mych[r] = old - cand;
-          changed = true;
-        }
+      T nv = old[r];
+      if (comp[r] && cur[r] < old[r]) {
+        nv = cur[r];
+        mych[r] = old[r] - cur[r];
+        changed = true;
+        if constexpr (RULE == PHJ_RULE_KRUZKOV) big |= mych[r] > T(p.act) * (T(1) - nv);
+        else big |= mych[r] > T(p.act) * max(T(1), nv);
       }
       vout[f0 + r] = nv;
       if (per0) {
@@ -1061,7 +1108,10 @@ __device__ __forceinline__ bool sweep_block(const SolveParams& p, const StencilS
     }
   }
   tm.mark(5);
-  return wchanged;
+  // 2: a change above the activity threshold (mark the 3^D neighbourhood),
+  // 1: only smaller changes (re-sweep this block once: both ping-pong
+  // buffers must hold its new values), 0: unchanged
+  return wchanged ? (__any_sync(FULL, big) ? 2 : 1) : 0;
 }
 
 // Deferred neighbour marking: a changed block's flag exchanges are issued
@@ -1081,10 +1131,11 @@ struct MarkQueue {
     b_base = 0;
     has_b = false;
   }
-  __device__ __forceinline__ void issue(const TileGrid& tg, const phj_grid& g, int blk, bool ch,
+  __device__ __forceinline__ void issue(const TileGrid& tg, const phj_grid& g, int blk, int ch,
                                         int lane, int* flags) {
     a_nt = -1;
-    if (ch && lane < (D == 2 ? 9 : 27)) {
+    constexpr int self = D == 2 ? 4 : 13;
+    if ((ch == 2 && lane < (D == 2 ? 9 : 27)) || (ch == 1 && lane == self)) {
       const int nt = neighbour_block<D>(tg, g, blk, lane);
       if (nt >= 0) {
         a_nt = nt;
@@ -1247,7 +1298,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __gri
       };
 #endif
       tm.mark(1);
-      const bool ch = sweep_block<D, T, RULE, COST>(p, s, blk, wtile + stage * S::N, wnodes + stage,
+      const int ch = sweep_block<D, T, RULE, COST>(p, s, blk, wtile + stage * S::N, wnodes + stage,
                                                     vout, s_done, s_max, gmax_row, evals, exec, pm,
                                                     tm, hook);
       ++blocks_done;
@@ -1320,6 +1371,210 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __gri
     atomicAdd(&p.evals[0], s_ev);
     atomicAdd(&p.evals[1], s_ex);
     atomicAdd(&p.info[2], s_blk);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Asynchronous (chaotic) relaxation of the same fixed point -- no grid
+// barrier.  One value buffer updated in place; work = a FIFO ring of block
+// ids with one state word per block:
+//   0 idle, 1 queued, 2 being swept, 3 being swept + dirty (a neighbour
+//   changed after the sweep started; the sweeper re-queues the block).
+// A block is therefore never swept by two warps at once, each node is
+// written only by its block's sweeper, and every value stays an upper bound
+// of the fixed point that never rises (the SL map is monotone; any mixture
+// of newer and older neighbour values >= v* maps to a value >= v*).  A node
+// change above the activity threshold re-queues the 3^D block neighbourhood
+// (the block itself included); the solve ends when nothing is queued or
+// being swept (`pending` = 0), i.e. when no node of a swept block can change
+// by more than the threshold -- the fixed point to within the threshold.
+// Ring capacity = number of blocks (a block is queued at most once).
+struct AsyncQ {
+  int* ring;           // [cap] block ids, -1 = empty slot
+  int* state;          // [cap]
+  unsigned int* head;  // tickets taken
+  unsigned int* tail;  // slots reserved beyond the initial n0
+  int* pending;        // queued + in-flight blocks, minus n0
+  int* abort;          // processing budget exhausted
+  unsigned int* swept; // blocks swept (budget)
+};
+
+template <int D>
+__device__ __forceinline__ AsyncQ async_queue(const Workspace& ws) {
+  AsyncQ q;
+  q.ring = ws.ring;
+  q.state = ws.flags[0];
+  q.head = (unsigned int*)&ws.take[0];
+  q.tail = (unsigned int*)&ws.take[1];
+  q.pending = &ws.take[2];
+  q.abort = &ws.take[3];
+  q.swept = (unsigned int*)&ws.take[4];
+  return q;
+}
+
+__device__ __forceinline__ void fence_acq_rel_gpu() {
+  asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+}
+__device__ __forceinline__ int ld_volatile(const int* p) {
+  return *(const volatile int*)p;
+}
+
+template <int D, typename T, int RULE, int COST, bool WCLS>
+__global__ void __launch_bounds__(kThreads, kCtasPerSm)
+    solve_async_kernel(const __grid_constant__ SolveParams p, unsigned int budget) {
+  using S = TileShape<D>;
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr bool warp_cls = WCLS;
+  const int64_t sbytes = solve_stencil_bytes<D, T>(WCLS ? 2 : 1, p.nc);
+  StencilSmem<D, T> s =
+      WCLS ? carve_stencil<D, T>(smem + (threadIdx.x >> 5) * solve_stencil_slot<D, T>(p.nc), 1,
+                                 p.nc)
+           : carve_stencil<D, T>(smem, 1, p.nc);
+  int* s_done = (int*)(smem + sbytes);
+  unsigned long long* s_max = (unsigned long long*)(s_done + ((p.R + 1) / 2 * 2));
+  T* tiles = (T*)(smem + align_up(sbytes + (int64_t)((p.R + 1) / 2 * 2) * 4 +
+                                      (int64_t)min(p.R, kSmemPatchReduce) * 8,
+                                  16));
+  T* wtile = tiles + (threadIdx.x >> 5) * 2 * S::N;
+  NodeStage<D, T>* wnodes =
+      (NodeStage<D, T>*)(tiles + kWarps * 2 * S::N) + (threadIdx.x >> 5) * 2;
+  if (!warp_cls)
+    stage_stencil<D, T, RULE>(s, p.n_classes, p.nc, p.oct_start, p.nzmask, p.weights, p.cost);
+  int wcls = -1;
+  for (int i = threadIdx.x; i < p.R; i += blockDim.x)
+    s_done[i] = (p.mine == nullptr || p.mine[i]) ? 0x7fffffff : 0;
+  for (int i = threadIdx.x; i < min(p.R, kSmemPatchReduce); i += blockDim.x) s_max[i] = 0ull;
+  __syncthreads();
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const AsyncQ q = async_queue<D>(p.ws);
+  const int n0 = ld_cg(&p.ws.counts[0]);
+  const unsigned cap = (unsigned)p.tg.total + (unsigned)(gridDim.x * kWarps);
+  unsigned long long* gmax_row = sweep_max_slots(p.ws, 0);
+  unsigned long long evals = 0, exec = 0;
+  int blocks_done = 0;
+  PatchMax pm{-1, 0.0};
+  PhaseTimer tm;
+  tm.start();
+  constexpr int NNB = D == 2 ? 9 : 27;
+  constexpr int self = D == 2 ? 4 : 13;
+  for (;;) {
+    // -- pop: one ticket per warp, wait for its slot (or for the end) --------
+    int blk = -1;
+    if (ld_volatile(q.abort)) break;
+    if (lane == 0) {
+      const unsigned t = atomicAdd(q.head, 1u);
+      int* slot = &q.ring[t % cap];
+      unsigned ns = 32;
+      for (;;) {
+        const int v = ld_volatile(slot);
+        if (v >= 0) {
+          *(volatile int*)slot = -1;  // the ticket holder is the slot's only reader
+          blk = v;
+          break;
+        }
+        if (n0 + ld_volatile(q.pending) == 0 || ld_volatile(q.abort)) break;
+        __nanosleep(ns);
+        ns = ns < 1024 ? ns * 2 : ns;
+      }
+      if (blk >= 0) atomicExch(&q.state[blk], 2);
+    }
+    blk = __shfl_sync(FULL, blk, 0);
+    if (blk < 0) break;
+    fence_acq_rel_gpu();  // neighbour values are read after the slot / state
+    tm.mark(0);
+    if (warp_cls) {
+      int bc[3];
+      decode_block<D>(p.tg, blk, bc);
+      if (bc[0] != wcls) {
+        __syncwarp();
+        stage_class<D, T, RULE>(s, bc[0], p.nc, lane, p.oct_start, p.nzmask, p.weights, p.cost);
+        wcls = bc[0];
+      }
+    }
+    stage_block<D, T, COST>(p, (const T*)p.v[0], blk, wtile, wnodes, lane);
+    cp_async_wait_all();
+    __syncwarp();
+    tm.mark(1);
+    auto hook = []() {};
+    const int ch = sweep_block<D, T, RULE, COST>(p, s, blk, wtile, wnodes, (T*)p.v[0], s_done,
+                                                 s_max, gmax_row, evals, exec, pm, tm, hook);
+    ++blocks_done;
+    // -- re-queue the neighbourhood of a changed block ------------------------
+    bool want = false;
+    int nt = -1;
+    if (ch == 2) {
+      __threadfence();  // node values before the state words
+      __syncwarp();
+      if (lane < NNB) {
+        nt = neighbour_block<D>(p.tg, p.g, blk, lane);
+        if (nt >= 0) want = atomicOr(&q.state[nt], 1) == 0;
+      }
+    }
+    (void)self;
+    const unsigned bal = __ballot_sync(FULL, want);
+    int base = 0;
+    if (bal != 0u && lane == 0) {
+      atomicAdd(q.pending, __popc(bal));
+      base = (int)atomicAdd(q.tail, (unsigned)__popc(bal));
+    }
+    base = __shfl_sync(FULL, base, 0);
+    if (want) {
+      const unsigned slot = (unsigned)(n0 + base + __popc(bal & ((1u << lane) - 1u))) % cap;
+      atomicExch(&q.ring[slot], nt);
+    }
+    // -- release the block (re-queue it if it went dirty) ---------------------
+    if (lane == 0) {
+      const int old = atomicCAS(&q.state[blk], 2, 0);
+      if (old == 3) {
+        atomicExch(&q.state[blk], 1);
+        const unsigned sl = ((unsigned)n0 + atomicAdd(q.tail, 1u)) % cap;
+        atomicExch(&q.ring[sl], blk);
+      } else {
+        atomicAdd(q.pending, -1);
+      }
+      if (atomicAdd(q.swept, 1u) + 1u >= budget) atomicExch(q.abort, 1);
+    }
+    tm.mark(6);
+  }
+  flush_patch_max(p, pm, s_max, gmax_row);
+#ifdef PHJ_TIMING
+  if (lane == 0)
+    for (int i = 0; i < 12; ++i) atomicAdd(&g_phase_cycles[i], tm.acc[i]);
+#endif
+  __shared__ unsigned long long s_ev, s_ex;
+  __shared__ int s_blk;
+  if (threadIdx.x == 0) {
+    s_ev = 0;
+    s_ex = 0;
+    s_blk = 0;
+  }
+  __syncthreads();
+  atomicAdd(&s_ev, evals);
+  atomicAdd(&s_ex, exec);
+  if (lane == 0) atomicAdd(&s_blk, blocks_done);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicAdd(&p.evals[0], s_ev);
+    atomicAdd(&p.evals[1], s_ex);
+    atomicAdd(&p.info[2], s_blk);
+  }
+}
+
+// Per-patch results of an asynchronous solve: "sweeps" = blocks swept /
+// initial blocks (rounded up; an equivalent sweep count), negated when the
+// budget ran out.
+__global__ void async_finish_kernel(Workspace ws, int R, const uint8_t* mine,
+                                    int32_t* patch_sweeps, int32_t* info) {
+  const int n0 = max(1, ws.counts[0]);
+  const unsigned swept = (unsigned)ws.take[4];
+  const int eq = (int)((swept + (unsigned)n0 - 1u) / (unsigned)n0);
+  const bool aborted = ws.take[3] != 0;
+  for (int i = threadIdx.x; i < R; i += blockDim.x)
+    patch_sweeps[i] = (mine == nullptr || mine[i]) ? (aborted ? -eq : max(eq, 1)) : 0;
+  if (threadIdx.x == 0) {
+    info[0] = max(eq, 1);
+    info[1] = 0;
   }
 }
 
@@ -2329,6 +2584,24 @@ static int coop_launch(K kernel, int want_blocks, size_t smem, void** args, cuda
   return PHJ_OK;
 }
 
+// Persistent non-cooperative launch (no grid barrier): all co-resident CTAs.
+template <typename K>
+static int plain_persistent_launch(K kernel, size_t smem, void** args, cudaStream_t stream) {
+  PHJ_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  PHJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem));
+  if (occ < 1) {
+    phj_set_error("kernel cannot be resident (smem %zu B)", smem);
+    return PHJ_ERR_UNSUPPORTED;
+  }
+  int blocks = std::min(occ * phj_num_sms(), kRingExtra / kWarps);
+  if (const char* cap = getenv("PHJ_MAX_BLOCKS")) blocks = std::min(blocks, atoi(cap));
+  if (blocks < 1) blocks = 1;
+  PHJ_CUDA(cudaLaunchKernel((void*)kernel, dim3(blocks), dim3(kThreads), args, smem, stream));
+  phj_count_launch(1);
+  return PHJ_OK;
+}
+
 template <int D, typename T, int RULE, int COST>
 static int solve_impl(const phj_solve_args* a) {
   cudaStream_t stream = (cudaStream_t)a->stream;
@@ -2358,18 +2631,24 @@ static int solve_impl(const phj_solve_args* a) {
   p.evals = a->evals;
   p.info = a->info;
   p.prune = (a->options & PHJ_SOLVE_NO_PRUNE) ? 0 : 1;
+  p.act = a->act_tol;
+  p.inner = a->inner_sweeps < 1 ? 1 : a->inner_sweeps;
   p.ao3_fb = a->ao3_fb;
   p.ao3_mask = a->ao3_mask;
   p.ao3_count = a->ao3_count;
   p.ao3_words = a->ao3_words;
   const int64_t ws_bytes = workspace_bytes<D>(a->grid, a->max_sweeps);
   PHJ_CUDA(cudaMemsetAsync(a->workspace, 0, ws_bytes, stream));
+  const bool async = (a->options & PHJ_SOLVE_ASYNC) != 0;
+  if (async)
+    PHJ_CUDA(cudaMemsetAsync(p.ws.ring, 0xff, ((size_t)p.tg.total + kRingExtra) * 4, stream));
   PHJ_CUDA(cudaMemsetAsync(a->maxch_hist, 0, sizeof(double) * (size_t)a->max_sweeps * a->n_patches,
                            stream));
   PHJ_CUDA(cudaMemsetAsync(a->evals, 0, 2 * sizeof(unsigned long long), stream));
   PHJ_CUDA(cudaMemsetAsync(a->info, 0, 4 * sizeof(int32_t), stream));
   build_list_kernel<D><<<(p.tg.total + kWarps - 1) / kWarps, kThreads, 0, stream>>>(
-      p.g, p.tg, p.lab, p.mine, p.ws.flags[0], p.ws.list[0], p.ws.counts, 0, nullptr, nullptr,
+      p.g, p.tg, p.lab, p.mine, p.ws.flags[0], async ? p.ws.ring : p.ws.list[0], p.ws.counts, 0,
+      nullptr, nullptr,
       nullptr, 0ull);
   phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
@@ -2378,6 +2657,21 @@ static int solve_impl(const phj_solve_args* a) {
                                      (int64_t)std::min(p.R, kSmemPatchReduce) * 8,
                                  16) +
                 (size_t)solve_tile_bytes<D, T>();
+  if (async) {
+    const long long want = (long long)a->max_sweeps * (long long)p.tg.total;
+    unsigned int budget = (unsigned int)std::min(want, (long long)0x7fffffff);
+    void* aargs[] = {(void*)&p, (void*)&budget};
+    int rc = (D == 3 && p.n_classes > 1)
+                 ? plain_persistent_launch(solve_async_kernel<D, T, RULE, COST, D == 3>, smem,
+                                           aargs, stream)
+                 : plain_persistent_launch(solve_async_kernel<D, T, RULE, COST, false>, smem,
+                                           aargs, stream);
+    if (rc) return rc;
+    async_finish_kernel<<<1, 256, 0, stream>>>(p.ws, p.R, p.mine, p.patch_sweeps, p.info);
+    phj_count_launch(1);
+    PHJ_CUDA(cudaGetLastError());
+    return PHJ_OK;
+  }
   void* args[] = {(void*)&p};
   int launched = 0;
   int rc = (D == 3 && p.n_classes > 1)
@@ -2408,6 +2702,10 @@ extern "C" int phj_solve(const phj_solve_args* a) {
   }
   if (a->n_patches < 1 || a->n_patches > kMaxPatches || a->max_sweeps < 1) {
     phj_set_error("phj_solve: n_patches must be in [1, %d], max_sweeps >= 1", kMaxPatches);
+    return PHJ_ERR_ARG;
+  }
+  if (!(a->act_tol >= 0.0)) {
+    phj_set_error("phj_solve: act_tol must be >= 0");
     return PHJ_ERR_ARG;
   }
   if (a->ao3_fb && (!a->ao3_mask || !a->ao3_count || a->ao3_words < 1 || a->ao3_words > 2 ||

@@ -172,7 +172,9 @@ def solve_full_internal(plan: StencilPlan, cfg: SolverConfig, work: Optional[tor
     work = init_working(plan, cfg.rule, cfg.dtype) if work is None else work
     lab = _full_domain_labels(plan)
     res = device_solve(plan, work, lab, plan.fmask_hard, 1, rule=cfg.rule, dtype=cfg.dtype,
-                       tol=cfg.tol, max_sweeps=cfg.sweep_limit(plan.grid))
+                       tol=cfg.tol, max_sweeps=cfg.sweep_limit(plan.grid),
+                       act_tol=cfg.act_tol, schedule=cfg.schedule,
+                           inner=cfg.inner_for(plan.grid.dim))
     n_free = int((plan.kind == KIND_FREE).sum().item())
     st = stats_for_patch(res, 0, n_free, plan.n_adm, cfg.tol)
     st.node_relaxations = plan.grid.n_interior * st.sweeps
@@ -414,7 +416,9 @@ def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Te
         fmask = plan.fmask_from_labels(lab)
         res = device_solve(plan, work, lab, fmask, n_patches, rule=rule, dtype=dtype, tol=cfg.tol,
                            ao3=ao3,
-                           max_sweeps=cfg.sweep_limit(plan.grid), mine=mine)
+                           max_sweeps=cfg.sweep_limit(plan.grid), mine=mine,
+                           act_tol=cfg.act_tol, schedule=cfg.schedule,
+                           inner=cfg.inner_for(plan.grid.dim))
         out = res.values
         performed = res.evals
         executed = res.executed
@@ -453,7 +457,9 @@ def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Te
             li.copy_(torch.where(own, torch.zeros_like(li), li))
             _sync_periodic(plan, labj)
             res = device_solve(plan, w, labj, plan.fmask_hard, 1, rule=rule, dtype=dtype, ao3=ao3,
-                               tol=cfg.tol, max_sweeps=cfg.sweep_limit(plan.grid))
+                               tol=cfg.tol, max_sweeps=cfg.sweep_limit(plan.grid),
+                               act_tol=cfg.act_tol, schedule=cfg.schedule,
+                           inner=cfg.inner_for(plan.grid.dim))
             oi = plan.interior_int(out)
             oi.copy_(torch.where(own, plan.interior_int(res.values), oi))
             performed += res.evals

@@ -392,3 +392,85 @@ def test_c1_patch_solves_dirichlet_and_warm_start(key, kw):
     ov, _ = O.solve_patches(C.c1_fine(), c["color"], 4, rule="reference", mode="jacobi",
                             tol=1e-8, lifted=_flat(c["lifted"]), **kw)
     assert _live_close(got, ov, 1e-8) <= 1e-8
+
+
+# -- asynchronous schedule (chaotic relaxation + block-local relaxations) ------------
+# Same fixed point as the Jacobi sweeps, reached to within activity_tol; the
+# oracle runs to a tight tol so both sides sit at the fixed point.
+
+ASYNC = dict(schedule="async")
+
+
+def test_async_c1_reference_rule_matches_golden():
+    c = golden("c1_fine.npz")
+    spec = _eik_spec((-2.0, -2.0), (2.0, 2.0), C.circle(32), 0.1)
+    g = phj.Grid(spec.box_lo, spec.box_hi, (101, 101))
+    u, st = phj.solve_single(spec, g, phj.SolverConfig(tol=1e-8, **ASYNC))
+    assert st.converged
+    got = _flat(u.numpy())
+    assert _live_close(got, _flat(c["u_jacobi"]), 1e-8) <= 1e-8
+    assert _live_close(got, _flat(c["u_gs"]), 1e-8) <= 1e-8
+
+
+@pytest.mark.parametrize("inner", [1, 2, 8])
+def test_async_c1_kruzkov_matches_tight_oracle(inner):
+    spec = _eik_spec((-2.0, -2.0), (2.0, 2.0), C.circle(32), 0.1)
+    g = phj.Grid(spec.box_lo, spec.box_hi, (101, 101))
+    u, st = phj.solve_single(spec, g, phj.SolverConfig(tol=1e-8, rule="kruzkov",
+                                                       inner_sweeps=inner, **ASYNC))
+    assert st.converged
+    pr = C.c1_fine()
+    v = O.init_field(pr, "kruzkov")
+    O.solve(v, pr, rule="kruzkov", mode="jacobi", tol=1e-14)
+    assert np.abs(_to_v(_flat(u.numpy())) - v).max() <= 1e-10
+
+
+def test_async_fib3d_both_rules_and_fp32():
+    spec = _eik_spec((-1.0,) * 3, (1.0,) * 3, C.fib_sphere(48), 0.25)
+    g = phj.Grid(spec.box_lo, spec.box_hi, (21, 21, 21))
+    f = golden("fib3d_21.npz")
+    u, st = phj.solve_single(spec, g, phj.SolverConfig(tol=1e-8, **ASYNC))
+    assert st.converged
+    assert _live_close(_flat(u.numpy()), _flat(f["u_gs"]), 1e-8) <= 1e-8
+    pr = C.fib3d()
+    v = O.init_field(pr, "kruzkov")
+    O.solve(v, pr, rule="kruzkov", mode="jacobi", tol=1e-14)
+    for dtype, bar in (("float64", 1e-10), ("float32", 1e-4)):
+        u, st = phj.solve_single(spec, g, phj.SolverConfig(tol=1e-8, rule="kruzkov",
+                                                           dtype=dtype, **ASYNC))
+        assert np.abs(_to_v(_flat(u.numpy())) - v).max() <= bar, dtype
+
+
+def test_async_zermelo_per_control_cost_matches_oracle():
+    spec = phj.preset("zermelo2d", controls=16)
+    g = phj.Grid(spec.box_lo, spec.box_hi, (41, 41))
+    pr = C.zermelo(41, 16)
+    u, _ = phj.solve_single(spec, g, phj.SolverConfig(tol=1e-8, **ASYNC))
+    uo = O.init_field(pr, "reference")
+    O.solve(uo, pr, rule="reference", mode="jacobi", tol=1e-14)
+    assert _live_close(_flat(u.numpy()), uo, 1e-8) <= 1e-8
+    uk, _ = phj.solve_single(spec, g, phj.SolverConfig(tol=1e-8, rule="kruzkov", **ASYNC))
+    vo = O.init_field(pr, "kruzkov")
+    O.solve(vo, pr, rule="kruzkov", mode="jacobi", tol=1e-14)
+    assert np.abs(_to_v(_flat(uk.numpy())) - vo).max() <= 1e-10
+
+
+def test_async_dubins_periodic_matches_tight_oracle():
+    w = configs.c4(nxy=33, nth=16, cxy=9, cth=8)
+    g = w.spec.make_grid(w.pcfg.fine_nodes)
+    u, st = phj.solve_single(w.spec, g, phj.SolverConfig(tol=1e-8, rule="kruzkov", **ASYNC))
+    og = O.OGrid(g.lo, g.hi, g.shape, g.periodic)
+    X = og.interior_points()
+    pr = O.OProblem(og, "dubins", w.spec.control_set.controls,
+                    np.linalg.norm(X[:, :2], axis=1) <= 0.2)
+    v = O.init_field(pr, "kruzkov")
+    O.solve(v, pr, rule="kruzkov", mode="jacobi", tol=1e-14)
+    inner = og.interior_flat()
+    assert np.abs(_to_v(_flat(u.numpy()))[inner] - v[inner]).max() <= 1e-10
+
+
+def test_async_budget_exhaustion_sets_warning():
+    spec = _eik_spec((-2.0, -2.0), (2.0, 2.0), C.circle(32), 0.1)
+    g = phj.Grid(spec.box_lo, spec.box_hi, (101, 101))
+    u, st = phj.solve_single(spec, g, phj.SolverConfig(tol=1e-8, max_sweeps=3, **ASYNC))
+    assert not st.converged and st.warning
