@@ -201,8 +201,16 @@ typedef struct phj_transport_args {
   int32_t* color_sweeps; /* out [n_colors]: sweeps to converge, -(cap) if not */
   int32_t* info;        /* out [4]: total sweeps, result buffer, -, - */
   unsigned long long* updates; /* out [1]: mover updates performed */
+  int32_t options;      /* PHJ_TRANSPORT_* bits */
+  int32_t inner_sweeps; /* async: relaxations of a colour per block visit (>= 1) */
   void* stream;
 } phj_transport_args;
+
+/* phj_transport_args.options: asynchronous in-place transport (block FIFO, no
+ * grid barrier; phi1 unused, result in phi0): every colour converges until
+ * no node changes by more than act_eps; color_sweeps = equivalent sweeps
+ * */
+#define PHJ_TRANSPORT_ASYNC 1
 
 /* argmax over the colours of a [n_colors][ext] colour field (strict >,
  * lowest colour on ties, patchy.py:251-256) */

@@ -62,13 +62,14 @@ class SolveArgs(ctypes.Structure):
 
 SOLVE_NO_PRUNE = 1  # PHJ_SOLVE_NO_PRUNE
 SOLVE_ASYNC = 2  # PHJ_SOLVE_ASYNC
+TRANSPORT_ASYNC = 1  # PHJ_TRANSPORT_ASYNC
 
 
 class TransportArgs(ctypes.Structure):
     _fields_ = [("grid", Grid), ("st", Stencil), ("phi0", P), ("phi1", P), ("fb", P),
                 ("kind", P), ("ent_scratch", P), ("n_colors", I32), ("tol", D), ("act_eps", D),
                 ("max_sweeps", I32), ("workspace", P), ("maxch_hist", P), ("color_sweeps", P),
-                ("info", P), ("updates", P), ("stream", P)]
+                ("info", P), ("updates", P), ("options", I32), ("inner_sweeps", I32), ("stream", P)]
 
 
 class Shapes(ctypes.Structure):

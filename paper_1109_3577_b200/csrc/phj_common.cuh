@@ -162,17 +162,21 @@ struct Workspace {
   // per-sweep max change per patch / colour, one 128-byte line per entry
   // (all CTAs reduce into these with atomics right before the grid barrier
   // and read them right after it: packed into one line, those requests
-  // serialise on one L2 slice), triple-buffered by sweep so the entries of
-  // sweep k+1 can be zeroed during sweep k
-  unsigned long long* pmax;  // [3][kMaxColors * kMaxPad]
+  // serialise on one L2 slice), six buffers by sweep: the two-sweep
+  // transport zeroes sweeps 2m+2, 2m+3 during pass m while it accumulates
+  // 2m, 2m+1 and slow CTAs may still read 2m-2, 2m-1 after the previous
+  // barrier (with three buffers the zeroing hit entries still being read and
+  // CTAs could take different stop decisions -- a rare grid-barrier hang)
+  unsigned long long* pmax;  // [kMaxBufs][kMaxColors * kMaxPad]
   // asynchronous solve: FIFO ring of block ids, capacity blocks + warps
   // (at most one queued entry per block and one waiting ticket per warp)
-  int* ring;  // [total + kRingExtra]
+  unsigned long long* ring;  // [total + kRingExtra] sequence-numbered cells
 };
 
 constexpr int kRingExtra = 1 << 16;  // >= resident warps of any launch
 
 constexpr int kMaxPad = 16;  // u64 per entry = 128 B
+constexpr int kMaxBufs = 6;  // per-sweep max-change buffers (see Workspace::pmax)
 
 __host__ __device__ inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
@@ -183,8 +187,8 @@ inline int64_t workspace_bytes(const phj_grid& g, int max_sweeps) {
   b += 4 * align_up((int64_t)tg.total * 4, 256);
   b += 2 * align_up((int64_t)(max_sweeps + 2) * 4, 256);
   b += 2 * align_up((int64_t)tg.total * 8, 256);
-  b += 3 * (int64_t)kMaxColors * kMaxPad * 8;
-  b += align_up(((int64_t)tg.total + kRingExtra) * 4, 256);
+  b += kMaxBufs * (int64_t)kMaxColors * kMaxPad * 8;
+  b += align_up(((int64_t)tg.total + kRingExtra) * 8, 256);
   return b;
 }
 
@@ -203,14 +207,14 @@ inline Workspace carve(const phj_grid& g, void* base, int max_sweeps) {
   w.cmask[0] = (unsigned long long*)p; p += align_up((int64_t)tg.total * 8, 256);
   w.cmask[1] = (unsigned long long*)p; p += align_up((int64_t)tg.total * 8, 256);
   w.pmax = (unsigned long long*)p;
-  p += 3 * (int64_t)kMaxColors * kMaxPad * 8;
-  w.ring = (int*)p;
+  p += kMaxBufs * (int64_t)kMaxColors * kMaxPad * 8;
+  w.ring = (unsigned long long*)p;
   return w;
 }
 
 // the padded max-change entries of sweep sw
 __device__ __forceinline__ unsigned long long* sweep_max_slots(const Workspace& w, int sw) {
-  return w.pmax + (int64_t)(sw % 3) * kMaxColors * kMaxPad;
+  return w.pmax + (int64_t)(sw % kMaxBufs) * kMaxColors * kMaxPad;
 }
 
 __device__ inline unsigned long long dbits(double x) {

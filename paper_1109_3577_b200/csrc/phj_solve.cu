@@ -1388,15 +1388,20 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __gri
 // (the block itself included); the solve ends when nothing is queued or
 // being swept (`pending` = 0), i.e. when no node of a swept block can change
 // by more than the threshold -- the fixed point to within the threshold.
-// Ring capacity = number of blocks (a block is queued at most once).
+// The FIFO is a bounded ring of 64-bit cells with per-cell sequence numbers
+// (high word) so a slow ticket holder can never miss or lose an entry when
+// the ring laps: a push at position p waits for seq == p and stores p + 1, a
+// pop with ticket t waits for seq == t + 1 and stores t + cap.  Capacity =
+// blocks + launched warps (at most one queued entry per block, one waiting
+// ticket per warp), so pushes practically never wait.
 struct AsyncQ {
-  int* ring;           // [cap] block ids, -1 = empty slot
-  int* state;          // [cap]
-  unsigned int* head;  // tickets taken
-  unsigned int* tail;  // slots reserved beyond the initial n0
-  int* pending;        // queued + in-flight blocks, minus n0
-  int* abort;          // processing budget exhausted
-  unsigned int* swept; // blocks swept (budget)
+  unsigned long long* ring;  // [cap] (seq << 32) | block id
+  int* state;                // [blocks]
+  unsigned int* head;        // tickets taken
+  unsigned int* tail;        // push positions reserved beyond the initial n0
+  int* pending;              // queued + in-flight blocks, minus n0
+  int* abort;                // processing budget exhausted
+  unsigned int* swept;       // blocks swept (budget)
 };
 
 template <int D>
@@ -1410,6 +1415,96 @@ __device__ __forceinline__ AsyncQ async_queue(const Workspace& ws) {
   q.abort = &ws.take[3];
   q.swept = (unsigned int*)&ws.take[4];
   return q;
+}
+
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+  return *(const volatile unsigned long long*)p;
+}
+
+// lane-0 pop: the next block id, or -1 once nothing is queued or in flight
+// (or the budget ran out)
+__device__ __forceinline__ int async_pop(const AsyncQ& q, unsigned cap, int n0) {
+  const unsigned t = atomicAdd(q.head, 1u);
+  unsigned long long* cell = &q.ring[t % cap];
+  unsigned ns = 32;
+#ifdef PHJ_ASYNC_DEBUG
+  unsigned spins = 0;
+#endif
+  for (;;) {
+    const unsigned long long c = ld_volatile_u64(cell);
+    if ((unsigned)(c >> 32) == t + 1u) {
+      *(volatile unsigned long long*)cell = ((unsigned long long)(t + cap) << 32) | 0xffffffffull;
+      return (int)(unsigned)(c & 0xffffffffull);
+    }
+    if (n0 + *(const volatile int*)q.pending == 0 || *(const volatile int*)q.abort) return -1;
+    __nanosleep(ns);
+    ns = ns < 1024 ? ns * 2 : ns;
+#ifdef PHJ_ASYNC_DEBUG
+    if (++spins == (1u << 22)) {
+      printf("async_pop stuck: t=%u cell_seq=%u cell_val=%d head=%u tail=%u pending=%d n0=%d cap=%u\n",
+             t, (unsigned)(c >> 32), (int)(unsigned)(c & 0xffffffffull), *(volatile unsigned*)q.head,
+             *(volatile unsigned*)q.tail, *(volatile int*)q.pending, n0, cap);
+      atomicExch(q.abort, 1);
+    }
+#endif
+  }
+}
+
+// push of block `blk` at absolute position `pos`
+__device__ __forceinline__ void async_push(const AsyncQ& q, unsigned cap, unsigned pos, int blk) {
+  unsigned long long* cell = &q.ring[pos % cap];
+  // (the previous lap's ticket holder may have left on an abort)
+#ifdef PHJ_ASYNC_DEBUG
+  unsigned spins = 0;
+#endif
+  while ((unsigned)(ld_volatile_u64(cell) >> 32) != pos) {
+    if (*(const volatile int*)q.abort) return;
+    __nanosleep(64);
+#ifdef PHJ_ASYNC_DEBUG
+    if (++spins == (1u << 24)) {
+      printf("async_push stuck: pos=%u cell_seq=%u blk=%d\n", pos,
+             (unsigned)(ld_volatile_u64(cell) >> 32), blk);
+      atomicExch(q.abort, 1);
+    }
+#endif
+  }
+  atomicExch(cell, ((unsigned long long)(pos + 1u) << 32) | (unsigned)blk);
+}
+
+// Re-queue the neighbourhood of a changed block (`want` lanes hold block
+// ids whose state went 0 -> 1), then release the block itself: back to idle,
+// or re-queued when a neighbour dirtied it during the visit.
+__device__ __forceinline__ void async_requeue_release(const AsyncQ& q, unsigned cap, int n0,
+                                                      int blk, bool want, int nt, int lane,
+                                                      unsigned budget) {
+  const unsigned FULL = 0xffffffffu;
+  const unsigned bal = __ballot_sync(FULL, want);
+  unsigned base = 0;
+  if (bal != 0u && lane == 0) {
+    atomicAdd(q.pending, __popc(bal));
+    base = atomicAdd(q.tail, (unsigned)__popc(bal));
+  }
+  base = __shfl_sync(FULL, base, 0);
+  if (want) async_push(q, cap, (unsigned)n0 + base + __popc(bal & ((1u << lane) - 1u)), nt);
+  if (lane == 0) {
+    const int old = atomicCAS(&q.state[blk], 2, 0);
+    if (old == 3) {
+      atomicExch(&q.state[blk], 1);
+      async_push(q, cap, (unsigned)n0 + atomicAdd(q.tail, 1u), blk);
+    } else {
+      atomicAdd(q.pending, -1);
+    }
+    if (atomicAdd(q.swept, 1u) + 1u >= budget) atomicExch(q.abort, 1);
+  }
+}
+
+// initial ring: positions < n0 hold the build_list blocks, the rest are free
+__global__ void async_ring_init(unsigned long long* ring, unsigned cap, const int* list,
+                                const int* count) {
+  const unsigned n0 = (unsigned)*count;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += gridDim.x * blockDim.x)
+    ring[i] = i < n0 ? (((unsigned long long)(i + 1u) << 32) | (unsigned)list[i])
+                     : (((unsigned long long)i << 32) | 0xffffffffull);
 }
 
 __device__ __forceinline__ void fence_acq_rel_gpu() {
@@ -1461,22 +1556,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   for (;;) {
     // -- pop: one ticket per warp, wait for its slot (or for the end) --------
     int blk = -1;
-    if (ld_volatile(q.abort)) break;
+    // warp-uniform: lanes still finishing their pushes read the flag later
+    if (__shfl_sync(FULL, lane == 0 ? ld_volatile(q.abort) : 0, 0)) break;
     if (lane == 0) {
-      const unsigned t = atomicAdd(q.head, 1u);
-      int* slot = &q.ring[t % cap];
-      unsigned ns = 32;
-      for (;;) {
-        const int v = ld_volatile(slot);
-        if (v >= 0) {
-          *(volatile int*)slot = -1;  // the ticket holder is the slot's only reader
-          blk = v;
-          break;
-        }
-        if (n0 + ld_volatile(q.pending) == 0 || ld_volatile(q.abort)) break;
-        __nanosleep(ns);
-        ns = ns < 1024 ? ns * 2 : ns;
-      }
+      blk = async_pop(q, cap, n0);
       if (blk >= 0) atomicExch(&q.state[blk], 2);
     }
     blk = __shfl_sync(FULL, blk, 0);
@@ -1511,30 +1594,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         if (nt >= 0) want = atomicOr(&q.state[nt], 1) == 0;
       }
     }
-    (void)self;
-    const unsigned bal = __ballot_sync(FULL, want);
-    int base = 0;
-    if (bal != 0u && lane == 0) {
-      atomicAdd(q.pending, __popc(bal));
-      base = (int)atomicAdd(q.tail, (unsigned)__popc(bal));
-    }
-    base = __shfl_sync(FULL, base, 0);
-    if (want) {
-      const unsigned slot = (unsigned)(n0 + base + __popc(bal & ((1u << lane) - 1u))) % cap;
-      atomicExch(&q.ring[slot], nt);
-    }
-    // -- release the block (re-queue it if it went dirty) ---------------------
-    if (lane == 0) {
-      const int old = atomicCAS(&q.state[blk], 2, 0);
-      if (old == 3) {
-        atomicExch(&q.state[blk], 1);
-        const unsigned sl = ((unsigned)n0 + atomicAdd(q.tail, 1u)) % cap;
-        atomicExch(&q.ring[sl], blk);
-      } else {
-        atomicAdd(q.pending, -1);
-      }
-      if (atomicAdd(q.swept, 1u) + 1u >= budget) atomicExch(q.abort, 1);
-    }
+    async_requeue_release(q, cap, n0, blk, want, nt, lane, budget);
     tm.mark(6);
   }
   flush_patch_max(p, pm, s_max, gmax_row);
@@ -1912,6 +1972,170 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
       p.info[0] = sw;
       p.info[1] = buf;
     }
+  }
+  __shared__ unsigned long long s_up;
+  if (threadIdx.x == 0) s_up = 0;
+  __syncthreads();
+  atomicAdd(&s_up, upd);
+  __syncthreads();
+  if (threadIdx.x == 0) atomicAdd(p.updates, s_up);
+}
+
+// ---------------------------------------------------------------------------
+// Asynchronous colour transport (PHJ_TRANSPORT_ASYNC): the same block FIFO
+// and state machine as solve_async_kernel, one phi buffer updated in place,
+// per-block pending-colour masks (OR-ed by the neighbours that changed those
+// colours).  phi only grows (from the 0/1 start, every read mixture is <= the
+// fixed point and >= the values the previous update of the node read; the
+// FMA chain of non-negative weights is monotone), so the iteration converges
+// to the fixed point; a colour change above act_eps re-queues the 3^D block
+// neighbourhood for that colour, and each visit relaxes a colour up to
+// `inner` times over the block (own values re-read through L2).
+template <int D>
+__global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS)
+    transport_async_kernel(const __grid_constant__ TransportParams p, int inner,
+                           unsigned int budget) {
+  using B = Blk<D>;
+  constexpr int NC = 1 << D;
+  constexpr int NB = B::NB;
+  constexpr int last = D - 1;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int nent = p.n_classes * p.nc;
+  const int R = p.R;
+  const int wpitch = nent | 1;
+  double* s_w = (double*)smem;                                         // [NC][wpitch]
+  signed char* s_oct = (signed char*)(s_w + (int64_t)wpitch * NC);     // [nent]
+  for (int i = threadIdx.x; i < nent * NC; i += blockDim.x)
+    s_w[(i % NC) * wpitch + i / NC] = p.weights[i];
+  for (int cls = 0; cls < p.n_classes; ++cls) {
+    const int32_t* os = p.oct_start + cls * (NC + 1);
+    for (int e = os[0] + threadIdx.x; e < os[NC]; e += blockDim.x) {
+      int oc = 0;
+      while (oc < NC - 1 && e >= os[oc + 1]) ++oc;
+      s_oct[e] = (signed char)oc;
+    }
+  }
+  __syncthreads();
+  const unsigned FULL = 0xffffffffu;
+  const phj_grid& g = p.g;
+  const int lane = threadIdx.x & 31;
+  const int64_t M0 = g.shape[0];
+  const bool per0 = g.periodic[0] != 0;
+  const int64_t ghost_shift = M0 * g.strides[0];
+  int64_t coff[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    int64_t o = 0;
+#pragma unroll
+    for (int ax = 0; ax < D; ++ax)
+      if ((k >> ax) & 1) o += g.strides[ax];
+    coff[k] = o;
+  }
+  const AsyncQ q = async_queue<D>(p.ws);
+  unsigned long long* cmask = p.ws.cmask[0];
+  const int n0 = ld_cg(&p.ws.counts[0]);
+  const unsigned cap = (unsigned)p.tg.total + (unsigned)(gridDim.x * kWarps);
+  double* phi = p.phi[0];
+  unsigned long long upd = 0;
+  constexpr int NNB = D == 2 ? 9 : 27;
+  for (;;) {
+    int blk = -1;
+    unsigned long long cm = 0ull;
+    // warp-uniform: lanes still finishing their pushes read the flag later
+    if (__shfl_sync(FULL, lane == 0 ? ld_volatile(q.abort) : 0, 0)) break;
+    if (lane == 0) {
+      blk = async_pop(q, cap, n0);
+      if (blk >= 0) {
+        atomicExch(&q.state[blk], 2);
+        cm = atomicExch(&cmask[blk], 0ull);
+      }
+    }
+    blk = __shfl_sync(FULL, blk, 0);
+    if (blk < 0) break;
+    cm = __shfl_sync(FULL, cm, 0);
+    fence_acq_rel_gpu();
+    int c[3];
+    const bool row_ok = lane_nodes<D>(g, p.tg, blk, lane, c);
+    const int64_t f0 = ext_flat<D>(g, c);
+    const int64_t s0 = serial_of<D>(g, c);
+    int e[NB];
+    int64_t base[NB];
+    int kself[NB];
+#pragma unroll
+    for (int r = 0; r < NB; ++r) {
+      const bool in = row_ok && c[last] + r < g.shape[last];
+      e[r] = in ? __ldg(&p.ent[s0 + r]) : -1;
+      base[r] = f0 + r;
+      kself[r] = 0;
+      if (e[r] >= 0) {
+        const int oc = s_oct[e[r]];
+#pragma unroll
+        for (int ax = 0; ax < D; ++ax)
+          if (!((oc >> ax) & 1)) base[r] -= g.strides[ax];
+        kself[r] = (~oc) & (NC - 1);
+      }
+    }
+    unsigned long long changed = 0ull;
+    const bool masked = R <= 64;
+    unsigned long long todo = masked ? cm : 0ull;
+    int jnext = 0;
+    for (;;) {
+      int j;
+      if (masked) {
+        if (!todo) break;
+        j = __ffsll((long long)todo) - 1;
+        todo &= todo - 1;
+      } else {
+        if (cm == 0ull || jnext >= R) break;
+        j = jnext++;
+      }
+      double* pj = phi + (int64_t)j * p.plane;
+      for (int it = 0; it < inner; ++it) {
+        double cv[NB][NC];
+#pragma unroll
+        for (int r = 0; r < NB; ++r)
+#pragma unroll
+          for (int k = 0; k < NC; ++k) cv[r][k] = e[r] >= 0 ? __ldcg(pj + base[r] + coff[k]) : 0.0;
+        bool big = false;
+#pragma unroll
+        for (int r = 0; r < NB; ++r) {
+          if (e[r] < 0) continue;
+          double acc = 0.0, old = cv[r][0];
+#pragma unroll
+          for (int k = 0; k < NC; ++k) {
+            acc = fma(s_w[k * wpitch + e[r]], cv[r][k], acc);
+            if (k > 0 && k == kself[r]) old = cv[r][k];
+          }
+          ++upd;
+          if (acc > old) {
+            big |= acc - old > p.act_eps;
+            pj[f0 + r] = acc;
+            if (per0) {
+              if (c[0] == 0) pj[f0 + r + ghost_shift] = acc;
+              else if (c[0] == M0 - 1) pj[f0 + r - ghost_shift] = acc;
+            }
+          }
+        }
+        if (!__any_sync(FULL, big)) break;
+        changed |= (j < 64) ? (1ull << j) : ~0ull;
+        __syncwarp();  // own-block values of this relaxation before the next
+      }
+    }
+    // re-queue the neighbourhood for the changed colours
+    bool want = false;
+    int nt = -1;
+    if (changed) {
+      __threadfence();
+      __syncwarp();
+      if (lane < NNB) {
+        nt = neighbour_block<D>(p.tg, g, blk, lane);
+        if (nt >= 0) {
+          atomicOr(&cmask[nt], changed);
+          want = atomicOr(&q.state[nt], 1) == 0;
+        }
+      }
+    }
+    async_requeue_release(q, cap, n0, blk, want, nt, lane, budget);
   }
   __shared__ unsigned long long s_up;
   if (threadIdx.x == 0) s_up = 0;
@@ -2584,9 +2808,10 @@ static int coop_launch(K kernel, int want_blocks, size_t smem, void** args, cuda
   return PHJ_OK;
 }
 
-// Persistent non-cooperative launch (no grid barrier): all co-resident CTAs.
+// Persistent non-cooperative launch (no grid barrier): all co-resident CTAs
+// (at most kRingExtra warps: the async ring holds one waiting ticket per warp).
 template <typename K>
-static int plain_persistent_launch(K kernel, size_t smem, void** args, cudaStream_t stream) {
+static int persistent_blocks(K kernel, size_t smem, int* blocks) {
   PHJ_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
   PHJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem));
@@ -2594,9 +2819,22 @@ static int plain_persistent_launch(K kernel, size_t smem, void** args, cudaStrea
     phj_set_error("kernel cannot be resident (smem %zu B)", smem);
     return PHJ_ERR_UNSUPPORTED;
   }
-  int blocks = std::min(occ * phj_num_sms(), kRingExtra / kWarps);
-  if (const char* cap = getenv("PHJ_MAX_BLOCKS")) blocks = std::min(blocks, atoi(cap));
-  if (blocks < 1) blocks = 1;
+  int b = std::min(occ * phj_num_sms(), kRingExtra / kWarps);
+  if (const char* cap = getenv("PHJ_MAX_BLOCKS")) b = std::min(b, atoi(cap));
+  *blocks = b < 1 ? 1 : b;
+  return PHJ_OK;
+}
+
+// ring cells for an asynchronous launch of `blocks` CTAs, then the launch
+template <typename K>
+static int async_launch(K kernel, size_t smem, void** args, const Workspace& ws, int total,
+                        cudaStream_t stream) {
+  int blocks = 0;
+  if (int rc = persistent_blocks(kernel, smem, &blocks)) return rc;
+  const unsigned cap = (unsigned)total + (unsigned)(blocks * kWarps);
+  async_ring_init<<<std::min(1024, (int)((cap + 255) / 256)), 256, 0, stream>>>(
+      ws.ring, cap, ws.list[0], ws.counts);
+  phj_count_launch(1);
   PHJ_CUDA(cudaLaunchKernel((void*)kernel, dim3(blocks), dim3(kThreads), args, smem, stream));
   phj_count_launch(1);
   return PHJ_OK;
@@ -2640,14 +2878,12 @@ static int solve_impl(const phj_solve_args* a) {
   const int64_t ws_bytes = workspace_bytes<D>(a->grid, a->max_sweeps);
   PHJ_CUDA(cudaMemsetAsync(a->workspace, 0, ws_bytes, stream));
   const bool async = (a->options & PHJ_SOLVE_ASYNC) != 0;
-  if (async)
-    PHJ_CUDA(cudaMemsetAsync(p.ws.ring, 0xff, ((size_t)p.tg.total + kRingExtra) * 4, stream));
   PHJ_CUDA(cudaMemsetAsync(a->maxch_hist, 0, sizeof(double) * (size_t)a->max_sweeps * a->n_patches,
                            stream));
   PHJ_CUDA(cudaMemsetAsync(a->evals, 0, 2 * sizeof(unsigned long long), stream));
   PHJ_CUDA(cudaMemsetAsync(a->info, 0, 4 * sizeof(int32_t), stream));
   build_list_kernel<D><<<(p.tg.total + kWarps - 1) / kWarps, kThreads, 0, stream>>>(
-      p.g, p.tg, p.lab, p.mine, p.ws.flags[0], async ? p.ws.ring : p.ws.list[0], p.ws.counts, 0,
+      p.g, p.tg, p.lab, p.mine, p.ws.flags[0], p.ws.list[0], p.ws.counts, 0,
       nullptr, nullptr,
       nullptr, 0ull);
   phj_count_launch(1);
@@ -2662,10 +2898,10 @@ static int solve_impl(const phj_solve_args* a) {
     unsigned int budget = (unsigned int)std::min(want, (long long)0x7fffffff);
     void* aargs[] = {(void*)&p, (void*)&budget};
     int rc = (D == 3 && p.n_classes > 1)
-                 ? plain_persistent_launch(solve_async_kernel<D, T, RULE, COST, D == 3>, smem,
-                                           aargs, stream)
-                 : plain_persistent_launch(solve_async_kernel<D, T, RULE, COST, false>, smem,
-                                           aargs, stream);
+                 ? async_launch(solve_async_kernel<D, T, RULE, COST, D == 3>, smem, aargs, p.ws,
+                                p.tg.total, stream)
+                 : async_launch(solve_async_kernel<D, T, RULE, COST, false>, smem, aargs, p.ws,
+                                p.tg.total, stream);
     if (rc) return rc;
     async_finish_kernel<<<1, 256, 0, stream>>>(p.ws, p.R, p.mine, p.patch_sweeps, p.info);
     phj_count_launch(1);
@@ -2784,6 +3020,7 @@ static int transport_impl(const phj_transport_args* a) {
   PHJ_CUDA(cudaMemsetAsync(a->maxch_hist, 0, 8 * (size_t)a->max_sweeps * p.R, stream));
   PHJ_CUDA(cudaMemsetAsync(a->info, 0, 4 * sizeof(int32_t), stream));
   PHJ_CUDA(cudaMemsetAsync(a->updates, 0, sizeof(unsigned long long), stream));
+  const bool async = (a->options & PHJ_TRANSPORT_ASYNC) != 0;
   {
     const int64_t N = p.g.shape[0] * p.g.shape[1] * (D == 3 ? p.g.shape[2] : 1);
     const int nb = (int)std::min<int64_t>((N + 255) / 256, 16 * phj_num_sms());
@@ -2795,11 +3032,25 @@ static int transport_impl(const phj_transport_args* a) {
     phj_count_launch(1);
   }
   build_list_kernel<D><<<(p.tg.total + kWarps - 1) / kWarps, kThreads, 0, stream>>>(
-      p.g, p.tg, nullptr, nullptr, p.ws.flags[0], p.ws.list[0], p.ws.counts, 1, p.fb, p.kind,
+      p.g, p.tg, nullptr, nullptr, p.ws.flags[0], p.ws.list[0], p.ws.counts,
+      1, p.fb, p.kind,
       p.ws.cmask[0], p.R >= 64 ? ~0ull : ((1ull << p.R) - 1ull));
   phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   const int nent = p.n_classes * p.nc;
+  if (async) {
+    int inner = a->inner_sweeps < 1 ? 1 : a->inner_sweeps;
+    const long long want = (long long)a->max_sweeps * (long long)p.tg.total;
+    unsigned int budget = (unsigned int)std::min(want, (long long)0x7fffffff);
+    void* aargs[] = {(void*)&p, (void*)&inner, (void*)&budget};
+    const size_t smem = (size_t)(nent | 1) * (1 << D) * 8 + (size_t)nent + 16;
+    int rc = async_launch(transport_async_kernel<D>, smem, aargs, p.ws, p.tg.total, stream);
+    if (rc) return rc;
+    async_finish_kernel<<<1, 256, 0, stream>>>(p.ws, p.R, nullptr, p.color_sweeps, p.info);
+    phj_count_launch(1);
+    PHJ_CUDA(cudaGetLastError());
+    return PHJ_OK;
+  }
   void* args[] = {(void*)&p};
   // two sweeps per barrier pay in 2D only (3D: the 2-ring halo is 5 planes
   // deep and the activity must reach +-2 planes -- measured 2x slower)
