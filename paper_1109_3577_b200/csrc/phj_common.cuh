@@ -173,7 +173,7 @@ struct Workspace {
   unsigned long long* ring;  // [total + kRingExtra] sequence-numbered cells
 };
 
-constexpr int kRingExtra = 1 << 16;  // >= resident warps of any launch
+constexpr int kRingExtra = 1 << 16;  // >= resident warps of any async launch
 
 constexpr int kMaxPad = 16;  // u64 per entry = 128 B
 constexpr int kMaxBufs = 6;  // per-sweep max-change buffers (see Workspace::pmax)

@@ -1393,15 +1393,20 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __gri
 // the ring laps: a push at position p waits for seq == p and stores p + 1, a
 // pop with ticket t waits for seq == t + 1 and stores t + cap.  Capacity =
 // blocks + launched warps (at most one queued entry per block, one waiting
-// ticket per warp), so pushes practically never wait.
+// ticket per warp).  Tickets are claimed only by idle warps (claiming one
+// ahead while busy lets a push wait on a ticket whose busy holder is itself
+// waiting in a push -- a cycle, observed); a push at position P can then only
+// wait on the reader of P - cap, who waits on the push of P - cap: a strictly
+// descending chain, so pushes always complete.
 struct AsyncQ {
   unsigned long long* ring;  // [cap] (seq << 32) | block id
   int* state;                // [blocks]
   unsigned int* head;        // tickets taken
-  unsigned int* tail;        // push positions reserved beyond the initial n0
-  int* pending;              // queued + in-flight blocks, minus n0
+  // low word: push positions reserved beyond the initial n0; high word:
+  // queued + in-flight blocks minus n0 (one atomic updates both)
+  unsigned long long* tp;
   int* abort;                // processing budget exhausted
-  unsigned int* swept;       // blocks swept (budget)
+  unsigned int* swept;       // blocks swept (budget; flushed per warp in batches)
 };
 
 template <int D>
@@ -1410,10 +1415,9 @@ __device__ __forceinline__ AsyncQ async_queue(const Workspace& ws) {
   q.ring = ws.ring;
   q.state = ws.flags[0];
   q.head = (unsigned int*)&ws.take[0];
-  q.tail = (unsigned int*)&ws.take[1];
-  q.pending = &ws.take[2];
   q.abort = &ws.take[3];
   q.swept = (unsigned int*)&ws.take[4];
+  q.tp = (unsigned long long*)&ws.take[6];
   return q;
 }
 
@@ -1421,82 +1425,81 @@ __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned lon
   return *(const volatile unsigned long long*)p;
 }
 
-// lane-0 pop: the next block id, or -1 once nothing is queued or in flight
-// (or the budget ran out)
-__device__ __forceinline__ int async_pop(const AsyncQ& q, unsigned cap, int n0) {
+__device__ __forceinline__ int async_pending(const AsyncQ& q) {
+  return (int)(unsigned)(ld_volatile_u64(q.tp) >> 32);
+}
+
+// lane-0 pop with ticket t: the next block id, or -1 once nothing is queued
+// or in flight (or the budget ran out)
+__device__ __forceinline__ int async_pop(const AsyncQ& q, unsigned cap, int n0, unsigned budget) {
   const unsigned t = atomicAdd(q.head, 1u);
   unsigned long long* cell = &q.ring[t % cap];
   unsigned ns = 32;
-#ifdef PHJ_ASYNC_DEBUG
-  unsigned spins = 0;
-#endif
   for (;;) {
     const unsigned long long c = ld_volatile_u64(cell);
     if ((unsigned)(c >> 32) == t + 1u) {
       *(volatile unsigned long long*)cell = ((unsigned long long)(t + cap) << 32) | 0xffffffffull;
       return (int)(unsigned)(c & 0xffffffffull);
     }
-    if (n0 + *(const volatile int*)q.pending == 0 || *(const volatile int*)q.abort) return -1;
+    if (n0 + async_pending(q) == 0 || *(const volatile int*)q.abort) return -1;
+    if (*(const volatile unsigned*)q.swept >= budget) {  // idle warps watch the budget
+      atomicExch(q.abort, 1);
+      return -1;
+    }
     __nanosleep(ns);
     ns = ns < 1024 ? ns * 2 : ns;
-#ifdef PHJ_ASYNC_DEBUG
-    if (++spins == (1u << 22)) {
-      printf("async_pop stuck: t=%u cell_seq=%u cell_val=%d head=%u tail=%u pending=%d n0=%d cap=%u\n",
-             t, (unsigned)(c >> 32), (int)(unsigned)(c & 0xffffffffull), *(volatile unsigned*)q.head,
-             *(volatile unsigned*)q.tail, *(volatile int*)q.pending, n0, cap);
-      atomicExch(q.abort, 1);
-    }
-#endif
   }
 }
 
-// push of block `blk` at absolute position `pos`
+// push of block `blk` at absolute position `pos` (the cell is free unless a
+// previous-lap ticket holder left on an abort)
 __device__ __forceinline__ void async_push(const AsyncQ& q, unsigned cap, unsigned pos, int blk) {
   unsigned long long* cell = &q.ring[pos % cap];
-  // (the previous lap's ticket holder may have left on an abort)
-#ifdef PHJ_ASYNC_DEBUG
-  unsigned spins = 0;
-#endif
   while ((unsigned)(ld_volatile_u64(cell) >> 32) != pos) {
     if (*(const volatile int*)q.abort) return;
     __nanosleep(64);
-#ifdef PHJ_ASYNC_DEBUG
-    if (++spins == (1u << 24)) {
-      printf("async_push stuck: pos=%u cell_seq=%u blk=%d\n", pos,
-             (unsigned)(ld_volatile_u64(cell) >> 32), blk);
-      atomicExch(q.abort, 1);
-    }
-#endif
   }
   atomicExch(cell, ((unsigned long long)(pos + 1u) << 32) | (unsigned)blk);
 }
 
-// Re-queue the neighbourhood of a changed block (`want` lanes hold block
-// ids whose state went 0 -> 1), then release the block itself: back to idle,
-// or re-queued when a neighbour dirtied it during the visit.
+// Release the visited block (back to idle, or re-queued when a neighbour
+// dirtied it during the visit) and queue the neighbours whose state went
+// 0 -> 1 (`want` lanes), with ONE atomic on the packed (pending, positions)
+// word: pending += pushes - (released ? 1 : 0), so it cannot reach 0 while
+// work remains.  The caller has fenced its value writes before marking.
 __device__ __forceinline__ void async_requeue_release(const AsyncQ& q, unsigned cap, int n0,
                                                       int blk, bool want, int nt, int lane,
-                                                      unsigned budget) {
+                                                      unsigned budget, unsigned& swept_local) {
   const unsigned FULL = 0xffffffffu;
-  const unsigned bal = __ballot_sync(FULL, want);
-  unsigned base = 0;
-  if (bal != 0u && lane == 0) {
-    atomicAdd(q.pending, __popc(bal));
-    base = atomicAdd(q.tail, (unsigned)__popc(bal));
-  }
-  base = __shfl_sync(FULL, base, 0);
-  if (want) async_push(q, cap, (unsigned)n0 + base + __popc(bal & ((1u << lane) - 1u)), nt);
+  int dirty = 0;
   if (lane == 0) {
     const int old = atomicCAS(&q.state[blk], 2, 0);
     if (old == 3) {
       atomicExch(&q.state[blk], 1);
-      async_push(q, cap, (unsigned)n0 + atomicAdd(q.tail, 1u), blk);
-    } else {
-      atomicAdd(q.pending, -1);
+      dirty = 1;
     }
-    if (atomicAdd(q.swept, 1u) + 1u >= budget) atomicExch(q.abort, 1);
   }
+  const unsigned bal = __ballot_sync(FULL, want);
+  unsigned base = 0;
+  if (lane == 0) {
+    const int npush = __popc(bal);
+    const int dpend = npush - (dirty ? 0 : 1);
+    const unsigned npos = (unsigned)(npush + dirty);
+    const unsigned long long add =
+        ((unsigned long long)(unsigned)dpend << 32) + (unsigned long long)npos;
+    base = (unsigned)atomicAdd(q.tp, add);
+    if (dirty) async_push(q, cap, (unsigned)n0 + base + (unsigned)npush, blk);
+    atomicAdd(q.swept, 1u);  // result unused: a fire-and-forget reduction
+    if (++swept_local == 32u) {
+      if (*(const volatile unsigned*)q.swept >= budget) atomicExch(q.abort, 1);
+      swept_local = 0u;
+    }
+  }
+  base = __shfl_sync(FULL, base, 0);
+  if (want) async_push(q, cap, (unsigned)n0 + base + __popc(bal & ((1u << lane) - 1u)), nt);
 }
+
+
 
 // initial ring: positions < n0 hold the build_list blocks, the rest are free
 __global__ void async_ring_init(unsigned long long* ring, unsigned cap, const int* list,
@@ -1545,6 +1548,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   const AsyncQ q = async_queue<D>(p.ws);
   const int n0 = ld_cg(&p.ws.counts[0]);
   const unsigned cap = (unsigned)p.tg.total + (unsigned)(gridDim.x * kWarps);
+  unsigned swept_local = 0;
   unsigned long long* gmax_row = sweep_max_slots(p.ws, 0);
   unsigned long long evals = 0, exec = 0;
   int blocks_done = 0;
@@ -1559,8 +1563,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     // warp-uniform: lanes still finishing their pushes read the flag later
     if (__shfl_sync(FULL, lane == 0 ? ld_volatile(q.abort) : 0, 0)) break;
     if (lane == 0) {
-      blk = async_pop(q, cap, n0);
-      if (blk >= 0) atomicExch(&q.state[blk], 2);
+      blk = async_pop(q, cap, n0, budget);
+      if (blk >= 0) {
+        atomicExch(&q.state[blk], 2);
+      }
     }
     blk = __shfl_sync(FULL, blk, 0);
     if (blk < 0) break;
@@ -1586,15 +1592,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     // -- re-queue the neighbourhood of a changed block ------------------------
     bool want = false;
     int nt = -1;
+    if (ch != 0) __threadfence();  // node values before the state words (release too)
+    __syncwarp();
     if (ch == 2) {
-      __threadfence();  // node values before the state words
-      __syncwarp();
       if (lane < NNB) {
         nt = neighbour_block<D>(p.tg, p.g, blk, lane);
         if (nt >= 0) want = atomicOr(&q.state[nt], 1) == 0;
       }
     }
-    async_requeue_release(q, cap, n0, blk, want, nt, lane, budget);
+    async_requeue_release(q, cap, n0, blk, want, nt, lane, budget, swept_local);
     tm.mark(6);
   }
   flush_patch_max(p, pm, s_max, gmax_row);
@@ -1989,22 +1995,36 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
 // fixed point and >= the values the previous update of the node read; the
 // FMA chain of non-negative weights is monotone), so the iteration converges
 // to the fixed point; a colour change above act_eps re-queues the 3^D block
-// neighbourhood for that colour, and each visit relaxes a colour up to
-// `inner` times over the block (own values re-read through L2).
+// neighbourhood for that colour.
+// A visit stages the halo tiles of up to kTC pending colours at once (all
+// their L2 loads in flight together), relaxes the block's movers up to
+// `inner` times in shared memory (halo fixed, own values updated in place),
+// and writes back the changed own values.
+template <int D>
+struct TTile {
+  static constexpr int TC = D == 2 ? 8 : 4;  // colours staged per chunk
+  static constexpr int N = TileShape<D>::N;
+};
+
 template <int D>
 __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS)
     transport_async_kernel(const __grid_constant__ TransportParams p, int inner,
                            unsigned int budget) {
   using B = Blk<D>;
+  using S = TileShape<D>;
   constexpr int NC = 1 << D;
   constexpr int NB = B::NB;
   constexpr int last = D - 1;
+  constexpr int TC = TTile<D>::TC;
+  constexpr int W = B::BX + 2;  // tile columns used
+  constexpr int NT = S::R * W;  // tile elements used
   extern __shared__ __align__(16) unsigned char smem[];
   const int nent = p.n_classes * p.nc;
   const int R = p.R;
   const int wpitch = nent | 1;
-  double* s_w = (double*)smem;                                         // [NC][wpitch]
-  signed char* s_oct = (signed char*)(s_w + (int64_t)wpitch * NC);     // [nent]
+  double* s_w = (double*)smem;                                           // [NC][wpitch]
+  double* s_tiles = s_w + (int64_t)wpitch * NC;                          // [warps][TC][N]
+  signed char* s_oct = (signed char*)(s_tiles + (int64_t)kWarps * TC * S::N);  // [nent]
   for (int i = threadIdx.x; i < nent * NC; i += blockDim.x)
     s_w[(i % NC) * wpitch + i / NC] = p.weights[i];
   for (int cls = 0; cls < p.n_classes; ++cls) {
@@ -2019,32 +2039,52 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS)
   const unsigned FULL = 0xffffffffu;
   const phj_grid& g = p.g;
   const int lane = threadIdx.x & 31;
+  double* wt = s_tiles + (int64_t)(threadIdx.x >> 5) * TC * S::N;
   const int64_t M0 = g.shape[0];
   const bool per0 = g.periodic[0] != 0;
   const int64_t ghost_shift = M0 * g.strides[0];
-  int64_t coff[NC];
+  // tile strides per internal axis and corner offsets (bit ax = +1 on axis ax)
+  int tstr[3];
+  if constexpr (D == 2) {
+    tstr[0] = S::C;
+    tstr[1] = 1;
+    tstr[2] = 0;
+  } else {
+    tstr[0] = S::RB * S::C;
+    tstr[1] = S::C;
+    tstr[2] = 1;
+  }
+  int tcoff[NC];
 #pragma unroll
   for (int k = 0; k < NC; ++k) {
-    int64_t o = 0;
+    int o = 0;
 #pragma unroll
     for (int ax = 0; ax < D; ++ax)
-      if ((k >> ax) & 1) o += g.strides[ax];
-    coff[k] = o;
+      if ((k >> ax) & 1) o += tstr[ax];
+    tcoff[k] = o;
   }
+  const int nlast = (int)0;
+  (void)nlast;
   const AsyncQ q = async_queue<D>(p.ws);
   unsigned long long* cmask = p.ws.cmask[0];
   const int n0 = ld_cg(&p.ws.counts[0]);
   const unsigned cap = (unsigned)p.tg.total + (unsigned)(gridDim.x * kWarps);
+  unsigned swept_local = 0;
   double* phi = p.phi[0];
   unsigned long long upd = 0;
   constexpr int NNB = D == 2 ? 9 : 27;
+  const int ly = lane / B::LX, lx = lane % B::LX;
+  // this lane's node r sits at tile index tnode + r
+  const int tnode = D == 2 ? (ly + 1) * S::C + lx * NB + 1
+                           : (S::RB + ly + 1) * S::C + lx * NB + 1;
+  PhaseTimer tm;
+  tm.start();
   for (;;) {
     int blk = -1;
     unsigned long long cm = 0ull;
-    // warp-uniform: lanes still finishing their pushes read the flag later
     if (__shfl_sync(FULL, lane == 0 ? ld_volatile(q.abort) : 0, 0)) break;
     if (lane == 0) {
-      blk = async_pop(q, cap, n0);
+      blk = async_pop(q, cap, n0, budget);
       if (blk >= 0) {
         atomicExch(&q.state[blk], 2);
         cm = atomicExch(&cmask[blk], 0ull);
@@ -2054,79 +2094,158 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS)
     if (blk < 0) break;
     cm = __shfl_sync(FULL, cm, 0);
     fence_acq_rel_gpu();
+    tm.mark(0);
     int c[3];
     const bool row_ok = lane_nodes<D>(g, p.tg, blk, lane, c);
     const int64_t f0 = ext_flat<D>(g, c);
     const int64_t s0 = serial_of<D>(g, c);
-    int e[NB];
-    int64_t base[NB];
-    int kself[NB];
+    int e[NB], tb[NB];
+    bool anym = false;
 #pragma unroll
     for (int r = 0; r < NB; ++r) {
       const bool in = row_ok && c[last] + r < g.shape[last];
       e[r] = in ? __ldg(&p.ent[s0 + r]) : -1;
-      base[r] = f0 + r;
-      kself[r] = 0;
+      tb[r] = tnode + r;
       if (e[r] >= 0) {
+        anym = true;
         const int oc = s_oct[e[r]];
 #pragma unroll
         for (int ax = 0; ax < D; ++ax)
-          if (!((oc >> ax) & 1)) base[r] -= g.strides[ax];
-        kself[r] = (~oc) & (NC - 1);
+          if (!((oc >> ax) & 1)) tb[r] -= tstr[ax];
       }
     }
+    // tile origin (ext coordinates of the block's lower halo corner) and the
+    // clamps for partial blocks at the far grid edge
+    int b[3];
+    decode_block<D>(p.tg, blk, b);
+    int64_t o, rs, s0x;
+    int row0, col0, rmax, cmax;
+    if constexpr (D == 2) {
+      row0 = b[0] * B::BY;
+      col0 = b[1] * B::BX;
+      rs = g.strides[0];
+      s0x = 0;
+      o = (int64_t)row0 * rs + col0;
+      rmax = (int)g.ext[0] - 1;
+      cmax = (int)g.ext[1] - 1;
+    } else {
+      row0 = b[1] * B::BY;
+      col0 = b[2] * B::BX;
+      rs = g.strides[1];
+      s0x = g.strides[0];
+      o = (int64_t)b[0] * s0x + (int64_t)row0 * rs + col0;
+      rmax = (int)g.ext[1] - 1;
+      cmax = (int)g.ext[2] - 1;
+    }
     unsigned long long changed = 0ull;
+    bool anywrote = false;
+    const bool work = __any_sync(FULL, anym) && cm != 0ull;
     const bool masked = R <= 64;
-    unsigned long long todo = masked ? cm : 0ull;
+    unsigned long long todo = work ? (masked ? cm : ~0ull) : 0ull;
     int jnext = 0;
-    for (;;) {
-      int j;
-      if (masked) {
-        if (!todo) break;
-        j = __ffsll((long long)todo) - 1;
-        todo &= todo - 1;
-      } else {
-        if (cm == 0ull || jnext >= R) break;
-        j = jnext++;
+    while (todo) {
+      // next chunk of pending colours
+      int js[TC];
+      int nj = 0;
+#pragma unroll
+      for (int t = 0; t < TC; ++t) {
+        int j = -1;
+        if (masked) {
+          if (todo) {
+            j = __ffsll((long long)todo) - 1;
+            todo &= todo - 1;
+          }
+        } else if (jnext < R) {
+          j = jnext++;
+          if (jnext >= R) todo = 0ull;
+        }
+        js[t] = j;
+        nj += j >= 0;
       }
-      double* pj = phi + (int64_t)j * p.plane;
+      if (!masked && jnext >= R) todo = 0ull;
+      // stage: every halo value of every chunk colour, loads issued together
+#pragma unroll
+      for (int t = 0; t < TC; ++t) {
+        if (js[t] < 0) continue;
+        const double* pj = phi + (int64_t)js[t] * p.plane;
+        double* tt = wt + t * S::N;
+#pragma unroll
+        for (int i0 = 0; i0 < NT; i0 += 32) {
+          const int i = i0 + lane;
+          if (i < NT) {
+            const int rr = i / W, cc = i - rr * W;
+            int pl = 0, ry = rr;
+            if constexpr (D == 3) {
+              pl = rr / S::RB;
+              ry = rr - pl * S::RB;
+            }
+            const int yy = min(row0 + ry, rmax) - row0, xx = min(col0 + cc, cmax) - col0;
+            tt[rr * S::C + cc] = __ldcg(pj + o + pl * s0x + (int64_t)yy * rs + xx);
+          }
+        }
+      }
+      __syncwarp();
+      tm.mark(1);
+      unsigned long long wrote = 0ull;
       for (int it = 0; it < inner; ++it) {
-        double cv[NB][NC];
+        unsigned long long bigm = 0ull;
 #pragma unroll
-        for (int r = 0; r < NB; ++r)
+        for (int t = 0; t < TC; ++t) {
+          if (js[t] < 0) continue;
+          double* tt = wt + t * S::N;
+          bool big = false, any = false;
 #pragma unroll
-          for (int k = 0; k < NC; ++k) cv[r][k] = e[r] >= 0 ? __ldcg(pj + base[r] + coff[k]) : 0.0;
-        bool big = false;
+          for (int r = 0; r < NB; ++r) {
+            if (e[r] < 0) continue;
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < NC; ++k) acc = fma(s_w[k * wpitch + e[r]], tt[tb[r] + tcoff[k]], acc);
+            const double old = tt[tnode + r];
+            ++upd;
+            if (acc > old) {
+              big |= acc - old > p.act_eps;
+              any = true;
+              tt[tnode + r] = acc;
+            }
+          }
+          if (__any_sync(FULL, any)) wrote |= 1ull << t;
+          if (__any_sync(FULL, big)) bigm |= 1ull << t;
+        }
+        if (bigm == 0ull) break;
+#pragma unroll
+        for (int t = 0; t < TC; ++t)
+          if ((bigm >> t) & 1ull) changed |= (js[t] < 64) ? (1ull << js[t]) : ~0ull;
+        __syncwarp();
+      }
+      tm.mark(3);
+      // write back the block's changed colours
+      anywrote |= wrote != 0ull;
+#pragma unroll
+      for (int t = 0; t < TC; ++t) {
+        if (!((wrote >> t) & 1ull)) continue;
+        double* pj = phi + (int64_t)js[t] * p.plane;
+        const double* tt = wt + t * S::N;
 #pragma unroll
         for (int r = 0; r < NB; ++r) {
           if (e[r] < 0) continue;
-          double acc = 0.0, old = cv[r][0];
-#pragma unroll
-          for (int k = 0; k < NC; ++k) {
-            acc = fma(s_w[k * wpitch + e[r]], cv[r][k], acc);
-            if (k > 0 && k == kself[r]) old = cv[r][k];
-          }
-          ++upd;
-          if (acc > old) {
-            big |= acc - old > p.act_eps;
-            pj[f0 + r] = acc;
-            if (per0) {
-              if (c[0] == 0) pj[f0 + r + ghost_shift] = acc;
-              else if (c[0] == M0 - 1) pj[f0 + r - ghost_shift] = acc;
-            }
+          const double v = tt[tnode + r];
+          pj[f0 + r] = v;
+          if (per0) {
+            if (c[0] == 0) pj[f0 + r + ghost_shift] = v;
+            else if (c[0] == M0 - 1) pj[f0 + r - ghost_shift] = v;
           }
         }
-        if (!__any_sync(FULL, big)) break;
-        changed |= (j < 64) ? (1ull << j) : ~0ull;
-        __syncwarp();  // own-block values of this relaxation before the next
       }
+      __syncwarp();  // the tiles are restaged by the next chunk
+      (void)nj;
+      tm.mark(4);
     }
     // re-queue the neighbourhood for the changed colours
     bool want = false;
     int nt = -1;
+    if (anywrote) __threadfence();  // phi values before the state words (release too)
+    __syncwarp();
     if (changed) {
-      __threadfence();
-      __syncwarp();
       if (lane < NNB) {
         nt = neighbour_block<D>(p.tg, g, blk, lane);
         if (nt >= 0) {
@@ -2135,8 +2254,13 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS)
         }
       }
     }
-    async_requeue_release(q, cap, n0, blk, want, nt, lane, budget);
+    async_requeue_release(q, cap, n0, blk, want, nt, lane, budget, swept_local);
+    tm.mark(6);
   }
+#ifdef PHJ_TIMING
+  if (lane == 0)
+    for (int i = 0; i < 12; ++i) atomicAdd(&g_phase_cycles[i], tm.acc[i]);
+#endif
   __shared__ unsigned long long s_up;
   if (threadIdx.x == 0) s_up = 0;
   __syncthreads();
@@ -3043,7 +3167,8 @@ static int transport_impl(const phj_transport_args* a) {
     const long long want = (long long)a->max_sweeps * (long long)p.tg.total;
     unsigned int budget = (unsigned int)std::min(want, (long long)0x7fffffff);
     void* aargs[] = {(void*)&p, (void*)&inner, (void*)&budget};
-    const size_t smem = (size_t)(nent | 1) * (1 << D) * 8 + (size_t)nent + 16;
+    const size_t smem = (size_t)(nent | 1) * (1 << D) * 8 +
+                        (size_t)kWarps * TTile<D>::TC * TileShape<D>::N * 8 + (size_t)nent + 16;
     int rc = async_launch(transport_async_kernel<D>, smem, aargs, p.ws, p.tg.total, stream);
     if (rc) return rc;
     async_finish_kernel<<<1, 256, 0, stream>>>(p.ws, p.R, nullptr, p.color_sweeps, p.info);

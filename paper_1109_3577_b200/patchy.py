@@ -49,6 +49,7 @@ TRANSPORT_ACT_FRAC = 1.0e-3
 #: asynchronous transport: a colour change re-queues the neighbourhood only
 #: above this fraction of color_tol; relaxations per block visit by dimension
 TRANSPORT_ASYNC_FRAC = float(os.environ.get("PHJ_TASYNC_FRAC", "1e-3"))
+TRANSPORT_ASYNC_3D = os.environ.get("PHJ_TRANSPORT_ASYNC3D", "0") == "1"
 TRANSPORT_INNER = {2: int(os.environ.get("PHJ_TASYNC_INNER2", "8")),
                    3: int(os.environ.get("PHJ_TASYNC_INNER3", "2"))}
 
@@ -275,7 +276,7 @@ def _transport_and_argmax(fplan: StencilPlan, fb: torch.Tensor, parts, color_tol
         # the asynchronous transport pays in 2D (C2 15.0 -> 6.9 ms); in 3D the
         # one-plane blocks relax little per visit and it is slower (C3 48 ->
         # 58 ms), so 3D keeps the Jacobi transport
-        tsched = schedule if fplan.grid.dim == 2 else "jacobi"
+        tsched = schedule if (fplan.grid.dim == 2 or TRANSPORT_ASYNC_3D) else "jacobi"
         phi, _, csw, upd = transport_internal(fplan, fb, parts_flat, color_tol, limit,
                                               tsched)
         best_val, best_idx = argmax_batched(fplan.gs, phi, len(mine), n, dev)
