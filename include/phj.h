@@ -177,6 +177,17 @@ int phj_feedback(const phj_grid* g, const phj_stencil* st, int32_t dtype, int32_
                  const void* v, const int8_t* kind, const uint32_t* fmask, const void* coef,
                  double coef0, double unreach, int32_t* out, unsigned long long* evals,
                  void* stream);
+/* phj_feedback restricted per node (solver.extract_feedback(allowed=...),
+ * _kernels.py:71-75): allow_row per ext node (-1 = all controls) indexes
+ * allow_mask [rows][allow_words] (bit e = stencil entry e allowed) and
+ * allow_count [rows] (allowed admissible controls, the evaluation count).
+ * Single-class stencils, <= 128 entries (allow_words 1..2). */
+int phj_feedback_allowed(const phj_grid* g, const phj_stencil* st, int32_t dtype, int32_t rule,
+                         const void* v, const int8_t* kind, const uint32_t* fmask,
+                         const void* coef, double coef0, double unreach,
+                         const int32_t* allow_row, const unsigned long long* allow_mask,
+                         const int32_t* allow_count, int32_t allow_words, int32_t* out,
+                         unsigned long long* evals, void* stream);
 
 /* Colour transport of all target parts at once, each to its own
  * max|change| <= tol (Jacobi, whole loop on device, one launch).  phi0/phi1

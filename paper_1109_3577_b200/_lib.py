@@ -87,7 +87,7 @@ class SpeedModel(ctypes.Structure):
 EXPORTS = (
     "phj_solve_workspace_bytes", "phj_unroll", "phj_blocks_total", "phj_solve", "phj_fmask_from_labels",
     "phj_fmask_from_hard",
-    "phj_feedback", "phj_transport", "phj_lift", "phj_argmax_update", "phj_argmax_colors",
+    "phj_feedback", "phj_feedback_allowed", "phj_transport", "phj_lift", "phj_argmax_update", "phj_argmax_colors",
     "phj_assemble_codes",
     "phj_assemble_repair", "phj_assemble_finish", "phj_classify", "phj_node_coef",
     "phj_init_field", "phj_to_kruzkov", "phj_from_kruzkov", "phj_sync_periodic",
@@ -120,6 +120,8 @@ def load() -> ctypes.CDLL:
         "phj_fmask_from_labels": (ctypes.c_int, [P, P, P, P]),
         "phj_fmask_from_hard": (ctypes.c_int, [P, P, P, P]),
         "phj_feedback": (ctypes.c_int, [P, P, I32, I32, P, P, P, P, D, D, P, P, P]),
+        "phj_feedback_allowed": (ctypes.c_int, [P, P, I32, I32, P, P, P, P, D, D, P, P, P, I32,
+                                                P, P, P]),
         "phj_transport": (ctypes.c_int, [P]),
         "phj_lift": (ctypes.c_int, [P, P, I32, P, P, D, D, I32, P]),
         "phj_argmax_update": (ctypes.c_int, [P, P, I32, P, P, P]),

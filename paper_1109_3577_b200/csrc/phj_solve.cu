@@ -468,28 +468,29 @@ struct NoHook {
 
 // All octants in order; `hook` runs once, right after octant 0 (the solve
 // sweep issues the next block's loads there so they overlap the rest).
-template <int D, typename T, int NB, int RULE, int COST, bool SLOW, int MODE, int O = 0>
+template <int D, typename T, int NB, int RULE, int COST, bool SLOW, int MODE, bool AO3 = false,
+          int O = 0>
 struct EvalAll {
   template <typename Hook>
   __device__ __forceinline__ static void run(const Nbhd<D, T, NB>& nb, const StencilSmem<D, T>& s,
                                              const int* os, const uint32_t (&fm)[NB],
                                              const T (&ncoef)[NB], const int32_t* ctrl_map,
                                              MinAcc<T> (&mn)[NB], T (&best)[NB], int (&bidx)[NB],
-                                             const Hook& hook) {
-    eval_octant<D, T, NB, RULE, COST, SLOW, MODE>(NbhdOct<D, T, NB, O>{nb}, O, s, os, fm, ncoef,
-                                                  ctrl_map, mn, best, bidx);
+                                             const Hook& hook, const Allowed<NB>* al = nullptr) {
+    eval_octant<D, T, NB, RULE, COST, SLOW, MODE, NbhdOct<D, T, NB, O>, AO3>(
+        NbhdOct<D, T, NB, O>{nb}, O, s, os, fm, ncoef, ctrl_map, mn, best, bidx, al);
     if constexpr (O == 0) hook();
-    EvalAll<D, T, NB, RULE, COST, SLOW, MODE, O + 1>::run(nb, s, os, fm, ncoef, ctrl_map, mn, best,
-                                                         bidx, hook);
+    EvalAll<D, T, NB, RULE, COST, SLOW, MODE, AO3, O + 1>::run(nb, s, os, fm, ncoef, ctrl_map, mn,
+                                                              best, bidx, hook, al);
   }
 };
-template <int D, typename T, int NB, int RULE, int COST, bool SLOW, int MODE>
-struct EvalAll<D, T, NB, RULE, COST, SLOW, MODE, (1 << D)> {
+template <int D, typename T, int NB, int RULE, int COST, bool SLOW, int MODE, bool AO3>
+struct EvalAll<D, T, NB, RULE, COST, SLOW, MODE, AO3, (1 << D)> {
   template <typename Hook>
   __device__ __forceinline__ static void run(const Nbhd<D, T, NB>&, const StencilSmem<D, T>&,
                                              const int*, const uint32_t (&)[NB], const T (&)[NB],
                                              const int32_t*, MinAcc<T> (&)[NB], T (&)[NB],
-                                             int (&)[NB], const Hook&) {}
+                                             int (&)[NB], const Hook&, const Allowed<NB>* = nullptr) {}
 };
 
 // ---- octant pruning (MODE 0, per-node cost) --------------------------------
@@ -2762,6 +2763,13 @@ struct FeedbackParams {
   double unreach;
   int32_t* out;
   unsigned long long* evals;
+  // allowed controls (solver.extract_feedback(allowed=...)): per ext node a
+  // row of allow_mask ([rows][allow_words] bitmask over stencil entries) and
+  // allow_count (admissible allowed controls); NULL allow_row = all allowed
+  const int32_t* allow_row;
+  const unsigned long long* allow_mask;
+  const int32_t* allow_count;
+  int allow_words;
 };
 
 template <int D, typename T, int RULE, int COST>
@@ -2819,12 +2827,31 @@ __global__ void __launch_bounds__(kThreads) feedback_kernel(const __grid_constan
       best[r] = big_value<T>();
       bidx[r] = 0x7fffffff;
     }
-    EvalAll<D, T, NB, RULE, COST, true, 1>::run(nb, s, os, fm, ncoef, s_ctrl, mn, best, bidx,
-                                                 NoHook());
+    int cnt[NB];
+#pragma unroll
+    for (int r = 0; r < NB; ++r) cnt[r] = nadm;
+    if (p.allow_row) {
+      Allowed<NB> al;
+#pragma unroll
+      for (int r = 0; r < NB; ++r) {
+        const int row = comp[r] ? __ldg(&p.allow_row[f0 + r]) : -1;
+#pragma unroll
+        for (int w = 0; w < 2; ++w)
+          al.w[r][w] = (row >= 0 && w < p.allow_words)
+                           ? __ldg(&p.allow_mask[(int64_t)row * p.allow_words + w])
+                           : ~0ull;
+        if (row >= 0) cnt[r] = __ldg(&p.allow_count[row]);
+      }
+      EvalAll<D, T, NB, RULE, COST, true, 1, true>::run(nb, s, os, fm, ncoef, s_ctrl, mn, best,
+                                                        bidx, NoHook(), &al);
+    } else {
+      EvalAll<D, T, NB, RULE, COST, true, 1>::run(nb, s, os, fm, ncoef, s_ctrl, mn, best, bidx,
+                                                   NoHook());
+    }
 #pragma unroll
     for (int r = 0; r < NB; ++r) {
       if (!comp[r]) continue;
-      ev += nadm;
+      ev += cnt[r];
       p.out[s0 + r] = (best[r] < big_value<T>()) ? bidx[r] : -1;
     }
   }
@@ -3213,7 +3240,9 @@ extern "C" int phj_transport(const phj_transport_args* a) {
 template <int D, typename T, int RULE, int COST>
 static int feedback_impl(const phj_grid* g, const phj_stencil* st, const void* v,
                          const int8_t* kind, const uint32_t* fmask, const void* coef,
-                         double coef0, double unreach, int32_t* out, unsigned long long* evals,
+                         double coef0, double unreach, const int32_t* allow_row,
+                         const unsigned long long* allow_mask, const int32_t* allow_count,
+                         int32_t allow_words, int32_t* out, unsigned long long* evals,
                          cudaStream_t stream) {
   FeedbackParams p;
   p.g = *g;
@@ -3234,6 +3263,10 @@ static int feedback_impl(const phj_grid* g, const phj_stencil* st, const void* v
   p.unreach = unreach;
   p.out = out;
   p.evals = evals;
+  p.allow_row = allow_row;
+  p.allow_mask = allow_mask;
+  p.allow_count = allow_count;
+  p.allow_words = allow_words;
   size_t smem = (size_t)StencilSmem<D, T>::bytes(p.n_classes, p.nc) +
                 (size_t)p.n_classes * p.nc * 4 + 16;
   auto k = feedback_kernel<D, T, RULE, COST>;
@@ -3245,12 +3278,21 @@ static int feedback_impl(const phj_grid* g, const phj_stencil* st, const void* v
   return PHJ_OK;
 }
 
-extern "C" int phj_feedback(const phj_grid* g, const phj_stencil* st, int32_t dtype, int32_t rule,
-                            const void* v, const int8_t* kind, const uint32_t* fmask,
-                            const void* coef, double coef0, double unreach, int32_t* out,
-                            unsigned long long* evals, void* stream) {
+extern "C" int phj_feedback_allowed(const phj_grid* g, const phj_stencil* st, int32_t dtype,
+                                    int32_t rule, const void* v, const int8_t* kind,
+                                    const uint32_t* fmask, const void* coef, double coef0,
+                                    double unreach, const int32_t* allow_row,
+                                    const unsigned long long* allow_mask,
+                                    const int32_t* allow_count, int32_t allow_words,
+                                    int32_t* out, unsigned long long* evals, void* stream) {
   if (!g || !st || !v || !kind || !fmask || !out) {
     phj_set_error("phj_feedback: missing argument");
+    return PHJ_ERR_ARG;
+  }
+  if (allow_row && (!allow_mask || !allow_count || allow_words < 1 || allow_words > 2 ||
+                    st->n_classes != 1)) {
+    phj_set_error("phj_feedback: allowed masks need counts, 1..2 words (<= 128 stencil "
+                  "entries) and a single-class stencil");
     return PHJ_ERR_ARG;
   }
   if (rule == PHJ_RULE_REF && dtype == PHJ_F32) {
@@ -3267,7 +3309,8 @@ extern "C" int phj_feedback(const phj_grid* g, const phj_stencil* st, int32_t dt
 #define PHJ_FB(DD, TT, RR, CC)                                                             \
   if (D == DD && f32 == (sizeof(TT) == 4) && krz == (RR == PHJ_RULE_KRUZKOV) &&           \
       cc == (CC == PHJ_COST_CTRL))                                                         \
-    return feedback_impl<DD, TT, RR, CC>(g, st, v, kind, fmask, coef, coef0, unreach, out, \
+    return feedback_impl<DD, TT, RR, CC>(g, st, v, kind, fmask, coef, coef0, unreach,      \
+                                         allow_row, allow_mask, allow_count, allow_words, out, \
                                          evals, s);
   PHJ_FB(2, double, PHJ_RULE_REF, PHJ_COST_NODE)
   PHJ_FB(2, double, PHJ_RULE_REF, PHJ_COST_CTRL)
@@ -3284,6 +3327,14 @@ extern "C" int phj_feedback(const phj_grid* g, const phj_stencil* st, int32_t dt
 #undef PHJ_FB
   phj_set_error("phj_feedback: unsupported combination");
   return PHJ_ERR_UNSUPPORTED;
+}
+
+extern "C" int phj_feedback(const phj_grid* g, const phj_stencil* st, int32_t dtype, int32_t rule,
+                            const void* v, const int8_t* kind, const uint32_t* fmask,
+                            const void* coef, double coef0, double unreach, int32_t* out,
+                            unsigned long long* evals, void* stream) {
+  return phj_feedback_allowed(g, st, dtype, rule, v, kind, fmask, coef, coef0, unreach, nullptr,
+                              nullptr, nullptr, 0, out, evals, stream);
 }
 
 static int fmask_launch(const phj_grid* g, const int16_t* lab, const uint8_t* hard,

@@ -512,6 +512,41 @@ def _ext_user_tensor(a, plan: StencilPlan, dtype) -> torch.Tensor:
     return t.reshape(plan.grid.ext_shape).to(dtype)
 
 
+def allowed_tables(plan: StencilPlan, allowed) -> tuple:
+    """Device tables for a per-(serial, control) ``allowed`` mask
+    (_kernels.py:71-75 ``allowed[s, c]``; e.g. solver.allowed_mask): per ext
+    node its row (= user serial) of a bitmask over the stencil entries (entry
+    e allowed iff its original control is), and per row the number of allowed
+    admissible controls (candidate-evaluation count).  Single-class stencils
+    with at most 128 entries."""
+    st = plan.stencils
+    if st.n_classes != 1:
+        raise ConfigurationError("allowed= needs a single-class stencil")
+    n = plan.grid.n_interior
+    a = allowed.detach() if isinstance(allowed, torch.Tensor) else torch.as_tensor(
+        np.asarray(allowed))
+    nc = len(plan.spec.control_set)
+    if tuple(a.shape) != (n, nc):
+        raise ConfigurationError(f"allowed must have shape ({n}, {nc}), got {tuple(a.shape)}")
+    dev = plan.device
+    a = a.to(dev) != 0
+    noct = st.oct_start.shape[1] - 1
+    e0, e1 = int(st.oct_start[0, 0]), int(st.oct_start[0, noct])
+    if e1 > 128:
+        raise ConfigurationError("allowed= supports at most 128 stencil entries")
+    words = 1 if e1 <= 64 else 2
+    ctrl = torch.as_tensor(st.ctrl[:e1].astype(np.int64), device=dev)
+    mask = torch.zeros((n, words), dtype=torch.int64, device=dev)
+    for e in range(e0, e1):
+        mask[:, e >> 6] |= a[:, int(ctrl[e])].long() << (e & 63)
+    adm = torch.unique(ctrl[e0:e1])
+    count = a[:, adm].sum(dim=1).to(torch.int32)
+    rows = torch.full(plan.int_ext, -1, dtype=torch.int32, device=dev)
+    user = torch.arange(n, dtype=torch.int32, device=dev)
+    plan.interior_int(rows).copy_(plan.serial_to_internal(user).view(plan.int_shape))
+    return rows.contiguous(), mask.contiguous(), count.contiguous(), words
+
+
 def solve(field: NodeField, spec: ProblemSpec, node_set=None,
           cfg: Optional[SolverConfig] = None, strategy: Optional[ExecutionStrategy] = None, *,
           table: Optional[StencilPlan] = None, active=None, frozen=None, hard=None,
@@ -521,14 +556,13 @@ def solve(field: NodeField, spec: ProblemSpec, node_set=None,
     Semantics follow the reference: ``active`` selects live reads, ``frozen``
     supplies Dirichlet data elsewhere, otherwise non-active corners are
     structurally blocked; ``hard`` overrides the block mask.  ``sweep_order``
-    is accepted and has no effect (Jacobi).  ``allowed`` (AO3) is not on the
-    device path yet."""
+    is accepted and has no effect (Jacobi).  ``allowed`` restricts the
+    controls per (serial, control) (_kernels.py:71-75, AO3)."""
     cfg = cfg or SolverConfig()
     grid = field.grid
     require_cuda(field.values)
-    if allowed is not None:
-        raise ConfigurationError("conical control reduction (allowed=) is not on the device path")
     plan = table if table is not None else StencilPlan(grid, spec)
+    ao3 = allowed_tables(plan, allowed) if allowed is not None else None
     order = _as_user_serials(grid, node_set)
     if order.size == 0:
         return SweepStats()
@@ -571,11 +605,16 @@ def solve(field: NodeField, spec: ProblemSpec, node_set=None,
         st = SweepStats(sweeps=1, node_relaxations=order.size)
     else:
         res = device_solve(plan, work, lab, fmask, 1, rule=rule, dtype=dtype, tol=cfg.tol,
-                           max_sweeps=cfg.sweep_limit(grid), act_tol=cfg.act_tol,
+                           max_sweeps=cfg.sweep_limit(grid), act_tol=cfg.act_tol, ao3=ao3,
                            schedule=cfg.schedule,
                            inner=cfg.inner_for(grid.dim))
         res_vals = res.values
-        st = stats_for_patch(res, 0, n_free, plan.n_adm, cfg.tol)
+        cands = None
+        if ao3 is not None:  # dense count over the allowed sets (_kernels.py:73-76)
+            cnt_user = ao3[2]  # rows are user serials
+            order_t = torch.as_tensor(order, device=dev)
+            cands = int(cnt_user[order_t[free]].sum().item())
+        st = stats_for_patch(res, 0, n_free, plan.n_adm, cfg.tol, cands_per_sweep=cands)
         st.node_relaxations = order.size * st.sweeps
         st.performed_evals = res.evals
     out_user = plan.user_from_working(res_vals, rule, dtype).view(-1)
@@ -593,25 +632,27 @@ def extract_feedback(field: NodeField, spec: ProblemSpec, table: Optional[Stenci
     target/obstacle/unreachable nodes, ties to the lowest control index.
     Returns ``(FeedbackField, candidate_evals)``."""
     require_cuda(field.values)
-    if allowed is not None:
-        raise ConfigurationError("conical control reduction (allowed=) is not on the device path")
     plan = table if table is not None else StencilPlan(field.grid, spec)
     work = plan.working_from_user(field.values, rule, dtype)
-    fb = feedback_internal(plan, work, rule=rule, dtype=dtype)
+    fb = feedback_internal(plan, work, rule=rule, dtype=dtype,
+                           allowed=allowed_tables(plan, allowed) if allowed is not None else None)
     return FeedbackField(field.grid, spec.control_set, plan.serial_to_user(fb[0])), fb[1]
 
 
-def feedback_internal(plan: StencilPlan, work: torch.Tensor, *, rule: str, dtype: str):
+def feedback_internal(plan: StencilPlan, work: torch.Tensor, *, rule: str, dtype: str,
+                      allowed=None):
     lib = _lib.load()
     out = torch.empty(plan.grid.n_interior, dtype=torch.int32, device=plan.device)
     ev = torch.zeros(1, dtype=torch.int64, device=plan.device)
     coef, coef0 = plan.coef(rule, dtype)
     st = plan.stencil_struct()
-    _lib.check(lib.phj_feedback(ctypes_ref(plan.gs), ctypes_ref(st), _dtype_id(dtype),
-                                _rule_id(rule), _lib.ptr(work), _lib.ptr(plan.kind),
-                                _lib.ptr(plan.fmask_hard), _lib.ptr(coef), coef0,
-                                unreach_threshold(rule), _lib.ptr(out), _lib.ptr(ev),
-                                _lib.stream_handle()), "phj_feedback")
+    rows, mask, count, words = allowed if allowed is not None else (None, None, None, 0)
+    _lib.check(lib.phj_feedback_allowed(ctypes_ref(plan.gs), ctypes_ref(st), _dtype_id(dtype),
+                                        _rule_id(rule), _lib.ptr(work), _lib.ptr(plan.kind),
+                                        _lib.ptr(plan.fmask_hard), _lib.ptr(coef), coef0,
+                                        unreach_threshold(rule), _lib.ptr(rows), _lib.ptr(mask),
+                                        _lib.ptr(count), int(words), _lib.ptr(out),
+                                        _lib.ptr(ev), _lib.stream_handle()), "phj_feedback")
     return out, ev
 
 

@@ -474,3 +474,54 @@ def test_async_budget_exhaustion_sets_warning():
     g = phj.Grid(spec.box_lo, spec.box_hi, (101, 101))
     u, st = phj.solve_single(spec, g, phj.SolverConfig(tol=1e-8, max_sweeps=3, **ASYNC))
     assert not st.converged and st.warning
+
+
+# -- per-(serial, control) allowed masks on single-domain solves / feedback ----------
+# (_kernels.py:71-75: `allowed[s, c] == 0` skips the candidate and is not
+# counted; solver.py:446-476 builds such masks for AO3)
+
+
+def _c1_allowed(kind):
+    g = phj.Grid((-2.0, -2.0), (2.0, 2.0), (101, 101))
+    rng = np.random.default_rng(1109)
+    if kind == "random":
+        a = (rng.random((g.n_interior, 32)) < 0.6).astype(np.uint8)
+    else:  # conical reduction around the golden feedback, r = 3
+        c = golden("c1_fine.npz")
+        a = O.allowed_mask(C.circle(32), c["feedback"], 3.0)
+    return g, a
+
+
+@pytest.mark.parametrize("kind", ["random", "conical"])
+def test_solve_with_allowed_matches_oracle(kind):
+    spec = _eik_spec((-2.0, -2.0), (2.0, 2.0), C.circle(32), 0.1)
+    g, a = _c1_allowed(kind)
+    plan = phj.StencilPlan(g, spec)
+    u = phj.init_value_field(g, spec, kind=plan.serial_to_user(plan.kind))
+    st = phj.solve(u, spec, cfg=phj.SolverConfig(tol=1e-8), table=plan, allowed=a)
+    pr = C.c1_fine()
+    uo = O.init_field(pr, "reference")
+    ost = O.solve(uo, pr, rule="reference", mode="jacobi", tol=1e-8, allowed=a)
+    got = _flat(u.numpy())
+    assert _live_close(got, uo, 1e-8) <= 1e-8
+    # the evaluation count follows the allowed sets (same sweeps on both sides)
+    if st.sweeps == ost.sweeps:
+        assert st.candidate_evals == ost.candidate_evals
+
+
+@pytest.mark.parametrize("kind", ["random", "conical"])
+def test_feedback_with_allowed_matches_oracle(kind):
+    c = golden("c1_fine.npz")
+    spec = _eik_spec((-2.0, -2.0), (2.0, 2.0), C.circle(32), 0.1)
+    g, a = _c1_allowed(kind)
+    u = phj.NodeField(g, c["u_gs"])
+    fb, ev = phj.extract_feedback(u, spec, allowed=a)
+    got = fb.indices.cpu().numpy()
+    want, gaps, ne = O.feedback(_flat(c["u_gs"]), C.c1_fine(), rule="reference", allowed=a)
+    diff = got != want
+    ties = gaps < 1e-12 * np.maximum(1.0, np.abs(_flat(c["u_gs"])[g.interior_flat()]))
+    assert not np.any(diff & ~ties), np.where(diff & ~ties)
+    assert int(ev) == ne
+    # every chosen control is an allowed one
+    ok = got >= 0
+    assert np.all(a[np.where(ok)[0], got[ok]] == 1)
