@@ -525,3 +525,23 @@ def test_feedback_with_allowed_matches_oracle(kind):
     # every chosen control is an allowed one
     ok = got >= 0
     assert np.all(a[np.where(ok)[0], got[ok]] == 1)
+
+
+# -- static domain decomposition (decomp.py:101-190, test_decomp.py:96-112) ----------
+
+
+@pytest.mark.parametrize("R", [1, 4])
+def test_solve_dd_reaches_single_domain_fixed_point(R):
+    spec = _eik_spec((-2.0, -2.0), (2.0, 2.0), C.circle(32), 0.1)
+    g = phj.Grid(spec.box_lo, spec.box_hi, (51, 51))
+    cfg = phj.SolverConfig(tol=1e-9)
+    single, sst = phj.solve_single(spec, g, cfg)
+    dd, dst = phj.solve_dd(spec, g, phj.make_static_decomposition(g, R), cfg)
+    assert dst.converged and sst.converged
+    a, b = _flat(single.numpy()), _flat(dd.numpy())
+    assert np.array_equal(a < 0.5e9, b < 0.5e9)
+    live = a < 0.5e9
+    assert np.abs(a[live] - b[live]).max() <= 1e-8
+    # one box = the single-domain Jacobi iteration (same sweep count up to the stop)
+    if R == 1:
+        assert abs(dst.sweeps - sst.sweeps) <= 1
