@@ -640,7 +640,8 @@ __device__ __forceinline__ int eval_sweep(const T* lt, bool prune_on, const Sten
                                           const int* os, const uint32_t (&fm)[NB],
                                           const T (&ncoef)[NB], const bool (&comp)[NB],
                                           MinAcc<T> (&mn)[NB], T (&best)[NB], int (&bidx)[NB],
-                                          const Hook& hook, const Allowed<NB>* al = nullptr) {
+                                          const Hook& hook, const Allowed<NB>* al = nullptr,
+                                          bool warm = false) {
 #if PHJ_CTRL_REGNB
   if constexpr (COST == PHJ_COST_CTRL) {
     // per-control costs (no pruning), few controls: the whole neighbourhood
@@ -669,9 +670,16 @@ __device__ __forceinline__ int eval_sweep(const T* lt, bool prune_on, const Sten
   const int first = prune ? preferred_octant<D, T>(lt) : 0;
   OctNb<D, T, NB> cell;
   cell.load(lt, first);
-  eval_octant<D, T, NB, RULE, COST, SLOW, 0, OctNb<D, T, NB>, AO3>(cell, first, s, os, fm, ncoef,
-                                                                   nullptr, mn, best, bidx, al);
-  int n_ent = os[first + 1] - os[first];
+  int n_ent = 0;
+  // warm: the running minima start at the previous block-local relaxation's
+  // minima (an upper bound of the new ones: values only decreased), so the
+  // preferred octant is prunable too
+  if (!(prune && warm) || __any_sync(0xffffffffu, octant_needed<D, T, NB>(cell, comp, mn))) {
+    eval_octant<D, T, NB, RULE, COST, SLOW, 0, OctNb<D, T, NB>, AO3>(cell, first, s, os, fm,
+                                                                     ncoef, nullptr, mn, best,
+                                                                     bidx, al);
+    n_ent = os[first + 1] - os[first];
+  }
   hook();
 #pragma unroll 1
   for (int O = 0; O < (1 << D); ++O) {
@@ -993,6 +1001,11 @@ __device__ __forceinline__ int sweep_block(const SolveParams& p, const StencilSm
         hook();
       }
     };
+    // minima of the previous block-local relaxation: upper bounds of the next
+    // ones (tile values only decrease; candidates are monotone in them)
+    T warmv[NB];
+#pragma unroll
+    for (int r = 0; r < NB; ++r) warmv[r] = big_value<T>();
     for (int it = 0;;) {
       MinAcc<T> mn[NB];
       T best[NB];
@@ -1000,19 +1013,21 @@ __device__ __forceinline__ int sweep_block(const SolveParams& p, const StencilSm
 #pragma unroll
       for (int r = 0; r < NB; ++r) {
         mn[r].init();
+        mn[r].take(warmv[r]);
         best[r] = big_value<T>();
         bidx[r] = 0;
       }
+      const bool warm = it > 0;
       int n_ent;
       if (p.ao3_fb) {
         n_ent = eval_sweep<D, T, NB, RULE, COST, true, decltype(once), true>(
-            lt, p.prune != 0, s, os, fm, ncoef, comp, mn, best, bidx, once, &al);
+            lt, p.prune != 0, s, os, fm, ncoef, comp, mn, best, bidx, once, &al, warm);
       } else if (slow) {
         n_ent = eval_sweep<D, T, NB, RULE, COST, true>(lt, p.prune != 0, s, os, fm, ncoef, comp,
-                                                       mn, best, bidx, once);
+                                                       mn, best, bidx, once, nullptr, warm);
       } else {
         n_ent = eval_sweep<D, T, NB, RULE, COST, false>(lt, p.prune != 0, s, os, fm, ncoef, comp,
-                                                        mn, best, bidx, once);
+                                                        mn, best, bidx, once, nullptr, warm);
       }
       exec += (unsigned long long)n_ent * NB;
       evals += fcnt_sum;
@@ -1021,6 +1036,7 @@ __device__ __forceinline__ int sweep_block(const SolveParams& p, const StencilSm
       for (int r = 0; r < NB; ++r) {
         if (!comp[r]) continue;
         const T b = mn[r].get();
+        warmv[r] = b;
         T cand = b;
         if constexpr (COST == PHJ_COST_NODE) {
           cand = (RULE == PHJ_RULE_KRUZKOV) ? fma(ncoef[r], b, T(1) - ncoef[r]) : b + ncoef[r];
