@@ -42,8 +42,9 @@ for rep in range(2):
     t = tick("parts", t)
     parts_flat = [fplan.user_serials_to_internal_flat(p) for p in parts]
     t = tick("parts_flat", t)
+    tsched = cfg.schedule if fplan.grid.dim == 2 else "jacobi"
     phi, R, csw, upd = patchy.transport_internal(fplan, fb, parts_flat, pcfg.color_tol,
-                                                 10 * max(fplan.grid.shape))
+                                                 10 * max(fplan.grid.shape), tsched)
     t = tick("transport_internal", t)
     print("   transport kernel ms", patchy.TRANSPORT_DIAG.get("kernel_ms"))
     bv, bi = patchy.argmax_batched(fplan.gs, phi, R, fplan.grid.n_interior, fplan.device)
