@@ -17,7 +17,6 @@ BASELINE config 1 whose 26^2 coarse grid holds no target node), ``parts``
 from __future__ import annotations
 
 import dataclasses
-import os
 from dataclasses import dataclass, field as _field
 from typing import Callable, Optional, Sequence, Union
 
@@ -48,10 +47,11 @@ TRANSPORT_DIAG: dict = {}
 TRANSPORT_ACT_FRAC = 1.0e-3
 #: asynchronous transport: a colour change re-queues the neighbourhood only
 #: above this fraction of color_tol; relaxations per block visit by dimension
-TRANSPORT_ASYNC_FRAC = float(os.environ.get("PHJ_TASYNC_FRAC", "1e-3"))
-TRANSPORT_ASYNC_3D = os.environ.get("PHJ_TRANSPORT_ASYNC3D", "0") == "1"
-TRANSPORT_INNER = {2: int(os.environ.get("PHJ_TASYNC_INNER2", "8")),
-                   3: int(os.environ.get("PHJ_TASYNC_INNER3", "2"))}
+TRANSPORT_ASYNC_FRAC = 1.0e-3
+#: asynchronous transport in 3D too (off: slower than the Jacobi kernel there,
+#: DESIGN.md §3.1b); module attributes so experiments can flip them
+TRANSPORT_ASYNC_3D = False
+TRANSPORT_INNER = {2: 8, 3: 4}
 
 
 @dataclass
