@@ -196,8 +196,8 @@ int phj_feedback_allowed(const phj_grid* g, const phj_stencil* st, int32_t dtype
 typedef struct phj_transport_args {
   phj_grid grid;
   phj_stencil st;
-  double* phi0;
-  double* phi1;
+  void* phi0;           /* [n_colors][ext] in phi_dtype */
+  void* phi1;
   const int32_t* fb;    /* per internal serial, original control index or -1 */
   const int8_t* kind;   /* per internal serial */
   int32_t* ent_scratch; /* [interior nodes] int32 scratch (mover -> stencil entry) */
@@ -214,6 +214,8 @@ typedef struct phj_transport_args {
   unsigned long long* updates; /* out [1]: mover updates performed */
   int32_t options;      /* PHJ_TRANSPORT_* bits */
   int32_t inner_sweeps; /* async: relaxations of a colour per block visit (>= 1) */
+  int32_t phi_dtype;    /* PHJ_F64 (0) or PHJ_F32: storage of the colour fields
+                           (accumulation is fp64 either way) */
   void* stream;
 } phj_transport_args;
 
@@ -227,6 +229,9 @@ typedef struct phj_transport_args {
  * lowest colour on ties, patchy.py:251-256) */
 int phj_argmax_colors(const phj_grid* g, const double* phi, int32_t n_colors, double* best_val,
                       int32_t* best_idx, void* stream);
+/* the same over colour fields stored in phi_dtype (PHJ_F64 / PHJ_F32) */
+int phj_argmax_colors_t(const phj_grid* g, const void* phi, int32_t phi_dtype, int32_t n_colors,
+                        double* best_val, int32_t* best_idx, void* stream);
 int phj_transport(const phj_transport_args* a);
 
 /* Saturating multilinear lift of a coarse ext field to fine ext interior. */

@@ -69,7 +69,8 @@ class TransportArgs(ctypes.Structure):
     _fields_ = [("grid", Grid), ("st", Stencil), ("phi0", P), ("phi1", P), ("fb", P),
                 ("kind", P), ("ent_scratch", P), ("n_colors", I32), ("tol", D), ("act_eps", D),
                 ("max_sweeps", I32), ("workspace", P), ("maxch_hist", P), ("color_sweeps", P),
-                ("info", P), ("updates", P), ("options", I32), ("inner_sweeps", I32), ("stream", P)]
+                ("info", P), ("updates", P), ("options", I32), ("inner_sweeps", I32), ("phi_dtype", I32),
+                ("stream", P)]
 
 
 class Shapes(ctypes.Structure):
@@ -87,7 +88,8 @@ class SpeedModel(ctypes.Structure):
 EXPORTS = (
     "phj_solve_workspace_bytes", "phj_unroll", "phj_blocks_total", "phj_solve", "phj_fmask_from_labels",
     "phj_fmask_from_hard",
-    "phj_feedback", "phj_feedback_allowed", "phj_transport", "phj_lift", "phj_argmax_update", "phj_argmax_colors",
+    "phj_feedback", "phj_feedback_allowed", "phj_transport", "phj_lift", "phj_argmax_update",
+    "phj_argmax_colors", "phj_argmax_colors_t",
     "phj_assemble_codes",
     "phj_assemble_repair", "phj_assemble_finish", "phj_classify", "phj_node_coef",
     "phj_init_field", "phj_to_kruzkov", "phj_from_kruzkov", "phj_sync_periodic",
@@ -126,6 +128,7 @@ def load() -> ctypes.CDLL:
         "phj_lift": (ctypes.c_int, [P, P, I32, P, P, D, D, I32, P]),
         "phj_argmax_update": (ctypes.c_int, [P, P, I32, P, P, P]),
         "phj_argmax_colors": (ctypes.c_int, [P, P, I32, P, P, P]),
+        "phj_argmax_colors_t": (ctypes.c_int, [P, P, I32, I32, P, P, P]),
         "phj_assemble_codes": (ctypes.c_int, [P, P, P, P, P, P, P]),
         "phj_assemble_repair": (ctypes.c_int, [P, P, P, I32, P, P]),
         "phj_assemble_finish": (ctypes.c_int, [P, P, P, P, P, P]),

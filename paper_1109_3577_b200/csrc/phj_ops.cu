@@ -149,7 +149,8 @@ __global__ void argmax_kernel(phj_grid g, const double* __restrict__ phi, int j,
   }
 }
 
-__global__ void argmax_colors_kernel(phj_grid g, const double* __restrict__ phi, int R,
+template <typename PT>
+__global__ void argmax_colors_kernel(phj_grid g, const PT* __restrict__ phi, int R,
                                      double* __restrict__ best_val, int32_t* __restrict__ best_idx) {
   const int64_t N = n_interior(g);
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < N;
@@ -157,11 +158,11 @@ __global__ void argmax_colors_kernel(phj_grid g, const double* __restrict__ phi,
     int c[3];
     unravel(g, s, c);
     const int64_t plane = g.ext[0] * g.ext[1] * (g.dim == 3 ? g.ext[2] : 1);
-    const double* v = phi + iflat(g, c);
+    const PT* v = phi + iflat(g, c);
     double bv = 0.0;
     int32_t bi = 0;
     for (int j = 0; j < R; ++j) {
-      const double x = v[j * plane];
+      const double x = (double)v[j * plane];
       if (x > bv) {
         bv = x;
         bi = j;
@@ -527,17 +528,28 @@ extern "C" int phj_argmax_update(const phj_grid* g, const double* phi, int32_t j
   return PHJ_OK;
 }
 
-extern "C" int phj_argmax_colors(const phj_grid* g, const double* phi, int32_t n_colors,
-                                 double* best_val, int32_t* best_idx, void* stream) {
-  if (!g || !phi || !best_val || !best_idx || n_colors < 1) {
+extern "C" int phj_argmax_colors_t(const phj_grid* g, const void* phi, int32_t phi_dtype,
+                                   int32_t n_colors, double* best_val, int32_t* best_idx,
+                                   void* stream) {
+  if (!g || !phi || !best_val || !best_idx || n_colors < 1 ||
+      (phi_dtype != PHJ_F64 && phi_dtype != PHJ_F32)) {
     phj_set_error("phj_argmax_colors: bad arguments");
     return PHJ_ERR_ARG;
   }
-  argmax_colors_kernel<<<grid_blocks(n_interior(*g)), 256, 0, (cudaStream_t)stream>>>(
-      *g, phi, n_colors, best_val, best_idx);
+  if (phi_dtype == PHJ_F32)
+    argmax_colors_kernel<float><<<grid_blocks(n_interior(*g)), 256, 0, (cudaStream_t)stream>>>(
+        *g, (const float*)phi, n_colors, best_val, best_idx);
+  else
+    argmax_colors_kernel<double><<<grid_blocks(n_interior(*g)), 256, 0, (cudaStream_t)stream>>>(
+        *g, (const double*)phi, n_colors, best_val, best_idx);
   phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   return PHJ_OK;
+}
+
+extern "C" int phj_argmax_colors(const phj_grid* g, const double* phi, int32_t n_colors,
+                                 double* best_val, int32_t* best_idx, void* stream) {
+  return phj_argmax_colors_t(g, phi, PHJ_F64, n_colors, best_val, best_idx, stream);
 }
 
 extern "C" int phj_assemble_codes(const phj_grid* g, const double* best_val,

@@ -1714,7 +1714,7 @@ struct TransportParams {
   const int32_t* oct_start;
   const int32_t* ctrl;
   const double* weights;
-  double* phi[2];
+  void* phi[2];        // colour-major [R][ext] planes of PT (double or float)
   const int32_t* fb;
   const int8_t* kind;
   const int32_t* ent;  // per internal serial: stencil entry of the mover's feedback, or -1
@@ -1733,7 +1733,7 @@ struct TransportParams {
 #ifndef PHJ_TRANSPORT_CTAS
 #define PHJ_TRANSPORT_CTAS 2
 #endif
-template <int D>
+template <int D, typename PT>
 __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel(const __grid_constant__ TransportParams p) {
   using B = Blk<D>;
   constexpr int NC = 1 << D;
@@ -1794,8 +1794,8 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
   MarkQueue<D> mq;
   mq.init();
   for (;;) {
-    const double* pin = p.phi[buf];
-    double* pout = p.phi[buf ^ 1];
+    const PT* pin = (const PT*)p.phi[buf];
+    PT* pout = (PT*)p.phi[buf ^ 1];
     const int cnt = ld_cg(&p.ws.counts[sw]);
     const int* list = p.ws.list[sw & 1];
     int* cur_flags = p.ws.flags[sw & 1];
@@ -1903,12 +1903,12 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
           double cv[CB][NB][NC];
 #pragma unroll
           for (int q = 0; q < CB; ++q) {
-            const double* pj = pin + (int64_t)max(js[q], 0) * p.plane;
+            const PT* pj = pin + (int64_t)max(js[q], 0) * p.plane;
 #pragma unroll
             for (int r = 0; r < NB; ++r)
 #pragma unroll
               for (int k = 0; k < NC; ++k)
-                cv[q][r][k] = (js[q] >= 0 && e[r] >= 0) ? pj[base[r] + coff[k]] : 0.0;
+                cv[q][r][k] = (js[q] >= 0 && e[r] >= 0) ? (double)pj[base[r] + coff[k]] : 0.0;
           }
           double lmax[CB];
 #pragma unroll
@@ -1917,7 +1917,7 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
             if (js[q] < 0) continue;
             const int j = js[q];
             const bool live = s_done[j] == 0x7fffffff;
-            double* qj = pout + (int64_t)j * p.plane;
+            PT* qj = pout + (int64_t)j * p.plane;
 #pragma unroll
             for (int r = 0; r < NB; ++r) {
               if (e[r] < 0) continue;
@@ -1927,8 +1927,8 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
                 acc = fma(s_w[k * wpitch + e[r]], cv[q][r][k], acc);
                 if (k > 0 && k == kself[r]) old = cv[q][r][k];
               }
-              const double nv = live ? acc : old;
-              lmax[q] = fmax(lmax[q], fabs(old - nv));
+              const PT nv = (PT)(live ? acc : old);  // changes measured on the stored value
+              lmax[q] = fmax(lmax[q], fabs(old - (double)nv));
               qj[f0 + r] = nv;
               if (per0) {
                 if (c[0] == 0) qj[f0 + r + ghost_shift] = nv;
@@ -2023,7 +2023,7 @@ struct TTile {
   static constexpr int N = TileShape<D>::N;
 };
 
-template <int D>
+template <int D, typename PT>
 __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS)
     transport_async_kernel(const __grid_constant__ TransportParams p, int inner,
                            unsigned int budget) {
@@ -2087,7 +2087,7 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS)
   const int n0 = ld_cg(&p.ws.counts[0]);
   const unsigned cap = (unsigned)p.tg.total + (unsigned)(gridDim.x * kWarps);
   unsigned swept_local = 0;
-  double* phi = p.phi[0];
+  PT* phi = (PT*)p.phi[0];
   unsigned long long upd = 0;
   constexpr int NNB = D == 2 ? 9 : 27;
   const int ly = lane / B::LX, lx = lane % B::LX;
@@ -2184,7 +2184,7 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS)
 #pragma unroll
       for (int t = 0; t < TC; ++t) {
         if (js[t] < 0) continue;
-        const double* pj = phi + (int64_t)js[t] * p.plane;
+        const PT* pj = phi + (int64_t)js[t] * p.plane;
         double* tt = wt + t * S::N;
 #pragma unroll
         for (int i0 = 0; i0 < NT; i0 += 32) {
@@ -2197,7 +2197,7 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS)
               ry = rr - pl * S::RB;
             }
             const int yy = min(row0 + ry, rmax) - row0, xx = min(col0 + cc, cmax) - col0;
-            tt[rr * S::C + cc] = __ldcg(pj + o + pl * s0x + (int64_t)yy * rs + xx);
+            tt[rr * S::C + cc] = (double)__ldcg(pj + o + pl * s0x + (int64_t)yy * rs + xx);
           }
         }
       }
@@ -2219,10 +2219,11 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS)
             for (int k = 0; k < NC; ++k) acc = fma(s_w[k * wpitch + e[r]], tt[tb[r] + tcoff[k]], acc);
             const double old = tt[tnode + r];
             ++upd;
-            if (acc > old) {
-              big |= acc - old > p.act_eps;
+            const double nv = (double)(PT)acc;  // the value the field will hold
+            if (nv > old) {
+              big |= nv - old > p.act_eps;
               any = true;
-              tt[tnode + r] = acc;
+              tt[tnode + r] = nv;
             }
           }
           if (__any_sync(FULL, any)) wrote |= 1ull << t;
@@ -2240,12 +2241,12 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS)
 #pragma unroll
       for (int t = 0; t < TC; ++t) {
         if (!((wrote >> t) & 1ull)) continue;
-        double* pj = phi + (int64_t)js[t] * p.plane;
+        PT* pj = phi + (int64_t)js[t] * p.plane;
         const double* tt = wt + t * S::N;
 #pragma unroll
         for (int r = 0; r < NB; ++r) {
           if (e[r] < 0) continue;
-          const double v = tt[tnode + r];
+          const PT v = (PT)tt[tnode + r];
           pj[f0 + r] = v;
           if (per0) {
             if (c[0] == 0) pj[f0 + r + ghost_shift] = v;
@@ -2410,8 +2411,8 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS)
   int ticket = 0;
   if (lane == 0) ticket = atomicAdd(&p.ws.take[0], 1);
   for (;;) {
-    const double* pin = p.phi[buf];
-    double* pout = p.phi[buf ^ 1];
+    const double* pin = (const double*)p.phi[buf];
+    double* pout = (double*)p.phi[buf ^ 1];
     const int cnt = ld_cg(&p.ws.counts[m]);
     const int* list = p.ws.list[m & 1];
     int* cur_flags = p.ws.flags[m & 1];
@@ -2665,8 +2666,8 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS)
     const int d = s_done[j];
     if (d == 0x7fffffff || !(d & 1)) continue;
     const int mj = (d - 1) / 2;  // pass that held the stop
-    const double* rj = p.phi[mj & 1] + (int64_t)j * p.plane;
-    double* wj = p.phi[(mj + 1) & 1] + (int64_t)j * p.plane;
+    const double* rj = (const double*)p.phi[mj & 1] + (int64_t)j * p.plane;
+    double* wj = (double*)p.phi[(mj + 1) & 1] + (int64_t)j * p.plane;
     for (int64_t sidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; sidx < N; sidx += gstride) {
       const int e = __ldg(&p.ent[sidx]);
       if (e < 0) continue;
@@ -2710,8 +2711,8 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS)
     const int d = s_done[j];
     const int mj = (d == 0x7fffffff) ? mfin - 1 : (d - 1) / 2;
     if (((mj + 1) & 1) == 0) continue;
-    const double* src = p.phi[1] + (int64_t)j * p.plane;
-    double* dst = p.phi[0] + (int64_t)j * p.plane;
+    const double* src = (const double*)p.phi[1] + (int64_t)j * p.plane;
+    double* dst = (double*)p.phi[0] + (int64_t)j * p.plane;
     for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < p.plane; f += gstride)
       dst[f] = src[f];
   }
@@ -3212,7 +3213,11 @@ static int transport_impl(const phj_transport_args* a) {
     void* aargs[] = {(void*)&p, (void*)&inner, (void*)&budget};
     const size_t smem = (size_t)(nent | 1) * (1 << D) * 8 +
                         (size_t)kWarps * TTile<D>::TC * TileShape<D>::N * 8 + (size_t)nent + 16;
-    int rc = async_launch(transport_async_kernel<D>, smem, aargs, p.ws, p.tg.total, stream);
+    int rc = a->phi_dtype == PHJ_F32
+                 ? async_launch(transport_async_kernel<D, float>, smem, aargs, p.ws, p.tg.total,
+                                stream)
+                 : async_launch(transport_async_kernel<D, double>, smem, aargs, p.ws, p.tg.total,
+                                stream);
     if (rc) return rc;
     async_finish_kernel<<<1, 256, 0, stream>>>(p.ws, p.R, nullptr, p.color_sweeps, p.info);
     phj_count_launch(1);
@@ -3223,9 +3228,12 @@ static int transport_impl(const phj_transport_args* a) {
   // two sweeps per barrier pay in 2D only (3D: the 2-ring halo is 5 planes
   // deep and the activity must reach +-2 planes -- measured 2x slower)
   static const bool one_sweep = getenv("PHJ_TRANSPORT_T1") && atoi(getenv("PHJ_TRANSPORT_T1"));
-  if (one_sweep || D == 3) {
+  if (one_sweep || D == 3 || a->phi_dtype == PHJ_F32) {  // fp32 phi: one-sweep kernel
     size_t smem = (size_t)(nent | 1) * (1 << D) * 8 + (size_t)p.R * 12 + (size_t)nent + 16;
-    return coop_launch(transport_kernel<D>, (p.tg.total + kWarps - 1) / kWarps, smem, args,
+    if (a->phi_dtype == PHJ_F32)
+      return coop_launch(transport_kernel<D, float>, (p.tg.total + kWarps - 1) / kWarps, smem,
+                         args, stream, nullptr);
+    return coop_launch(transport_kernel<D, double>, (p.tg.total + kWarps - 1) / kWarps, smem, args,
                        stream, nullptr);
   }
   size_t smem = (size_t)align_up((int64_t)(nent | 1) * (1 << D) * 8 + 16 * (int64_t)p.R +
@@ -3245,6 +3253,10 @@ extern "C" int phj_transport(const phj_transport_args* a) {
   if (a->grid.periodic[1] || a->grid.periodic[2]) {
     phj_set_error("phj_transport: only internal axis 0 may be periodic");
     return PHJ_ERR_UNSUPPORTED;
+  }
+  if (a->phi_dtype != PHJ_F64 && a->phi_dtype != PHJ_F32) {
+    phj_set_error("phj_transport: phi_dtype must be PHJ_F64 or PHJ_F32");
+    return PHJ_ERR_ARG;
   }
   if (a->n_colors < 1 || a->n_colors > kMaxColors || !a->maxch_hist || !a->color_sweeps) {
     phj_set_error("phj_transport: n_colors must be in [1, %d]", kMaxColors);

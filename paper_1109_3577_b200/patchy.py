@@ -52,6 +52,8 @@ TRANSPORT_ASYNC_FRAC = 1.0e-3
 #: DESIGN.md §3.1b); module attributes so experiments can flip them
 TRANSPORT_ASYNC_3D = False
 TRANSPORT_INNER = {2: 8, 3: 4}
+#: fp32 workloads store the colour fields in fp32
+TRANSPORT_PHI_FP32 = True
 
 
 @dataclass
@@ -202,15 +204,18 @@ def lift_internal(cplan: StencilPlan, vc: torch.Tensor, fplan: StencilPlan, rule
 
 
 def transport_internal(plan: StencilPlan, fb_int: torch.Tensor, parts_flat: Sequence,
-                       tol: float, max_sweeps: int, schedule: str = "jacobi"):
+                       tol: float, max_sweeps: int, schedule: str = "jacobi",
+                       phi_dtype: torch.dtype = torch.float64):
     """All colours in one launch, each Jacobi to its own max|change| <= tol
     ("jacobi"), or asynchronously in place until no node changes a colour by
     more than TRANSPORT_ASYNC_FRAC * tol ("async").
     ``parts_flat``: per colour, internal ext flat indices of its part.
+    ``phi_dtype`` float32 halves the colour fields' footprint (fp64
+    accumulation either way; used for fp32 workloads).
     Returns (phi [R][ext] tensor, R, per-colour sweeps, updates)."""
     lib = _lib.load()
     R = len(parts_flat)
-    phi0 = torch.zeros((R,) + plan.int_ext, dtype=torch.float64, device=plan.device)
+    phi0 = torch.zeros((R,) + plan.int_ext, dtype=phi_dtype, device=plan.device)
     for j, pf in enumerate(parts_flat):
         phi0[j].view(-1)[pf] = 1.0
         _sync_periodic(plan, phi0[j])
@@ -236,6 +241,7 @@ def transport_internal(plan: StencilPlan, fb_int: torch.Tensor, parts_flat: Sequ
     a.act_eps = tol * (TRANSPORT_ASYNC_FRAC if asyn else TRANSPORT_ACT_FRAC)
     a.options = _lib.TRANSPORT_ASYNC if asyn else 0
     a.inner_sweeps = TRANSPORT_INNER[plan.grid.dim]
+    a.phi_dtype = _lib.F32 if phi_dtype == torch.float32 else _lib.F64
     a.max_sweeps = max_sweeps
     a.workspace = _lib.ptr(ws)
     a.maxch_hist = _lib.ptr(mc)
@@ -259,7 +265,7 @@ def transport_internal(plan: StencilPlan, fb_int: torch.Tensor, parts_flat: Sequ
 
 
 def _transport_and_argmax(fplan: StencilPlan, fb: torch.Tensor, parts, color_tol: float,
-                          limit: int, schedule: str = "jacobi"):
+                          limit: int, schedule: str = "jacobi", dtype: str = "float64"):
     """Transport of every colour + running argmax (patchy.py:183-219,
     251-256).  With several ranks each rank transports its own colours
     (dist.my_colours) and the argmax is merged exactly across ranks.
@@ -277,8 +283,11 @@ def _transport_and_argmax(fplan: StencilPlan, fb: torch.Tensor, parts, color_tol
         # one-plane blocks relax little per visit and it is slower (C3 48 ->
         # 58 ms), so 3D keeps the Jacobi transport
         tsched = schedule if (fplan.grid.dim == 2 or TRANSPORT_ASYNC_3D) else "jacobi"
+        # fp32 workloads keep their colour fields in fp32 too (half the
+        # footprint: 35 GB instead of 70 GB at config 5)
+        pdt = torch.float32 if (dtype == "float32" and TRANSPORT_PHI_FP32) else torch.float64
         phi, _, csw, upd = transport_internal(fplan, fb, parts_flat, color_tol, limit,
-                                              tsched)
+                                              tsched, pdt)
         best_val, best_idx = argmax_batched(fplan.gs, phi, len(mine), n, dev)
         del phi
         csw_all[torch.as_tensor(mine, device=dev)] = torch.as_tensor(csw, device=dev)
@@ -313,8 +322,9 @@ def argmax_batched(gs, phi: torch.Tensor, R: int, n_serial: int, device):
     lib = _lib.load()
     best_val = torch.empty(n_serial, dtype=torch.float64, device=device)
     best_idx = torch.empty(n_serial, dtype=torch.int32, device=device)
-    _lib.check(lib.phj_argmax_colors(ctypes_ref(gs), _lib.ptr(phi), R, _lib.ptr(best_val),
-                                     _lib.ptr(best_idx), _lib.stream_handle()), "argmax")
+    pdt = _lib.F32 if phi.dtype == torch.float32 else _lib.F64
+    _lib.check(lib.phj_argmax_colors_t(ctypes_ref(gs), _lib.ptr(phi), pdt, R, _lib.ptr(best_val),
+                                       _lib.ptr(best_idx), _lib.stream_handle()), "argmax")
     return best_val, best_idx
 
 
@@ -667,7 +677,7 @@ def run_patchy(spec: ProblemSpec, pcfg: PatchyConfig, cfg: Optional[SolverConfig
         limit = pcfg.transport_max_sweeps or 10 * max(fine_grid.shape)
         n_colors = len(parts)
         best_val, best_idx, csw, upd = _transport_and_argmax(fplan, fb, parts, pcfg.color_tol,
-                                                             limit, cfg.schedule)
+                                                             limit, cfg.schedule, cfg.dtype)
         stats.transport_updates += upd
         transport_sweeps = [abs(x) for x in csw]
         for j, x in enumerate(csw):

@@ -62,7 +62,7 @@ def _values_on_oracle_labels(w, ores, fine):
     return _to_v(val.numpy().reshape(-1))[fine.grid.interior_flat()]
 
 
-def _compare(res, ores, fine, bar, name, w, tie_gap=1e-12):
+def _compare(res, ores, fine, bar, name, w, tie_gap=1e-12, phi_gap=1e-9):
     g = fine.grid
     inner = g.interior_flat()
     got_v = _to_v(res.value.numpy().reshape(-1))[inner]
@@ -77,8 +77,9 @@ def _compare(res, ores, fine, bar, name, w, tie_gap=1e-12):
     assert not np.any(fdiff & ~ties), "feedback differs away from argmin ties"
     if not fdiff.any():
         # identical feedback => identical transport inputs => labels agree
-        # except where two colours' masses are within 1e-9 (counted)
-        phi_ties = ores.phi_gap < 1e-9
+        # except where two colours' masses are within phi_gap (counted; fp32
+        # workloads store the colour fields in fp32: ~1e-7)
+        phi_ties = ores.phi_gap < phi_gap
         print(f"   colour-mass near-ties {int(phi_ties.sum())}")
         assert not np.any(ldiff & ~phi_ties)
     if ldiff.any():
@@ -102,7 +103,7 @@ def test_c2_reduced_kruzkov_fp32():
     # away from such gaps, values on common labels at 1e-4
     w = configs.c2(n=129, dtype="float32")
     res, ores, fine = _run_both(w)
-    _compare(res, ores, fine, 1e-4, "c2@129 fp32", w, tie_gap=1e-5)
+    _compare(res, ores, fine, 1e-4, "c2@129 fp32", w, tie_gap=1e-5, phi_gap=1e-6)
 
 
 @pytest.mark.parametrize("schedule", ["jacobi", "async"])
@@ -129,7 +130,7 @@ def test_c5_reduced_kruzkov_fp64(schedule):
 def test_c5_reduced_kruzkov_fp32():
     w = configs.c5(n=65, dtype="float32")
     res, ores, fine = _run_both(w)
-    _compare(res, ores, fine, 1e-4, "c5@65 fp32", w, tie_gap=1e-5)
+    _compare(res, ores, fine, 1e-4, "c5@65 fp32", w, tie_gap=1e-5, phi_gap=1e-6)
 
 
 def test_c1_reference_rule_full_pipeline_matches_oracle_gs():
