@@ -248,6 +248,10 @@ int phj_assemble_codes(const phj_grid* g, const double* best_val, const int32_t*
 int phj_assemble_repair(const phj_grid* g, const int32_t* color_in, int32_t* color_out,
                         int32_t n_colors, int32_t* counters, void* stream);
 /* leftovers -> 0, boundary flags, patch labels for the solve (patchy.py:284-300) */
+/* patch sizes: counts[c] = #{s < n : color[s] == c}, 0 <= c < n_colors <= 16384
+ * (the per-patch node counts of patchy.py:293-300 / the LPT weights) */
+int phj_count_labels(const int32_t* color, int64_t n, int32_t n_colors,
+                     unsigned long long* counts, void* stream);
 int phj_assemble_finish(const phj_grid* g, int32_t* color, uint8_t* boundary, int16_t* lab,
                         int32_t* counters, void* stream);
 

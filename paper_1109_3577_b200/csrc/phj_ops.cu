@@ -6,6 +6,8 @@
 #include <cstdio>
 #include <cstring>
 
+#include <algorithm>
+
 #include "phj_common.cuh"
 
 static thread_local char g_err[512] = "";
@@ -575,6 +577,39 @@ extern "C" int phj_assemble_repair(const phj_grid* g, const int32_t* color_in, i
   PHJ_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(int32_t), s));
   repair_kernel<<<grid_blocks(n_interior(*g)), 256, 0, s>>>(*g, color_in, color_out, n_colors,
                                                             counters); phj_count_launch(1);
+  PHJ_CUDA(cudaGetLastError());
+  return PHJ_OK;
+}
+
+// Patch sizes: counts[c] += #{s : color[s] == c} for 0 <= c < n_colors
+// (per-CTA shared-memory histogram, one global add per bin and CTA).
+__global__ void count_labels_kernel(const int32_t* __restrict__ color, int64_t n, int n_colors,
+                                    unsigned long long* __restrict__ counts) {
+  extern __shared__ unsigned int s_cnt[];
+  for (int i = threadIdx.x; i < n_colors; i += blockDim.x) s_cnt[i] = 0u;
+  __syncthreads();
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int c = color[s];
+    if (c >= 0 && c < n_colors) atomicAdd(&s_cnt[c], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n_colors; i += blockDim.x)
+    if (s_cnt[i]) atomicAdd(&counts[i], (unsigned long long)s_cnt[i]);
+}
+
+extern "C" int phj_count_labels(const int32_t* color, int64_t n, int32_t n_colors,
+                                unsigned long long* counts, void* stream) {
+  if (!color || !counts || n_colors < 1 || n_colors > 16384 || n < 0) {
+    phj_set_error("phj_count_labels: bad arguments");
+    return PHJ_ERR_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  PHJ_CUDA(cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * n_colors, st));
+  if (n == 0) return PHJ_OK;
+  const int nb = (int)std::min<int64_t>((n + 255) / 256, 2 * 148);
+  count_labels_kernel<<<nb, 256, n_colors * sizeof(unsigned int), st>>>(color, n, n_colors, counts);
+  phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   return PHJ_OK;
 }

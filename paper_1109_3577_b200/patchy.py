@@ -113,9 +113,7 @@ class PatchMap:
         return self._patch_nodes
 
     def sizes(self) -> np.ndarray:
-        c = self.color
-        live = c[c >= 0].long()
-        return torch.bincount(live, minlength=self.n_patches)[: self.n_patches].cpu().numpy()
+        return count_labels(self.color, self.n_patches).cpu().numpy()
 
     def size_report(self) -> tuple:
         sizes = self.sizes()
@@ -400,6 +398,19 @@ def ao3_tables(plan: StencilPlan, spec: ProblemSpec, fb_int: torch.Tensor, r: fl
             torch.as_tensor(count, device=dev), words)
 
 
+def count_labels(color: torch.Tensor, n_labels: int) -> torch.Tensor:
+    """Nodes per label 0..n_labels-1 of an int32 label vector (phj_count_labels
+    on the device; a host-resident PatchMap is counted on the host)."""
+    if not color.is_cuda:
+        c = color.numpy()
+        return torch.as_tensor(np.bincount(c[c >= 0], minlength=n_labels)[:n_labels])
+    out = torch.empty(n_labels, dtype=torch.int64, device=color.device)
+    c = color.to(torch.int32).contiguous()
+    _lib.check(_lib.load().phj_count_labels(_lib.ptr(c), c.numel(), n_labels, _lib.ptr(out),
+                                            _lib.stream_handle()), "count_labels")
+    return out
+
+
 def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Tensor,
                            n_patches: int, pcfg: PatchyConfig, cfg: SolverConfig,
                            lifted_work: Optional[torch.Tensor] = None,
@@ -419,7 +430,7 @@ def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Te
         seed = torch.where(lv < thr, lv, torch.full_like(lv, unr))
         inner_w.copy_(torch.where(col3 >= 0, seed, inner_w))
         _sync_periodic(plan, work)
-    sizes = torch.bincount(color[color >= 0].long(), minlength=n_patches)[:n_patches].cpu().numpy()
+    sizes = count_labels(color, n_patches).cpu().numpy()
     cands = None  # AO3: candidates per sweep per patch (reduced control sets)
     if ao3 is not None:
         fbx, _, acount, _ = ao3
