@@ -235,6 +235,16 @@ int phj_argmax_colors_t(const phj_grid* g, const void* phi, int32_t phi_dtype, i
 int phj_transport(const phj_transport_args* a);
 
 /* Saturating multilinear lift of a coarse ext field to fine ext interior. */
+/* multilinear interpolation of an ext field (dtype) at n arbitrary points
+ * (row-major [n][dim] doubles in the grid's coordinates): grid.interpolate_many
+ * (grid.py:242-261) semantics -- 1e-9 bounds tolerance on the ghost-extended
+ * box (ood[i] = 1 outside), snapped locals, saturation to sat_value when a
+ * nonzero-weight corner is >= sat_threshold (saturate != 0); out in double.
+ * Used by analysis.trace_trajectory (analysis.py:82-139). */
+int phj_interpolate_points(const phj_grid* g, int32_t dtype, const void* field,
+                           const double* points, int64_t n, double sat_threshold,
+                           double sat_value, int32_t saturate, double* out, int8_t* ood,
+                           void* stream);
 int phj_lift(const phj_grid* gc, const phj_grid* gf, int32_t dtype, const void* vc, void* vf,
              double sat_threshold, double sat_value, int32_t saturate, void* stream);
 

@@ -90,6 +90,7 @@ EXPORTS = (
     "phj_fmask_from_hard",
     "phj_feedback", "phj_feedback_allowed", "phj_transport", "phj_lift", "phj_argmax_update",
     "phj_argmax_colors", "phj_argmax_colors_t", "phj_count_labels",
+    "phj_interpolate_points",
     "phj_assemble_codes",
     "phj_assemble_repair", "phj_assemble_finish", "phj_classify", "phj_node_coef",
     "phj_init_field", "phj_to_kruzkov", "phj_from_kruzkov", "phj_sync_periodic",
@@ -130,6 +131,8 @@ def load() -> ctypes.CDLL:
         "phj_argmax_colors": (ctypes.c_int, [P, P, I32, P, P, P]),
         "phj_argmax_colors_t": (ctypes.c_int, [P, P, I32, I32, P, P, P]),
         "phj_count_labels": (ctypes.c_int, [P, ctypes.c_int64, I32, P, P]),
+        "phj_interpolate_points": (ctypes.c_int, [P, I32, P, P, ctypes.c_int64, D, D, I32, P, P,
+                                                  P]),
         "phj_assemble_codes": (ctypes.c_int, [P, P, P, P, P, P, P]),
         "phj_assemble_repair": (ctypes.c_int, [P, P, P, I32, P, P]),
         "phj_assemble_finish": (ctypes.c_int, [P, P, P, P, P, P]),

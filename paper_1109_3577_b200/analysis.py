@@ -1,4 +1,5 @@
-"""Error metrics (mirror of patchyhjb.analysis.error_report, analysis.py:25-63).
+"""Error metrics and greedy-feedback trajectories (mirror of patchyhjb.analysis,
+analysis.py:25-139).
 
 ``e1`` averages |a - b| over nodes finite (< sentinel/2) in both fields,
 ``e1_allnodes`` divides the same sum by the interior node count.  The
@@ -12,8 +13,14 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+import ctypes
+
 from . import _lib
 from .grid import NodeField, require_cuda
+
+
+def ctypes_ref(x):
+    return ctypes.byref(x)
 
 
 @dataclass(frozen=True)
@@ -58,3 +65,124 @@ def error_report(a, b, against: str = "dd_reference") -> ErrorReport:
     if compared == 0:
         return ErrorReport(0.0, 0.0, 0.0, 0, n, against)
     return ErrorReport(s / compared, mx, s / n, compared, n - compared, against)
+
+
+# -- greedy-feedback trajectories (analysis.py:67-139) -------------------------------
+
+REACHED_TARGET = "reached_target"
+LEFT_DOMAIN = "left_domain"
+STEP_LIMIT = "step_limit"
+STALLED = "stalled"
+
+
+@dataclass(frozen=True)
+class Trajectory:
+    """Discrete path from a start point; steps have length exactly k."""
+
+    points: np.ndarray
+    termination: str
+
+    @property
+    def n_steps(self) -> int:
+        return self.points.shape[0] - 1
+
+    @property
+    def length(self) -> float:
+        return float(np.linalg.norm(np.diff(self.points, axis=0), axis=1).sum())
+
+
+def trace_trajectories(field: NodeField, spec, starts, max_steps=None) -> list:
+    """Follow the value function's greedy feedback from many starts at once
+    (analysis.py:82-139, batched): each step minimises interpolated value +
+    step cost over the controls with |h f| = k; stops on target entry,
+    domain exit, the step cap, or when no control has a finite candidate.
+
+    The user's dynamics / target / obstacle callables run on the host for
+    all live trajectories at once (they are arbitrary Python); the candidate
+    feet of every (trajectory, control) are interpolated on the device
+    (``phj_interpolate_points``, bit-exact with the reference's
+    interpolate_many) -- the arithmetic around it follows the reference
+    operation by operation."""
+    grid = field.grid
+    X = np.atleast_2d(np.asarray(starts, dtype=float)).copy()
+    if X.shape[1] != grid.dim:
+        raise ValueError(f"start must be a {grid.dim}-vector")
+    if spec.running_cost is not None:
+        from .grid import ConfigurationError
+        raise ConfigurationError("running costs are not supported")
+    if spec.obstacles is not None and np.any(spec.obstacles.contains(X)):
+        raise ValueError("trajectory start lies inside an obstacle")
+    if max_steps is None:
+        max_steps = 10 * int(sum(grid.shape))
+    dev = require_cuda(field.values)
+    lib = _lib.load()
+    gs = grid.device_struct()
+    vals = field.values.contiguous()
+    dtype_id = _lib.F32 if vals.dtype == torch.float32 else _lib.F64
+    sent = float(field.sentinel)
+    half = 0.5 * sent
+    k = grid.k_step
+    controls = np.asarray(spec.control_set.controls, dtype=float)
+    nc = controls.shape[0]
+    K = X.shape[0]
+    per = np.asarray(grid.periodic, dtype=bool)
+    paths = [[X[i].copy()] for i in range(K)]
+    term = [None] * K
+    live = np.arange(K)
+    for _ in range(max_steps):
+        x = X[live]
+        inside = np.asarray(spec.target.contains(x), dtype=bool)
+        for i in live[inside]:
+            term[i] = REACHED_TARGET
+        live, x = live[~inside], x[~inside]
+        if live.size == 0:
+            break
+        F = np.stack([np.asarray(spec.dynamics(x, controls[c]), dtype=float)
+                      for c in range(nc)], axis=1)                     # [L, nc, d]
+        speeds = np.linalg.norm(F, axis=2)
+        eps = 1.0e-12 * np.maximum(speeds.max(axis=1), 1.0)
+        ok = speeds >= eps[:, None]
+        with np.errstate(divide="ignore", invalid="ignore"):
+            h = np.where(ok, k / speeds, 0.0)
+        feet = x[:, None, :] + h[:, :, None] * F
+        pts = torch.as_tensor(feet.reshape(-1, grid.dim), device=dev).contiguous()
+        out = torch.empty(pts.shape[0], dtype=torch.float64, device=dev)
+        ood = torch.empty(pts.shape[0], dtype=torch.int8, device=dev)
+        _lib.check(lib.phj_interpolate_points(ctypes_ref(gs), dtype_id, _lib.ptr(vals),
+                                              _lib.ptr(pts), pts.shape[0], half, sent, 1,
+                                              _lib.ptr(out), _lib.ptr(ood),
+                                              _lib.stream_handle()), "interpolate_points")
+        v = out.cpu().numpy().reshape(live.size, nc)
+        bad = ood.cpu().numpy().reshape(live.size, nc) != 0
+        ok &= ~bad & (v < half)
+        cand = np.where(ok, v + h, np.inf)
+        best = np.argmin(cand, axis=1)                                  # lowest index on ties
+        found = ok[np.arange(live.size), best]
+        for j in np.where(~found)[0]:
+            term[live[j]] = STALLED
+        keep = np.where(found)[0]
+        nx = feet[keep, best[keep]]
+        if per.any():  # periodic axes (extension): keep the coordinate in [lo, hi)
+            span = grid.hi - grid.lo
+            nx[:, per] = grid.lo[per] + np.mod(nx[:, per] - grid.lo[per], span[per])
+        X[live[keep]] = nx
+        left = np.any((nx < grid.lo) & ~per, axis=1) | np.any((nx > grid.hi) & ~per, axis=1)
+        for j, i in enumerate(live[keep]):
+            paths[i].append(nx[j].copy())
+            if left[j]:
+                term[i] = LEFT_DOMAIN
+        live = live[keep][~left]
+        if live.size == 0:
+            break
+    for i in range(K):
+        if term[i] is None:
+            term[i] = STEP_LIMIT
+    return [Trajectory(np.array(paths[i]), term[i]) for i in range(K)]
+
+
+def trace_trajectory(field: NodeField, spec, start, max_steps=None) -> Trajectory:
+    """Single-start form (analysis.py:82-139)."""
+    x = np.asarray(start, dtype=float)
+    if x.shape != (field.grid.dim,):
+        raise ValueError(f"start must be a {field.grid.dim}-vector")
+    return trace_trajectories(field, spec, x[None, :], max_steps)[0]

@@ -499,6 +499,102 @@ __global__ void __launch_bounds__(256) peak_kernel(int iters, T* sink) {
 
 using namespace phj;
 
+// Multilinear interpolation of an ext field at arbitrary points (grid.py
+// interpolate_many, :242-261; used by analysis.trace_trajectory): locate in
+// the ghost-extended box with the 1e-9 bounds tolerance (out-of-box points
+// flagged in ood), snapped locals, bit-order corner weights, numpy's sum
+// orders, saturation to sat_value when a nonzero-weight corner is >=
+// sat_threshold.  Periodic axes wrap the coordinate first.
+template <typename T>
+__global__ void points_interp_kernel(phj_grid g, const T* __restrict__ v,
+                                     const double* __restrict__ pts, int64_t n, double thr,
+                                     double sat, int saturate, double* __restrict__ out,
+                                     int8_t* __restrict__ ood) {
+  const int d = g.dim;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t cell[3];
+    double loc[3];
+    bool outside = false;
+    for (int ax = 0; ax < d; ++ax) {
+      double x = pts[i * d + ax];
+      if (g.periodic[ax]) {
+        const double period = __dmul_rn((double)g.shape[ax], g.spacing[ax]);
+        double r = fmod(__dsub_rn(x, g.lo[ax]), period);
+        if (r < 0.0) r = __dadd_rn(r, period);
+        x = __dadd_rn(g.lo[ax], r);
+      }
+      const double t = __ddiv_rn(__dsub_rn(x, g.ext_lo[ax]), g.spacing[ax]);
+      const int64_t nmax = g.ext[ax] - 1;
+      if (!(t >= -1.0e-9) || !(t <= (double)nmax + 1.0e-9)) outside = true;
+      int64_t ce = (int64_t)floor(t);
+      if (ce < 0) ce = 0;
+      if (ce > nmax - 1) ce = nmax - 1;
+      double l = __dsub_rn(t, (double)ce);
+      if (l < 1.0e-12) l = 0.0;
+      if (l > 1.0 - 1.0e-12) l = 1.0;
+      cell[ax] = ce;
+      loc[ax] = l;
+    }
+    ood[i] = outside ? 1 : 0;
+    if (outside) {
+      out[i] = sat;
+      continue;
+    }
+    T terms[8];
+    bool bad = false;
+    const int ncor = 1 << d;
+    for (int k = 0; k < ncor; ++k) {
+      double w = 1.0;
+      int64_t f = 0;
+      for (int ax = 0; ax < d; ++ax) {
+        const int up = (k >> ax) & 1;
+        w = __dmul_rn(w, up ? loc[ax] : __dsub_rn(1.0, loc[ax]));
+        int64_t e = cell[ax] + up;
+        if (g.periodic[ax]) {
+          if (e == 0) e = g.shape[ax];
+          else if (e == g.shape[ax] + 1) e = 1;
+        }
+        f += e * g.strides[ax];
+      }
+      const T cv = v[f];
+      terms[k] = t_mul<T>((T)w, cv);
+      if (w > 0.0 && (double)cv >= thr) bad = true;
+    }
+    T r;
+    if (ncor == 4) {
+      r = t_add<T>(t_add<T>(t_add<T>(terms[0], terms[1]), terms[2]), terms[3]);
+    } else {
+      r = t_add<T>(t_add<T>(t_add<T>(terms[0], terms[1]), t_add<T>(terms[2], terms[3])),
+                   t_add<T>(t_add<T>(terms[4], terms[5]), t_add<T>(terms[6], terms[7])));
+    }
+    out[i] = (saturate && bad) ? sat : (double)r;
+  }
+}
+
+extern "C" int phj_interpolate_points(const phj_grid* g, int32_t dtype, const void* field,
+                                      const double* points, int64_t n, double sat_threshold,
+                                      double sat_value, int32_t saturate, double* out,
+                                      int8_t* ood, void* stream) {
+  if (!g || !field || (n > 0 && (!points || !out || !ood)) || n < 0 || g->dim < 2 ||
+      g->dim > 3) {
+    phj_set_error("phj_interpolate_points: bad arguments");
+    return PHJ_ERR_ARG;
+  }
+  if (n == 0) return PHJ_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nb = grid_blocks(n);
+  if (dtype == PHJ_F32)
+    points_interp_kernel<float><<<nb, 256, 0, s>>>(*g, (const float*)field, points, n,
+                                                   sat_threshold, sat_value, saturate, out, ood);
+  else
+    points_interp_kernel<double><<<nb, 256, 0, s>>>(*g, (const double*)field, points, n,
+                                                    sat_threshold, sat_value, saturate, out, ood);
+  phj_count_launch(1);
+  PHJ_CUDA(cudaGetLastError());
+  return PHJ_OK;
+}
+
 extern "C" int phj_lift(const phj_grid* gc, const phj_grid* gf, int32_t dtype, const void* vc,
                         void* vf, double sat_threshold, double sat_value, int32_t saturate,
                         void* stream) {

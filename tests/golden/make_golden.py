@@ -253,9 +253,48 @@ def main_ao3():
     np.savez_compressed(os.path.join(OUT, "c1_patchy_bc.npz"), **out)
 
 
+def main_traj():
+    """G9: greedy-feedback trajectories (analysis.py:82-139) on committed
+    fields: config-1 fine field (u_gs of c1_fine.npz) from several starts
+    (target reached, trivial start inside the target, step limit) and the
+    fan2d field (zero-speed line: stalled)."""
+    phj = import_reference()
+    out = {}
+    spec1 = phj.ProblemSpec(name="c1", dim=2, box_lo=(-2.0, -2.0), box_hi=(2.0, 2.0),
+                            dynamics=eikonal_dyn,
+                            control_set=phj.discretize_circle(32),
+                            target=phj.TargetSpec.ball((0.0, 0.0), 0.1))
+    g1 = phj.Grid(spec1.box_lo, spec1.box_hi, (101, 101))
+    f1 = phj.NodeField(g1, np.load(os.path.join(OUT, "c1_fine.npz"))["u_gs"])
+    starts = [(1.5, 0.0), (-1.3, 0.9), (0.05, 0.0), (1.9, -1.9), (0.7, 0.23), (-0.4, -1.7)]
+    for i, st in enumerate(starts):
+        tr = phj.trace_trajectory(f1, spec1, st)
+        out[f"c1_start_{i}"] = np.asarray(st, dtype=float)
+        out[f"c1_points_{i}"] = tr.points
+        out[f"c1_term_{i}"] = np.array(tr.termination)
+    tr = phj.trace_trajectory(f1, spec1, (1.5, 1.5), max_steps=3)
+    out["c1_limit_points"] = tr.points
+    out["c1_limit_term"] = np.array(tr.termination)
+    specf = phj.preset("fan2d", controls=16)
+    gf = phj.Grid(specf.box_lo, specf.box_hi, (41, 41))
+    ff = phj.NodeField(gf, np.load(os.path.join(OUT, "fan41.npz"))["u_gs"])
+    for i, st in enumerate([(-0.2, 0.1), (0.6, -0.5)]):
+        tr = phj.trace_trajectory(ff, specf, st)
+        out[f"fan_start_{i}"] = np.asarray(st, dtype=float)
+        out[f"fan_points_{i}"] = tr.points
+        out[f"fan_term_{i}"] = np.array(tr.termination)
+    for k, v in out.items():
+        if "term" in k:
+            print(k, v)
+    np.savez_compressed(os.path.join(OUT, "trajectories.npz"), **out)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "ao3":
         main_ao3()
+    elif len(sys.argv) > 1 and sys.argv[1] == "traj":
+        main_traj()
     else:
         main()
         main_ao3()
+        main_traj()
