@@ -174,6 +174,19 @@ def init_working(plan: StencilPlan, rule: str, dtype: str) -> torch.Tensor:
     return w
 
 
+def coarse_cfg(cfg: SolverConfig) -> SolverConfig:
+    """Solver settings of the coarse stage.  It runs barrier-separated Jacobi
+    sweeps even for asynchronous workloads (with 2 block-local relaxations:
+    same speed on config 2's 513^2 grid): block-Jacobi is schedule
+    independent, so the lifted field, the feedback and hence the patch labels
+    are identical run to run.  Asynchronous coarse values differ between runs
+    at rounding level, enough to flip feedback argmin ties (config 4's
+    symmetric controls) and move patch boundaries."""
+    if cfg.schedule == "async":
+        return dataclasses.replace(cfg, schedule="jacobi", inner_sweeps=2)
+    return cfg
+
+
 def solve_full_internal(plan: StencilPlan, cfg: SolverConfig, work: Optional[torch.Tensor] = None):
     """Single-domain device solve from the init field; (working result, SweepStats)."""
     work = init_working(plan, cfg.rule, cfg.dtype) if work is None else work
@@ -544,7 +557,7 @@ def coarse_solve_and_lift(spec: ProblemSpec, coarse_grid: Grid, fine_grid: Grid,
     require_cuda()
     with stats.phase("coarse"):
         cplan = StencilPlan(coarse_grid, _coarse_spec(spec, coarse_target))
-        vc, cst = solve_full_internal(cplan, cfg)
+        vc, cst = solve_full_internal(cplan, coarse_cfg(cfg))
         stats.merge_counts(cst)
         if cst.warning:
             stats.warnings.append(cst.warning)
@@ -668,7 +681,7 @@ def run_patchy(spec: ProblemSpec, pcfg: PatchyConfig, cfg: Optional[SolverConfig
         fplan, cplan = plans if plans is not None else make_plans(spec, pcfg)
     fine_grid = fplan.grid
     with stats.phase("coarse"):
-        vc, cst = solve_full_internal(cplan, cfg)
+        vc, cst = solve_full_internal(cplan, coarse_cfg(cfg))
         stats.merge_counts(cst)
         if cst.warning:
             stats.warnings.append(cst.warning)
