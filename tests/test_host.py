@@ -187,3 +187,36 @@ def test_lpt_assignment_and_bound():
     assert dist.load_balance_bound(sizes, 4) == pytest.approx(sum(sizes) / (4 * 26098))
     assert dist.load_balance_bound([10] * 8, 8) == 1.0
     assert dist.mine_mask(sizes, 0, 1, "cpu") is None
+
+
+def test_schedule_options_validated_and_resolved():
+    for kw in ({"schedule": "gauss-seidel"}, {"inner_sweeps": 0}, {"activity_tol": -1.0}):
+        with pytest.raises(phj.ConfigurationError):
+            phj.SolverConfig(**kw)
+    c = phj.SolverConfig(rule="kruzkov", schedule="async")
+    assert (c.inner_for(2), c.inner_for(3)) == (8, 3)
+    assert phj.SolverConfig().inner_for(2) == 1  # Jacobi default: plain sweeps
+    assert phj.SolverConfig(inner_sweeps=5).inner_for(3) == 5
+    assert phj.SolverConfig().act_tol == 1e-12
+    assert phj.SolverConfig(rule="kruzkov", dtype="float32").act_tol == 1e-7
+    assert phj.SolverConfig(activity_tol=0.0).act_tol == 0.0
+
+
+def test_coarse_stage_is_deterministic_block_jacobi():
+    from paper_1109_3577_b200 import patchy
+
+    a = patchy.coarse_cfg(phj.SolverConfig(rule="kruzkov", schedule="async", tol=1e-8))
+    assert a.schedule == "jacobi" and a.inner_sweeps == 2 and a.tol == 1e-8
+    j = phj.SolverConfig(rule="kruzkov")
+    assert patchy.coarse_cfg(j) is j
+    # BASELINE workloads: async except config 5 (Jacobi measured faster)
+    assert [configs.CONFIGS[n]().cfg.schedule for n in ("c1", "c2", "c3", "c4", "c5")] == \
+        ["async"] * 4 + ["jacobi"]
+
+
+def test_solve_args_layout_matches_header():
+    # the ctypes mirrors carry the async / transport fields in header order
+    names = [f[0] for f in _lib.SolveArgs._fields_]
+    assert names[-4:] == ["options", "act_tol", "inner_sweeps", "stream"]
+    tnames = [f[0] for f in _lib.TransportArgs._fields_]
+    assert tnames[-4:] == ["options", "inner_sweeps", "phi_dtype", "stream"]
