@@ -33,6 +33,21 @@ namespace phj {
 
 // Optional per-phase cycle accounting (diagnostic builds only, -DPHJ_TIMING).
 #ifdef PHJ_TIMING
+// visit timeline of the asynchronous kernels: visits per 20 us bin since the
+// first visit of the launch (diagnostic builds only)
+__device__ unsigned int g_visit_bins[4096];
+__device__ unsigned long long g_t0;
+__device__ __forceinline__ void timeline_visit() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  unsigned long long t0 = *(volatile unsigned long long*)&g_t0;
+  if (t0 == 0ull) {
+    atomicCAS(&g_t0, 0ull, t);
+    t0 = *(volatile unsigned long long*)&g_t0;
+  }
+  const unsigned long long b = (t - t0) / 20000ull;
+  atomicAdd(&g_visit_bins[b < 4095 ? b : 4095], 1u);
+}
 __device__ unsigned long long g_phase_cycles[12];
 struct PhaseTimer {
   unsigned long long acc[12];
@@ -1617,6 +1632,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         if (nt >= 0) want = atomicOr(&q.state[nt], 1) == 0;
       }
     }
+#ifdef PHJ_TIMING
+    if (lane == 0) timeline_visit();
+#endif
     async_requeue_release(q, cap, n0, blk, want, nt, lane, budget, swept_local);
     tm.mark(6);
   }
@@ -2272,6 +2290,9 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS)
         }
       }
     }
+#ifdef PHJ_TIMING
+    if (lane == 0) timeline_visit();
+#endif
     async_requeue_release(q, cap, n0, blk, want, nt, lane, budget, swept_local);
     tm.mark(6);
   }
@@ -3090,6 +3111,14 @@ static int solve_impl(const phj_solve_args* a) {
 
 #ifdef PHJ_TIMING
 // diagnostic: summed per-warp cycles of the solve kernel phases since the last call
+extern "C" int phj_dbg_timeline(unsigned int* bins) {
+  PHJ_CUDA(cudaMemcpyFromSymbol(bins, g_visit_bins, 4096 * sizeof(unsigned int)));
+  static unsigned int zb[4096];
+  unsigned long long z = 0ull;
+  PHJ_CUDA(cudaMemcpyToSymbol(g_visit_bins, zb, sizeof(zb)));
+  PHJ_CUDA(cudaMemcpyToSymbol(g_t0, &z, sizeof(z)));
+  return PHJ_OK;
+}
 extern "C" int phj_dbg_phase_cycles(unsigned long long* out) {
   PHJ_CUDA(cudaMemcpyFromSymbol(out, g_phase_cycles, 12 * sizeof(unsigned long long)));
   unsigned long long z[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
