@@ -36,6 +36,7 @@ namespace phj {
 // visit timeline of the asynchronous kernels: visits per 20 us bin since the
 // first visit of the launch (diagnostic builds only)
 __device__ unsigned int g_visit_bins[4096];
+__device__ unsigned long long g_visit_kind[4];  // solve visits by outcome: 0 / small / big change
 __device__ unsigned long long g_t0;
 __device__ __forceinline__ void timeline_visit() {
   unsigned long long t;
@@ -1621,6 +1622,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     const int ch = sweep_block<D, T, RULE, COST>(p, s, blk, wtile, wnodes, (T*)p.v[0], s_done,
                                                  s_max, gmax_row, evals, exec, pm, tm, hook);
     ++blocks_done;
+#ifdef PHJ_TIMING
+    if (lane == 0) atomicAdd(&g_visit_kind[ch], 1ull);
+#endif
     // -- re-queue the neighbourhood of a changed block ------------------------
     bool want = false;
     int nt = -1;
@@ -3111,6 +3115,12 @@ static int solve_impl(const phj_solve_args* a) {
 
 #ifdef PHJ_TIMING
 // diagnostic: summed per-warp cycles of the solve kernel phases since the last call
+extern "C" int phj_dbg_visit_kinds(unsigned long long* out) {
+  PHJ_CUDA(cudaMemcpyFromSymbol(out, g_visit_kind, 4 * sizeof(unsigned long long)));
+  unsigned long long z[4] = {0, 0, 0, 0};
+  PHJ_CUDA(cudaMemcpyToSymbol(g_visit_kind, z, sizeof(z)));
+  return PHJ_OK;
+}
 extern "C" int phj_dbg_timeline(unsigned int* bins) {
   PHJ_CUDA(cudaMemcpyFromSymbol(bins, g_visit_bins, 4096 * sizeof(unsigned int)));
   static unsigned int zb[4096];

@@ -55,9 +55,15 @@ bv, bi = patchy.argmax_batched(fplan.gs, phi, R, fplan.grid.n_interior, fplan.de
 mask = patchy.plan_interior_serial(fplan, vf) >= patchy.unreach_threshold(cfg.rule)
 color, _, _, lab = patchy.assemble_internal(fplan.gs, bv, bi, R, mask, fplan.kind,
                                             fplan.grid.n_interior, fplan.device, [])
+kinds = (ctypes.c_ulonglong * 4)()
+lib.phj_dbg_visit_kinds.argtypes = [ctypes.c_void_p]
 for _ in range(2):
     fn(bins)
+    lib.phj_dbg_visit_kinds(kinds)
     patchy.solve_patches_internal(fplan, color, lab, R, w.pcfg, cfg, vf)
     torch.cuda.synchronize()
     fn(bins)
+    lib.phj_dbg_visit_kinds(kinds)
 report("patch_solve_async")
+print(json.dumps({"solve_visits_by_outcome": {"unchanged": kinds[0], "below_threshold": kinds[1],
+                                              "changed": kinds[2]}}))
