@@ -1671,7 +1671,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 // budget ran out.
 __global__ void async_finish_kernel(Workspace ws, int R, const uint8_t* mine,
                                     int32_t* patch_sweeps, int32_t* info) {
-  const int n0 = max(1, ws.counts[0]);
+  // equivalent sweeps: block visits / blocks holding work (take[5], counted
+  // by the async solve's build_list; the transport queues all of them)
+  const int n0 = max(1, ws.take[5] > 0 ? ws.take[5] : ws.counts[0]);
   const unsigned swept = (unsigned)ws.take[4];
   const int eq = (int)((swept + (unsigned)n0 - 1u) / (unsigned)n0);
   const bool aborted = ws.take[3] != 0;
@@ -1690,14 +1692,16 @@ __global__ void build_list_kernel(phj_grid g, TileGrid tg, const int16_t* __rest
                                   const uint8_t* __restrict__ mine, int* flags, int* list,
                                   int* count, int want_movers, const int32_t* __restrict__ fb,
                                   const int8_t* __restrict__ kind, unsigned long long* mask0,
-                                  unsigned long long mask_all) {
+                                  unsigned long long mask_all, const void* __restrict__ vfin = nullptr,
+                                  int vfin_f32 = 0, double finite_below = 0.0,
+                                  int* n_work = nullptr) {
   constexpr int NB = Blk<D>::NB;
   const int lane = threadIdx.x & 31;
   const int blk = blockIdx.x * kWarps + (threadIdx.x >> 5);
   if (blk >= tg.total) return;  // whole warp
   int c[3];
   const bool row_ok = lane_nodes<D>(g, tg, blk, lane, c);
-  bool any = false;
+  bool any = false, work = false;
   if (row_ok) {
     const int64_t f0 = ext_flat<D>(g, c);
     const int64_t s0 = serial_of<D>(g, c);
@@ -1707,10 +1711,33 @@ __global__ void build_list_kernel(phj_grid g, TileGrid tg, const int16_t* __rest
         any |= fb[s0 + r] >= 0 && kind[s0 + r] == 0;
       } else {
         const int l = lab[f0 + r];
-        any |= l >= 0 && (mine == nullptr || mine[l]);
+        bool take = l >= 0 && (mine == nullptr || mine[l]);
+        work |= take;
+        if (take && vfin) {
+          // value solves: a node can only move if some value in its 3^D
+          // neighbourhood is below the unreached level or its own value is
+          // above it (with every corner unreached, every candidate equals
+          // the unreached level exactly) -- cold solves start at the blocks
+          // next to the target instead of every block
+          bool fin = (vfin_f32 ? (double)((const float*)vfin)[f0 + r]
+                               : ((const double*)vfin)[f0 + r]) > finite_below;
+          for (int q = 0; q < (D == 2 ? 9 : 27); ++q) {
+            int64_t off;
+            if (D == 2) off = (int64_t)(q / 3 - 1) * g.strides[0] + (q % 3 - 1);
+            else
+              off = (int64_t)(q / 9 - 1) * g.strides[0] + (int64_t)((q / 3) % 3 - 1) * g.strides[1] +
+                    (q % 3 - 1);
+            const double x = vfin_f32 ? (double)((const float*)vfin)[f0 + r + off]
+                                      : ((const double*)vfin)[f0 + r + off];
+            fin |= x < finite_below;
+          }
+          take = fin;
+        }
+        any |= take;
       }
     }
   }
+  if (n_work && __any_sync(0xffffffffu, work) && lane == 0) atomicAdd(n_work, 1);
   if (__any_sync(0xffffffffu, any) && lane == 0) {
     flags[blk] = 1;
     if (mask0) mask0[blk] = mask_all;
@@ -3075,10 +3102,14 @@ static int solve_impl(const phj_solve_args* a) {
                            stream));
   PHJ_CUDA(cudaMemsetAsync(a->evals, 0, 2 * sizeof(unsigned long long), stream));
   PHJ_CUDA(cudaMemsetAsync(a->info, 0, 4 * sizeof(int32_t), stream));
+  // initial blocks: those that can move from the start field (exact: from
+  // the unreached start a block with no reached value within its 3^D
+  // neighbourhood reproduces itself)
   build_list_kernel<D><<<(p.tg.total + kWarps - 1) / kWarps, kThreads, 0, stream>>>(
       p.g, p.tg, p.lab, p.mine, p.ws.flags[0], p.ws.list[0], p.ws.counts, 0,
       nullptr, nullptr,
-      nullptr, 0ull);
+      nullptr, 0ull, a->v0, sizeof(T) == 4, RULE == PHJ_RULE_KRUZKOV ? 1.0 : 1.0e9,
+      async ? &p.ws.take[5] : nullptr);
   phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   size_t smem = (size_t)align_up(solve_stencil_bytes<D, T>(p.n_classes, p.nc) +
