@@ -270,14 +270,16 @@ def transport_internal(plan: StencilPlan, fb_int: torch.Tensor, parts_flat: Sequ
     e0.record()
     _lib.check(lib.phj_transport(ctypes_ref(a)), "phj_transport")
     e1.record()
-    ih = info.cpu().numpy()
+    # one device->host copy for the counters (exact in fp64)
+    pack = torch.cat([info.double(), csw.double(), upd.double()]).cpu().numpy()
+    ih = pack[:4].astype(np.int64)
     phi = phi1 if int(ih[1]) == 1 else phi0
     from .solver import active_blocks_per_sweep
 
     TRANSPORT_DIAG["kernel_ms"] = e0.elapsed_time(e1)
     if _lib.DIAG:
         TRANSPORT_DIAG["block_counts"] = active_blocks_per_sweep(plan, ws, max_sweeps, int(ih[0]))
-    return phi, R, [int(x) for x in csw.cpu().tolist()], int(upd.item())
+    return phi, R, [int(x) for x in pack[4:4 + R]], int(pack[4 + R])
 
 
 def _transport_and_argmax(fplan: StencilPlan, fb: torch.Tensor, parts, color_tol: float,

@@ -398,7 +398,7 @@ def init_value_field(grid: Grid, spec: ProblemSpec, kind=None) -> NodeField:
 class DeviceSolveResult:
     values: torch.Tensor           # working field holding the result (internal)
     patch_sweeps: np.ndarray       # per patch, negative = not converged
-    maxch: np.ndarray              # [max_sweeps, R]
+    last_change: np.ndarray        # [R] max change of each patch's last sweep (Jacobi)
     evals: int
     info: np.ndarray
     device_ms: float = 0.0
@@ -458,11 +458,18 @@ def device_solve(plan: StencilPlan, work: torch.Tensor, lab: torch.Tensor, fmask
     e0.record()
     _lib.check(lib.phj_solve(ctypes_ref(a)), "phj_solve")
     e1.record()
-    info_h = info.cpu().numpy()
+    # one device->host copy (one synchronisation) for every counter: info,
+    # per-patch sweeps, evaluation counters and each patch's last max change
+    # (exact in fp64: all counts are < 2^53)
+    last = mc.view(max_sweeps, n_patches)[
+        (ps.abs().long() - 1).clamp(0, max_sweeps - 1), torch.arange(n_patches, device=dev)]
+    pack = torch.cat([info.double(), ps.double(), ev.double(), last]).cpu().numpy()
+    info_h = pack[:4].astype(np.int64)
+    ps_h = pack[4:4 + n_patches].astype(np.int32)
+    ev_h = pack[4 + n_patches:6 + n_patches].astype(np.int64)
     res = v1 if int(info_h[1]) == 1 else work
-    ev_h = ev.cpu().numpy()
-    out = DeviceSolveResult(res, ps.cpu().numpy(), mc.view(max_sweeps, n_patches).cpu().numpy(),
-                            int(ev_h[0]), info_h, executed=int(ev_h[1]))
+    out = DeviceSolveResult(res, ps_h, pack[6 + n_patches:].copy(), int(ev_h[0]), info_h,
+                            executed=int(ev_h[1]))
     out.device_ms = e0.elapsed_time(e1)
     if _lib.DIAG:
         out.block_counts = active_blocks_per_sweep(plan, ws, max_sweeps, int(info_h[0]))
@@ -488,8 +495,7 @@ def stats_for_patch(res: DeviceSolveResult, p: int, n_nodes: int, n_adm: int, to
     st.sweeps = abs(s)
     st.converged = s > 0
     # asynchronous solves report equivalent sweeps and keep no per-sweep history
-    st.max_change = (float(res.maxch[st.sweeps - 1, p])
-                     if 0 < st.sweeps <= res.maxch.shape[0] else 0.0)
+    st.max_change = float(res.last_change[p]) if st.sweeps > 0 else 0.0
     st.node_relaxations = n_nodes * st.sweeps
     st.candidate_evals = (n_nodes * n_adm if cands_per_sweep is None
                           else int(cands_per_sweep)) * st.sweeps
