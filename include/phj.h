@@ -216,6 +216,13 @@ typedef struct phj_transport_args {
   int32_t inner_sweeps; /* async: relaxations of a colour per block visit (>= 1) */
   int32_t phi_dtype;    /* PHJ_F64 (0) or PHJ_F32: storage of the colour fields
                            (accumulation is fp64 either way) */
+  /* optional seeding (n_colors <= 64): the part nodes (internal ext flat
+   * index, colour) -- only blocks next to a part of colour j start active for
+   * colour j (exact: elsewhere phi_j = 0 on every foot corner); NULL = every
+   * mover block starts active for every colour */
+  const int64_t* seed_flat;
+  const int32_t* seed_col;
+  int64_t n_seed;
   void* stream;
 } phj_transport_args;
 

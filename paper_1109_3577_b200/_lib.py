@@ -70,7 +70,7 @@ class TransportArgs(ctypes.Structure):
                 ("kind", P), ("ent_scratch", P), ("n_colors", I32), ("tol", D), ("act_eps", D),
                 ("max_sweeps", I32), ("workspace", P), ("maxch_hist", P), ("color_sweeps", P),
                 ("info", P), ("updates", P), ("options", I32), ("inner_sweeps", I32), ("phi_dtype", I32),
-                ("stream", P)]
+                ("seed_flat", P), ("seed_col", P), ("n_seed", ctypes.c_int64), ("stream", P)]
 
 
 class Shapes(ctypes.Structure):

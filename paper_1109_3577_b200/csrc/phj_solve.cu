@@ -1685,6 +1685,34 @@ __global__ void async_finish_kernel(Workspace ws, int R, const uint8_t* mine,
   }
 }
 
+// Colour transport seeding: OR colour j into the masks of the 3^D block
+// neighbourhood of every node of part j.  A mover whose 3^D neighbourhood
+// holds no part-j node starts at phi_j = 0 with every foot corner at 0, so
+// only seeded (block, colour) pairs can change in the first sweep / visit.
+template <int D>
+__global__ void transport_seed_kernel(phj_grid g, TileGrid tg, const int64_t* __restrict__ flat,
+                                      const int32_t* __restrict__ col, int64_t n,
+                                      unsigned long long* __restrict__ mask) {
+  using B = Blk<D>;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t f = flat[i];
+    int c[3];
+    for (int ax = 0; ax < D; ++ax) {
+      c[ax] = (int)(f / g.strides[ax]) - 1;
+      f -= (int64_t)(c[ax] + 1) * g.strides[ax];
+    }
+    int t;
+    if (D == 2) t = (c[0] / B::BY) * tg.n[1] + c[1] / B::BX;
+    else t = (c[0] * tg.n[1] + c[1] / B::BY) * tg.n[2] + c[2] / B::BX;
+    const unsigned long long bit = 1ull << col[i];
+    for (int q = 0; q < (D == 2 ? 9 : 27); ++q) {
+      const int nb = neighbour_block<D>(tg, g, t, q);
+      if (nb >= 0) atomicOr(&mask[nb], bit);
+    }
+  }
+}
+
 // Initial active block list: every block holding a node to sweep (solve:
 // label >= 0 of a mine patch; transport: a mover).  One warp per block.
 template <int D>
@@ -1694,7 +1722,7 @@ __global__ void build_list_kernel(phj_grid g, TileGrid tg, const int16_t* __rest
                                   const int8_t* __restrict__ kind, unsigned long long* mask0,
                                   unsigned long long mask_all, const void* __restrict__ vfin = nullptr,
                                   int vfin_f32 = 0, double finite_below = 0.0,
-                                  int* n_work = nullptr) {
+                                  int* n_work = nullptr, int seeded = 0) {
   constexpr int NB = Blk<D>::NB;
   const int lane = threadIdx.x & 31;
   const int blk = blockIdx.x * kWarps + (threadIdx.x >> 5);
@@ -1708,7 +1736,9 @@ __global__ void build_list_kernel(phj_grid g, TileGrid tg, const int16_t* __rest
     for (int r = 0; r < NB; ++r) {
       if (c[D - 1] + r >= g.shape[D - 1]) break;
       if (want_movers) {
-        any |= fb[s0 + r] >= 0 && kind[s0 + r] == 0;
+        const bool mv = fb[s0 + r] >= 0 && kind[s0 + r] == 0;
+        any |= mv;
+        work |= mv;
       } else {
         const int l = lab[f0 + r];
         bool take = l >= 0 && (mine == nullptr || mine[l]);
@@ -1738,9 +1768,11 @@ __global__ void build_list_kernel(phj_grid g, TileGrid tg, const int16_t* __rest
     }
   }
   if (n_work && __any_sync(0xffffffffu, work) && lane == 0) atomicAdd(n_work, 1);
+  // seeded transport: only blocks whose colour mask was seeded next to a part
+  if (seeded) any = any && mask0[blk] != 0ull;
   if (__any_sync(0xffffffffu, any) && lane == 0) {
     flags[blk] = 1;
-    if (mask0) mask0[blk] = mask_all;
+    if (mask0 && !seeded) mask0[blk] = mask_all;
     list[atomicAdd(count, 1)] = blk;
   }
 }
@@ -3269,10 +3301,19 @@ static int transport_impl(const phj_transport_args* a) {
                                             p.kind, a->ent_scratch);
     phj_count_launch(1);
   }
+  const bool seeded = a->seed_flat && a->n_seed > 0 && p.R <= 64;
+  if (seeded) {
+    const int nb = (int)std::min<int64_t>((a->n_seed + 255) / 256, 4 * phj_num_sms());
+    transport_seed_kernel<D><<<std::max(nb, 1), 256, 0, stream>>>(p.g, p.tg, a->seed_flat,
+                                                                  a->seed_col, a->n_seed,
+                                                                  p.ws.cmask[0]);
+    phj_count_launch(1);
+  }
   build_list_kernel<D><<<(p.tg.total + kWarps - 1) / kWarps, kThreads, 0, stream>>>(
       p.g, p.tg, nullptr, nullptr, p.ws.flags[0], p.ws.list[0], p.ws.counts,
       1, p.fb, p.kind,
-      p.ws.cmask[0], p.R >= 64 ? ~0ull : ((1ull << p.R) - 1ull));
+      p.ws.cmask[0], p.R >= 64 ? ~0ull : ((1ull << p.R) - 1ull), nullptr, 0, 0.0,
+      async ? &p.ws.take[5] : nullptr, seeded ? 1 : 0);
   phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   const int nent = p.n_classes * p.nc;

@@ -229,9 +229,10 @@ def transport_internal(plan: StencilPlan, fb_int: torch.Tensor, parts_flat: Sequ
     phi0 = torch.zeros((R,) + plan.int_ext, dtype=phi_dtype, device=plan.device)
     # every colour's part in one scatter (one index set, one launch)
     sizes = [int(pf.numel()) for pf in parts_flat]
-    col = torch.repeat_interleave(torch.arange(R, device=plan.device),
+    col = torch.repeat_interleave(torch.arange(R, device=plan.device, dtype=torch.int32),
                                   torch.as_tensor(sizes, device=plan.device))
-    phi0.view(R, -1)[col, torch.cat([pf.view(-1) for pf in parts_flat])] = 1.0
+    seed_flat = torch.cat([pf.view(-1) for pf in parts_flat]).to(torch.int64).contiguous()
+    phi0.view(R, -1)[col.long(), seed_flat] = 1.0
     if any(plan.gs.periodic[i] for i in range(plan.grid.dim)):
         for j in range(R):
             _sync_periodic(plan, phi0[j])
@@ -258,6 +259,11 @@ def transport_internal(plan: StencilPlan, fb_int: torch.Tensor, parts_flat: Sequ
     a.options = _lib.TRANSPORT_ASYNC if asyn else 0
     a.inner_sweeps = TRANSPORT_INNER[plan.grid.dim]
     a.phi_dtype = _lib.F32 if phi_dtype == torch.float32 else _lib.F64
+    # only blocks next to a part start active (exact; the library ignores the
+    # seeds beyond 64 colours)
+    a.seed_flat = _lib.ptr(seed_flat)
+    a.seed_col = _lib.ptr(col)
+    a.n_seed = int(seed_flat.numel())
     a.max_sweeps = max_sweeps
     a.workspace = _lib.ptr(ws)
     a.maxch_hist = _lib.ptr(mc)

@@ -219,4 +219,5 @@ def test_solve_args_layout_matches_header():
     names = [f[0] for f in _lib.SolveArgs._fields_]
     assert names[-4:] == ["options", "act_tol", "inner_sweeps", "stream"]
     tnames = [f[0] for f in _lib.TransportArgs._fields_]
-    assert tnames[-4:] == ["options", "inner_sweeps", "phi_dtype", "stream"]
+    assert tnames[-7:] == ["options", "inner_sweeps", "phi_dtype", "seed_flat", "seed_col",
+                           "n_seed", "stream"]
