@@ -18,13 +18,14 @@ import paper_1109_3577_b200 as phj  # noqa: E402
 from paper_1109_3577_b200 import configs  # noqa: E402
 
 name, n = sys.argv[1], int(sys.argv[2])
+KW = dict(nxy=n, nth=16, cxy=(n - 1) // 4 + 1, cth=8) if name == "c4" else dict(n=n)
 torch.cuda.set_device(0)
-w = configs.CONFIGS[name](n=n)
+w = configs.CONFIGS[name](**KW)
 single = phj.run_patchy(w.spec, w.pcfg, w.cfg).value.values.clone()
 single_col = None
 td.init_process_group("gloo")
 rank = td.get_rank()
-w = configs.CONFIGS[name](n=n)
+w = configs.CONFIGS[name](**KW)
 res = phj.run_patchy(w.spec, w.pcfg, w.cfg)
 v = res.value.values
 fin = (single < 1e8) & (v < 1e8)
