@@ -158,6 +158,40 @@ def _weights_for(disp: np.ndarray):
     return octant, w, nz
 
 
+def _weights_all(disp: np.ndarray):
+    """_weights_for over many displacements at once ([n, d] -> octant [n],
+    weights [n, 2^d], nonzero masks [n]); the same IEEE operations in the
+    same order, so the results are bit-identical (checked in the tests)."""
+    disp = np.asarray(disp, dtype=float)
+    n, d = disp.shape
+    x = np.clip(disp, -1.0, 1.0)
+    up_side = x >= 0.0
+    octant = (up_side.astype(np.int64) << np.arange(d)).sum(axis=1)
+    t = np.where(up_side, x, x + 1.0)
+    t = np.where(t < SNAP_TOL, 0.0, t)
+    t = np.where(t > 1.0 - SNAP_TOL, 1.0, t)
+    nk = 2 ** d
+    w = np.ones((n, nk))
+    nz = np.zeros(n, dtype=np.int64)
+    for k in range(nk):
+        pos = np.zeros(n, dtype=np.int64)
+        for ax in range(d):
+            up = (k >> ax) & 1
+            w[:, k] = w[:, k] * (t[:, ax] if up else 1.0 - t[:, ax])
+            off = np.where((octant >> ax) & 1, 0, -1) + up
+            pos = pos * 3 + (off + 1)
+        nz |= np.where(w[:, k] != 0.0, np.int64(1) << pos, 0)
+    # sequential left-to-right sum of the weights before the last nonzero
+    # one, which is replaced by 1 - sum (see _weights_for)
+    nzw = w != 0.0
+    last = nk - 1 - np.argmax(nzw[:, ::-1], axis=1)
+    ssum = np.zeros(n)
+    for k in range(nk):
+        ssum = np.where(k < last, ssum + w[:, k], ssum)
+    w[np.arange(n), last] = 1.0 - ssum
+    return octant, w, nz
+
+
 def unroll(dim: int) -> int:
     """Entries per kernel inner-loop iteration (PHJ_UNROLL of the built
     library, include/phj.h)."""
@@ -179,11 +213,10 @@ def build_stencil(disp: np.ndarray, cost: Optional[np.ndarray], admissible: np.n
     n_real = 0
     for cls in range(ncls):
         info = []
-        for c in range(nc):
-            if not admissible[cls, c]:
-                continue
-            o, w, nz = _weights_for(disp[cls, c])
-            info.append((o, c, w, nz))
+        adm = np.nonzero(admissible[cls])[0]
+        if adm.size:
+            oa, wa, nza = _weights_all(disp[cls, adm])
+            info = [(int(oa[i]), int(c), wa[i], int(nza[i])) for i, c in enumerate(adm)]
         info.sort(key=lambda e: (e[0], e[1]))  # octant, then original order
         groups = []
         for o in range(noct):

@@ -221,3 +221,15 @@ def test_solve_args_layout_matches_header():
     tnames = [f[0] for f in _lib.TransportArgs._fields_]
     assert tnames[-7:] == ["options", "inner_sweeps", "phi_dtype", "seed_flat", "seed_col",
                            "n_seed", "stream"]
+
+
+def test_vectorised_stencil_weights_bit_identical():
+    rng = np.random.default_rng(3577)
+    for d in (2, 3):
+        disp = rng.uniform(-1.0, 1.0, size=(300, d))
+        disp[::7] = np.round(disp[::7])      # axis-aligned feet (snapped weights)
+        disp[::11, 0] = 1.0e-13              # below the snap tolerance
+        o, w, nz = dynamics._weights_all(disp)
+        for i in range(disp.shape[0]):
+            o1, w1, nz1 = dynamics._weights_for(disp[i])
+            assert o1 == o[i] and nz1 == nz[i] and np.array_equal(w1, w[i])
