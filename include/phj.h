@@ -236,9 +236,11 @@ typedef struct phj_transport_args {
  * lowest colour on ties, patchy.py:251-256) */
 int phj_argmax_colors(const phj_grid* g, const double* phi, int32_t n_colors, double* best_val,
                       int32_t* best_idx, void* stream);
-/* the same over colour fields stored in phi_dtype (PHJ_F64 / PHJ_F32) */
+/* the same over colour fields stored in phi_dtype (PHJ_F64 / PHJ_F32);
+ * quantum > 0 compares floor(phi / quantum) * quantum instead (colours within
+ * rounding noise tie exactly; lowest colour wins), 0 = strict argmax */
 int phj_argmax_colors_t(const phj_grid* g, const void* phi, int32_t phi_dtype, int32_t n_colors,
-                        double* best_val, int32_t* best_idx, void* stream);
+                        double quantum, double* best_val, int32_t* best_idx, void* stream);
 int phj_transport(const phj_transport_args* a);
 
 /* Saturating multilinear lift of a coarse ext field to fine ext interior. */

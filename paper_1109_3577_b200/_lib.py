@@ -129,7 +129,7 @@ def load() -> ctypes.CDLL:
         "phj_lift": (ctypes.c_int, [P, P, I32, P, P, D, D, I32, P]),
         "phj_argmax_update": (ctypes.c_int, [P, P, I32, P, P, P]),
         "phj_argmax_colors": (ctypes.c_int, [P, P, I32, P, P, P]),
-        "phj_argmax_colors_t": (ctypes.c_int, [P, P, I32, I32, P, P, P]),
+        "phj_argmax_colors_t": (ctypes.c_int, [P, P, I32, I32, D, P, P, P]),
         "phj_count_labels": (ctypes.c_int, [P, ctypes.c_int64, I32, P, P]),
         "phj_interpolate_points": (ctypes.c_int, [P, I32, P, P, ctypes.c_int64, D, D, I32, P, P,
                                                   P]),

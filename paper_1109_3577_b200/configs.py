@@ -117,8 +117,11 @@ def c4(rule: str = "kruzkov", dtype: str = "float64", schedule: str = "async", n
     pcfg = PatchyConfig(n_patches=16, coarse_nodes=(cxy, cxy, cth), fine_nodes=(nxy, nxy, nth),
                         parts=theta_slabs(16))
     return Workload("c4", f"3D Dubins {nxy}x{nxy}x{nth}, 5 controls, 16 patches", spec, pcfg,
-                    SolverConfig(schedule=schedule, tol=1e-8 if dtype == "float64" else 1e-6, rule=rule,
-                                 dtype=dtype), (nxy, nxy, nth), (cxy, cxy, cth))
+                    SolverConfig(schedule=schedule, tol=1e-8 if dtype == "float64" else 1e-6,
+                                 rule=rule, dtype=dtype,
+                                 # 4 block-local relaxations: measured best here (63 vs 70 ms)
+                                 inner_sweeps=4 if schedule == "async" else None),
+                    (nxy, nxy, nth), (cxy, cxy, cth))
 
 
 def c5(rule: str = "kruzkov", dtype: str = "float32", schedule: str = "jacobi", n: int = 513,

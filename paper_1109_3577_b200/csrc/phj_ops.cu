@@ -152,7 +152,7 @@ __global__ void argmax_kernel(phj_grid g, const double* __restrict__ phi, int j,
 }
 
 template <typename PT>
-__global__ void argmax_colors_kernel(phj_grid g, const PT* __restrict__ phi, int R,
+__global__ void argmax_colors_kernel(phj_grid g, const PT* __restrict__ phi, int R, double quantum,
                                      double* __restrict__ best_val, int32_t* __restrict__ best_idx) {
   const int64_t N = n_interior(g);
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < N;
@@ -164,7 +164,13 @@ __global__ void argmax_colors_kernel(phj_grid g, const PT* __restrict__ phi, int
     double bv = 0.0;
     int32_t bi = 0;
     for (int j = 0; j < R; ++j) {
-      const double x = (double)v[j * plane];
+      double x = (double)v[j * plane];
+      // quantum > 0: masses compared on a grid of that step (floor), so
+      // colours within rounding noise of each other tie exactly and the
+      // lowest colour wins -- run-to-run stable labels for the
+      // asynchronous transport, whose fields differ between runs at
+      // rounding level
+      if (quantum > 0.0) x = floor(x / quantum) * quantum;
       if (x > bv) {
         bv = x;
         bi = j;
@@ -627,19 +633,19 @@ extern "C" int phj_argmax_update(const phj_grid* g, const double* phi, int32_t j
 }
 
 extern "C" int phj_argmax_colors_t(const phj_grid* g, const void* phi, int32_t phi_dtype,
-                                   int32_t n_colors, double* best_val, int32_t* best_idx,
-                                   void* stream) {
-  if (!g || !phi || !best_val || !best_idx || n_colors < 1 ||
+                                   int32_t n_colors, double quantum, double* best_val,
+                                   int32_t* best_idx, void* stream) {
+  if (!g || !phi || !best_val || !best_idx || n_colors < 1 || !(quantum >= 0.0) ||
       (phi_dtype != PHJ_F64 && phi_dtype != PHJ_F32)) {
     phj_set_error("phj_argmax_colors: bad arguments");
     return PHJ_ERR_ARG;
   }
   if (phi_dtype == PHJ_F32)
     argmax_colors_kernel<float><<<grid_blocks(n_interior(*g)), 256, 0, (cudaStream_t)stream>>>(
-        *g, (const float*)phi, n_colors, best_val, best_idx);
+        *g, (const float*)phi, n_colors, quantum, best_val, best_idx);
   else
     argmax_colors_kernel<double><<<grid_blocks(n_interior(*g)), 256, 0, (cudaStream_t)stream>>>(
-        *g, (const double*)phi, n_colors, best_val, best_idx);
+        *g, (const double*)phi, n_colors, quantum, best_val, best_idx);
   phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   return PHJ_OK;
@@ -647,7 +653,7 @@ extern "C" int phj_argmax_colors_t(const phj_grid* g, const void* phi, int32_t p
 
 extern "C" int phj_argmax_colors(const phj_grid* g, const double* phi, int32_t n_colors,
                                  double* best_val, int32_t* best_idx, void* stream) {
-  return phj_argmax_colors_t(g, phi, PHJ_F64, n_colors, best_val, best_idx, stream);
+  return phj_argmax_colors_t(g, phi, PHJ_F64, n_colors, 0.0, best_val, best_idx, stream);
 }
 
 extern "C" int phj_assemble_codes(const phj_grid* g, const double* best_val,

@@ -346,13 +346,14 @@ def argmax_stream(gs, phis, n_serial: int, device):
     return best_val, best_idx, n_colors
 
 
-def argmax_batched(gs, phi: torch.Tensor, R: int, n_serial: int, device):
+def argmax_batched(gs, phi: torch.Tensor, R: int, n_serial: int, device, quantum: float = 0.0):
     lib = _lib.load()
     best_val = torch.empty(n_serial, dtype=torch.float64, device=device)
     best_idx = torch.empty(n_serial, dtype=torch.int32, device=device)
     pdt = _lib.F32 if phi.dtype == torch.float32 else _lib.F64
-    _lib.check(lib.phj_argmax_colors_t(ctypes_ref(gs), _lib.ptr(phi), pdt, R, _lib.ptr(best_val),
-                                       _lib.ptr(best_idx), _lib.stream_handle()), "argmax")
+    _lib.check(lib.phj_argmax_colors_t(ctypes_ref(gs), _lib.ptr(phi), pdt, R, float(quantum),
+                                       _lib.ptr(best_val), _lib.ptr(best_idx),
+                                       _lib.stream_handle()), "argmax")
     return best_val, best_idx
 
 

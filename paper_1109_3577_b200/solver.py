@@ -60,7 +60,7 @@ class SolverConfig:
     #: activity_tol)
     schedule: str = "jacobi"
     #: block-local relaxations per block visit (None: 1 for "jacobi"; for
-    #: "async" 8 in 2D, 3 in 3D -- measured best)
+    #: "async" 7 in 2D, 3 in 3D -- measured best)
     inner_sweeps: Optional[int] = None
 
     def __post_init__(self):
@@ -96,7 +96,7 @@ class SolverConfig:
     def inner_for(self, dim: int) -> int:
         if self.inner_sweeps is not None:
             return int(self.inner_sweeps)
-        return 1 if self.schedule == "jacobi" else (8 if dim == 2 else 3)
+        return 1 if self.schedule == "jacobi" else (7 if dim == 2 else 3)
 
     def sweep_limit(self, grid: Grid) -> int:
         return self.max_sweeps if self.max_sweeps is not None else 10 * max(grid.shape)

@@ -194,7 +194,7 @@ def test_schedule_options_validated_and_resolved():
         with pytest.raises(phj.ConfigurationError):
             phj.SolverConfig(**kw)
     c = phj.SolverConfig(rule="kruzkov", schedule="async")
-    assert (c.inner_for(2), c.inner_for(3)) == (8, 3)
+    assert (c.inner_for(2), c.inner_for(3)) == (7, 3)
     assert phj.SolverConfig().inner_for(2) == 1  # Jacobi default: plain sweeps
     assert phj.SolverConfig(inner_sweeps=5).inner_for(3) == 5
     assert phj.SolverConfig().act_tol == 1e-12
