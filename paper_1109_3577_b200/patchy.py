@@ -47,7 +47,10 @@ TRANSPORT_DIAG: dict = {}
 TRANSPORT_ACT_FRAC = 1.0e-3
 #: asynchronous transport: a colour change re-queues the neighbourhood only
 #: above this fraction of color_tol; relaxations per block visit by dimension
-TRANSPORT_ASYNC_FRAC = 1.0e-3
+# 1e-4: labels run-to-run identical at full config-2 size (1e-3: 1-3 of 4.2 M
+# labels differed between runs, the dropped sub-threshold changes depending
+# on visit order; profiles/r1d_c2_label_reproducibility.txt), +0.4 ms
+TRANSPORT_ASYNC_FRAC = 1.0e-4
 #: asynchronous transport in 3D too (off: slower than the Jacobi kernel there,
 #: DESIGN.md §3.1b); module attributes so experiments can flip them
 TRANSPORT_ASYNC_3D = False
