@@ -5,19 +5,24 @@
 
 One step = one full patchy solve of the workload (coarse solve -> lift ->
 feedback -> colour transport -> assembly -> patch solves) to convergence,
-i.e. the time-to-converge.  The workloads use the asynchronous device
-schedule: the value solves stop when no node can change by
-more than activity_tol (1e-12 in time units) -- a tighter stop than the
-reference's per-sweep max change <= tol (1e-8).  Units = candidate evaluations (node x control x sweep,
-``candidate_evals`` of _kernels.py:76) the value sweeps actually performed
-(coarse + patch solves); the reference's dense count is reported beside it.
+i.e. the time-to-converge (``time_to_converge_ms``, the figure to compare
+across schedules).  The workloads use the asynchronous device schedule
+(DESIGN.md §3.1c): the patch solves stop when no node can change by more
+than activity_tol (1e-12 in time units) -- a tighter stop than the
+reference's per-sweep max change <= tol (1e-8); the coarse stage is
+deterministic block-Jacobi.  Units = candidate evaluations (node x control
+x sweep, ``candidate_evals`` of _kernels.py:76) the value solves actually
+performed (coarse + patch solves) -- a work rate, so a schedule that wastes
+fewer evaluations can score lower while converging sooner; the reference's
+dense count is reported beside it.
 
 * ``value``  -- device-resident: plans (stencils, node kinds, coefficients)
   built before timing, each step timed with CUDA events, L2 flushed between
   steps (256 MiB write, untimed).
 * ``e2e``    -- through the public API ``run_patchy(spec, pcfg, cfg)`` from
   host inputs (problem description -> device tables: H2D) to the value field
-  on the host (D2H), all inside the timed region.
+  in a pinned host buffer (D2H), all inside the timed region; wall clock over
+  max(5, min(K, 10)) steps after W untimed calls.
 * ``roofline`` -- dominant kernel = the fine patch solve launch; algorithmic
   FP64 (FP32) flops per candidate 2*2^d + 1 x candidates the
   kernel executed (after exact octant pruning) / its CUDA-event duration,
