@@ -221,9 +221,15 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
     if world > 1:
-        td.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # PHJ_DIST_BACKEND=gloo: two ranks on one GPU for functional checks of
+        # the multi-rank bench path (NCCL needs one device per rank)
+        backend = os.environ.get("PHJ_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            td.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            td.init_process_group(backend)
     lib = _lib.load()
     w = _workload(args)
     spec, pcfg, cfg = w.spec, w.pcfg, w.cfg
