@@ -25,7 +25,8 @@ import torch
 
 from . import _lib, dist
 from .grid import SENTINEL, ConfigurationError, Grid, NodeField, require_cuda
-from .problems import ProblemSpec, TargetSpec, partition_target
+from .problems import (ProblemSpec, TargetSpec, _check_parts, device_partition_codes,
+                       partition_target)
 from .runtime import ExecutionStrategy, RunStats
 from .solver import (DIRICHLET, KIND_FREE, KIND_OBSTACLE, KIND_TARGET, STATE_CONSTRAINT,
                      FeedbackField, SolverConfig, StencilPlan, SweepStats, ctypes_ref,
@@ -777,7 +778,19 @@ def _resolve_parts(pcfg: PatchyConfig, spec: ProblemSpec, grid: Grid, plan=None)
     serials = None
     if plan is not None:
         kind_user = plan.serial_to_user(plan.kind)
-        serials = torch.nonzero(kind_user == KIND_TARGET).view(-1).cpu().numpy()
+        ser_t = torch.nonzero(kind_user == KIND_TARGET).view(-1)
+        dev = device_partition_codes(pcfg.parts, spec.target, grid, ser_t)
+        if dev is not None:
+            # built-in partitions on the device: one copy of (serials, codes)
+            n_parts, code = dev
+            both = torch.stack([ser_t.to(torch.int64), code]).cpu().numpy()
+            parts = [both[0][both[1] == j] for j in range(n_parts)]
+            _check_parts(parts, n_parts)
+            if cache is None:
+                plan._parts_cache = cache = {}
+            cache[key] = parts
+            return parts
+        serials = ser_t.cpu().numpy()
     if pcfg.parts is None:
         parts = partition_target(spec.target, grid, pcfg.n_patches, serials=serials)
     else:

@@ -233,3 +233,21 @@ def test_vectorised_stencil_weights_bit_identical():
         for i in range(disp.shape[0]):
             o1, w1, nz1 = dynamics._weights_for(disp[i])
             assert o1 == o[i] and nz1 == nz[i] and np.array_equal(w1, w[i])
+
+
+def test_device_partition_codes_match_numpy_partitions():
+    # the built-in partitions computed with torch ops (device path of
+    # patchy._resolve_parts; run here on CPU tensors) equal the numpy forms
+    import torch
+
+    for w in (configs.c2(n=257), configs.c3(n=65)):
+        g = w.spec.make_grid(w.pcfg.fine_nodes)
+        ser = np.nonzero(w.spec.target.contains(g.interior_points()))[0]
+        want = w.pcfg.parts(w.spec.target, g, serials=ser)
+        n, code = problems.device_partition_codes(w.pcfg.parts, w.spec.target, g,
+                                                  torch.as_tensor(ser))
+        code = code.numpy()
+        got = [ser[code == j] for j in range(n)]
+        assert len(got) == len(want)
+        for a, b in zip(got, want):
+            assert np.array_equal(a, b)
