@@ -175,11 +175,19 @@ class StencilPlan:
         self.int_shape = tuple(grid.shape[p] for p in self.perm)
         self.int_ext = tuple(grid.ext_shape[p] for p in self.perm)
         dev = self.device
-        self.d_oct = torch.as_tensor(st.oct_start.ravel(), dtype=torch.int32, device=dev)
-        self.d_ctrl = torch.as_tensor(st.ctrl, dtype=torch.int32, device=dev)
-        self.d_nz = torch.as_tensor(st.nzmask.view(np.int32), device=dev)
-        self.d_w = torch.as_tensor(st.weights.ravel(), dtype=torch.float64, device=dev)
-        self.d_cost = torch.as_tensor(st.cost, dtype=torch.float64, device=dev)
+        # the stencil tables in ONE host->device copy (fp64 parts first: aligned)
+        parts = [np.ascontiguousarray(st.weights.ravel(), dtype=np.float64),
+                 np.ascontiguousarray(st.cost, dtype=np.float64),
+                 np.ascontiguousarray(st.oct_start.ravel(), dtype=np.int32),
+                 np.ascontiguousarray(st.ctrl, dtype=np.int32),
+                 np.ascontiguousarray(st.nzmask.view(np.int32))]
+        blob = torch.as_tensor(np.concatenate([q.view(np.uint8) for q in parts])).to(dev)
+        views, off = [], 0
+        for q, tdt in zip(parts, (torch.float64, torch.float64, torch.int32, torch.int32,
+                                  torch.int32)):
+            views.append(blob[off:off + q.nbytes].view(tdt))
+            off += q.nbytes
+        self.d_w, self.d_cost, self.d_oct, self.d_ctrl, self.d_nz = views
         self.n_adm = int(st.n_real)
         self.kind = self._classify(lib)
         # hard base = ghost + obstacle (solver.py:111-126); periodic ghosts copy
