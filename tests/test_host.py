@@ -209,9 +209,9 @@ def test_coarse_stage_is_deterministic_block_jacobi():
     assert a.schedule == "jacobi" and a.inner_sweeps == 2 and a.tol == 1e-8
     j = phj.SolverConfig(rule="kruzkov")
     assert patchy.coarse_cfg(j) is j
-    # BASELINE workloads: async except config 5 (Jacobi measured faster)
+    # BASELINE workloads: all asynchronous
     assert [configs.CONFIGS[n]().cfg.schedule for n in ("c1", "c2", "c3", "c4", "c5")] == \
-        ["async"] * 4 + ["jacobi"]
+        ["async"] * 5
 
 
 def test_solve_args_layout_matches_header():
