@@ -118,9 +118,12 @@ typedef struct phj_solve_args {
   void* workspace;            /* phj_solve_workspace_bytes() bytes */
   int32_t* patch_sweeps;      /* out [n_patches]: sweeps to converge, -(cap) if not */
   double* maxch_hist;         /* out [max_sweeps * n_patches], may be NULL */
-  unsigned long long* evals;  /* out [2]: [0] candidate evaluations of the swept nodes
-                                 (nodes x admissible controls), [1] stencil-entry
-                                 evaluations executed (incl. padding, after pruning) */
+  unsigned long long* evals;  /* out [3]: [0] candidate evaluations of the swept nodes
+                                 (nodes x admissible controls, per block-local
+                                 relaxation), [1] stencil-entry evaluations executed
+                                 (incl. padding and masked lanes, after pruning),
+                                 [2] real candidate evaluations executed (computing
+                                 nodes x non-padding entries, after pruning) */
   int32_t* info;              /* out [4]: total sweeps, index of result buffer,
                                  tiles processed, launches */
   /* AO3 conical control reduction (solver.py:446-476; NULL ao3_fb = off):
@@ -143,6 +146,11 @@ typedef struct phj_solve_args {
    * halo ring held at the sweep's input -- block-Jacobi with inner
    * iterations, same fixed point, schedule-independent */
   int32_t inner_sweeps;
+  /* out [n_patches][3] or NULL: per patch, node relaxations, logical candidate
+   * evaluations (evals[0] split by patch) and real executed ones (evals[2]);
+   * the reference's per-patch SweepStats counters (solver.py:79-88) under both
+   * schedules */
+  unsigned long long* patch_counts;
   void* stream;               /* cudaStream_t */
 } phj_solve_args;
 

@@ -99,13 +99,13 @@ static void og_locate(const og_grid* g, const double P[3], int64_t cell[3], doub
   }
 }
 
-/* Candidate foot of (serial s, control c); returns 0 when inadmissible
- * (|f| < eps_speed, solver.py:176-179).  solver.py:175-188. */
-static int og_foot(const og_grid* g, const og_dyn* dy, int64_t s, int c,
-                   int64_t cell[3], double loc[3], double* cost) {
+/* Candidate foot of (serial s at point X, control c); returns 0 when
+ * inadmissible (|f| < eps_speed, solver.py:176-179).  solver.py:175-188.
+ * X = og_point(s), hoisted out of the control loops by the callers. */
+static int og_foot_at(const og_grid* g, const og_dyn* dy, int64_t s, const double X[3], int c,
+                      int64_t cell[3], double loc[3], double* cost) {
   const int d = g->dim;
-  double X[3], F[3] = {0.0, 0.0, 0.0};
-  og_point(g, s, X);
+  double F[3] = {0.0, 0.0, 0.0};
   if (dy->kind == OG_DYN_SCALED) {
     double sp = dy->speed[s];
     for (int ax = 0; ax < d; ++ax) F[ax] = sp * dy->controls[c * dy->m + ax];
@@ -127,6 +127,13 @@ static int og_foot(const og_grid* g, const og_dyn* dy, int64_t s, int c,
   og_locate(g, P, cell, loc);
   *cost = dy->cost_l ? h * dy->cost_l[(int64_t)s * dy->nc + c] : h;
   return 1;
+}
+
+static int og_foot(const og_grid* g, const og_dyn* dy, int64_t s, int c,
+                   int64_t cell[3], double loc[3], double* cost) {
+  double X[3];
+  og_point(g, s, X);
+  return og_foot_at(g, dy, s, X, c, cell, loc, cost);
 }
 
 /* flat index of corner `corner` (bit ax = upper face on axis ax) of an ext
@@ -155,6 +162,38 @@ static double og_weight(int dim, const double loc[3], int corner) {
   return w;
 }
 
+/* Weights (og_weight's products, same order: 1.0 * axis 0 * axis 1 ...)
+ * and flat indices (og_corner) of all corners of one candidate cell. */
+static inline void og_cell_corners(const og_grid* g, const int64_t cell[3], const double loc[3],
+                                   double w[8], int64_t f[8]) {
+  const int d = g->dim;
+  const int ncorner = 1 << d;
+  double lo_w[3], hi_w[3];
+  int64_t lo_f[3], hi_f[3];
+  for (int ax = 0; ax < d; ++ax) {
+    hi_w[ax] = loc[ax];
+    lo_w[ax] = 1.0 - loc[ax];
+    int64_t e0 = cell[ax], e1 = cell[ax] + 1;
+    if (g->periodic[ax]) {
+      int64_t M = g->shape[ax];
+      if (e0 == 0) e0 = M; else if (e0 == M + 1) e0 = 1;
+      if (e1 == 0) e1 = M; else if (e1 == M + 1) e1 = 1;
+    }
+    lo_f[ax] = e0 * g->strides[ax];
+    hi_f[ax] = e1 * g->strides[ax];
+  }
+  for (int corner = 0; corner < ncorner; ++corner) {
+    double ww = 1.0;
+    int64_t ff = 0;
+    for (int ax = 0; ax < d; ++ax) {
+      if ((corner >> ax) & 1) { ww *= hi_w[ax]; ff += hi_f[ax]; }
+      else { ww *= lo_w[ax]; ff += lo_f[ax]; }
+    }
+    w[corner] = ww;
+    f[corner] = ff;
+  }
+}
+
 static inline double og_apply_rule(int rule, double v, double cost) {
   if (rule == OG_RULE_REF) return v + cost;
   double beta = exp(-cost);
@@ -167,19 +206,22 @@ static void og_relax(const og_grid* g, const og_dyn* dy, int64_t s,
                      const uint8_t* hard, const uint8_t* allowed, int rule,
                      double* best_out, int64_t* nevals) {
   const int ncorner = 1 << g->dim;
-  double best = OG_BIG;
+  double best = OG_BIG, X[3];
+  og_point(g, s, X);
   for (int c = 0; c < dy->nc; ++c) {
     int64_t cell[3];
     double loc[3], cost;
-    if (!og_foot(g, dy, s, c, cell, loc, &cost)) continue;
+    if (!og_foot_at(g, dy, s, X, c, cell, loc, &cost)) continue;
     if (allowed && allowed[(int64_t)s * dy->nc + c] == 0) continue;
     *nevals += 1;
-    double v = 0.0;
+    double v = 0.0, wc[8];
+    int64_t fc[8];
     int rejected = 0;
+    og_cell_corners(g, cell, loc, wc, fc);
     for (int corner = 0; corner < ncorner; ++corner) {
-      double w = og_weight(g->dim, loc, corner);
+      double w = wc[corner];
       if (w == 0.0) continue;
-      int64_t f2 = og_corner(g, cell, corner);
+      int64_t f2 = fc[corner];
       if (hard[f2] != 0) {
         rejected = 1;
         break;
@@ -278,20 +320,23 @@ int64_t og_feedback(const og_grid* g, const og_dyn* dy, const double* u,
     if (gap_out) gap_out[s] = OG_BIG;
     if (kind[s] != 0) continue;
     if (u[fi] >= unreach) continue;
-    double best = OG_BIG, second = OG_BIG;
+    double best = OG_BIG, second = OG_BIG, X[3];
     int32_t bc = -1;
+    og_point(g, s, X);
     for (int c = 0; c < dy->nc; ++c) {
       int64_t cell[3];
       double loc[3], cost;
-      if (!og_foot(g, dy, s, c, cell, loc, &cost)) continue;
+      if (!og_foot_at(g, dy, s, X, c, cell, loc, &cost)) continue;
       if (allowed && allowed[s * dy->nc + c] == 0) continue;
       nevals += 1;
-      double v = 0.0;
+      double v = 0.0, wc[8];
+      int64_t fc[8];
       int rejected = 0;
+      og_cell_corners(g, cell, loc, wc, fc);
       for (int corner = 0; corner < ncorner; ++corner) {
-        double w = og_weight(g->dim, loc, corner);
+        double w = wc[corner];
         if (w == 0.0) continue;
-        int64_t f2 = og_corner(g, cell, corner);
+        int64_t f2 = fc[corner];
         if (hard[f2] != 0) { rejected = 1; break; }
         v += w * u[f2];
       }
@@ -417,6 +462,136 @@ void og_lift(const og_grid* gc, const double* uc, const og_grid* gf, double* out
     }
     out[s] = (saturate && bad) ? sat_value : v;
   }
+}
+
+/*
+ * Fixed-point residual certificate of a converged patch solve (full-size
+ * parity, tests/test_gpu_fullsize.py).  One Jacobi application of the
+ * reference relaxation (_kernels.py:57-100) to a given field u WITHOUT the
+ * monotone write of :101-105, under the state constraint of a given patch
+ * map: a nonzero-weight corner is readable iff it is an interior node whose
+ * label is the node's own patch or TARGET (patchy.py:369-371 active = patch
+ * u target; solver.py:247 hard = hard_base | ~active).
+ *   lab_ext : int32 per ext node (patchy.py:40-45 codes): >= 0 patch, -2
+ *             TARGET, other < 0 blocked (UNREACHABLE / OBSTACLE / ghost);
+ *             periodic ghosts are never read (corners wrap).
+ *   unreach : 1.0 (Kruzkov) or 0.5*sentinel (reference rule).
+ * out[0] = max |T(u)_i - u_i| over free patch nodes with u_i < unreach
+ * out[1] = serial where out[0] is attained
+ * cnt[0] = free patch nodes with u >= unreach but T(u) < unreach (missed)
+ * cnt[1] = free patch nodes with u < unreach but T(u) >= unreach (spurious)
+ * cnt[2] = target nodes with u != 0
+ * cnt[3] = blocked nodes with u < unreach
+ * cnt[4] = free patch nodes with u < unreach (the certified set)
+ * cnt[5] = candidate evaluations
+ */
+void og_residual(const og_grid* g, const og_dyn* dy, const double* u, const uint8_t* kind,
+                 const int32_t* lab_ext, double unreach, int rule, int nthreads,
+                 double* out, int64_t* cnt) {
+  const int64_t N = g->shape[0] * g->shape[1] * (g->dim == 3 ? g->shape[2] : 1);
+  const int ncorner = 1 << g->dim;
+  double rmax = 0.0;
+  int64_t at = -1, missed = 0, spurious = 0, badt = 0, badb = 0, ncert = 0, nevals = 0;
+  if (nthreads < 1) nthreads = 1;
+#ifdef _OPENMP
+#pragma omp parallel num_threads(nthreads) reduction(+ : missed, spurious, badt, badb, ncert, nevals)
+#endif
+  {
+    double lmax = 0.0;
+    int64_t lat = -1;
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 1024)
+#endif
+    for (int64_t s = 0; s < N; ++s) {
+      const int64_t fi = og_iflat(g, s);
+      const int32_t L = lab_ext[fi];
+      if (kind[s] == 1 || L == -2) {
+        if (u[fi] != 0.0) badt += 1;
+        continue;
+      }
+      if (L < 0 || kind[s] != 0) {
+        if (u[fi] < unreach) badb += 1;
+        continue;
+      }
+      double best = OG_BIG, X[3];
+      og_point(g, s, X);
+      for (int c = 0; c < dy->nc; ++c) {
+        int64_t cell[3];
+        double loc[3], cost;
+        if (!og_foot_at(g, dy, s, X, c, cell, loc, &cost)) continue;
+        nevals += 1;
+        double v = 0.0, wc[8];
+        int64_t fc[8];
+        int rejected = 0;
+        og_cell_corners(g, cell, loc, wc, fc);
+        for (int corner = 0; corner < ncorner; ++corner) {
+          if (wc[corner] == 0.0) continue;
+          const int32_t L2 = lab_ext[fc[corner]];
+          if (!(L2 == L || L2 == -2)) { rejected = 1; break; }
+          v += wc[corner] * u[fc[corner]];
+        }
+        if (rejected) continue;
+        v = og_apply_rule(rule, v, cost);
+        if (v < best) best = v;
+      }
+      if (u[fi] >= unreach) {
+        if (best < unreach) missed += 1;
+        continue;
+      }
+      if (best >= unreach) { spurious += 1; continue; }
+      ncert += 1;
+      double r = best - u[fi];
+      if (r < 0.0) r = -r;
+      if (r > lmax) { lmax = r; lat = s; }
+    }
+#ifdef _OPENMP
+#pragma omp critical
+#endif
+    {
+      if (lmax > rmax) { rmax = lmax; at = lat; }
+    }
+  }
+  out[0] = rmax;
+  out[1] = (double)at;
+  cnt[0] = missed; cnt[1] = spurious; cnt[2] = badt; cnt[3] = badb; cnt[4] = ncert;
+  cnt[5] = nevals;
+}
+
+/*
+ * Transport residual of one colour field (transport_batch, _kernels.py:
+ * 179-204, one Jacobi application without the update): max over movers
+ * (patchy.py:165-180: feedback >= 0, free, admissible foot) of
+ * |phi_i - sum_{w != 0} w phi(corner)|.  Feet on the fly from the feedback
+ * control (solver.py:175-188).  Returns the residual; *n_movers counts.
+ */
+double og_transport_residual(const og_grid* g, const og_dyn* dy, const int32_t* fb,
+                             const uint8_t* kind, const double* phi, int nthreads,
+                             int64_t* n_movers) {
+  const int64_t N = g->shape[0] * g->shape[1] * (g->dim == 3 ? g->shape[2] : 1);
+  const int ncorner = 1 << g->dim;
+  double rmax = 0.0;
+  int64_t nm = 0;
+  if (nthreads < 1) nthreads = 1;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) num_threads(nthreads) reduction(max : rmax) reduction(+ : nm)
+#endif
+  for (int64_t s = 0; s < N; ++s) {
+    if (kind[s] != 0 || fb[s] < 0) continue;
+    int64_t cell[3];
+    double loc[3], cost;
+    if (!og_foot(g, dy, s, fb[s], cell, loc, &cost)) continue;
+    nm += 1;
+    double v = 0.0;
+    for (int corner = 0; corner < ncorner; ++corner) {
+      double w = og_weight(g->dim, loc, corner);
+      if (w != 0.0) v += w * phi[og_corner(g, cell, corner)];
+    }
+    double r = phi[og_iflat(g, s)] - v;
+    if (r < 0.0) r = -r;
+    if (r > rmax) rmax = r;
+  }
+  *n_movers = nm;
+  return rmax;
 }
 
 /* max over serials of |f(...)| for eps_speed (solver.py:162-168). */

@@ -57,7 +57,8 @@ class SolveArgs(ctypes.Structure):
                 ("n_patches", I32), ("max_sweeps", I32), ("mine", P), ("tol", D),
                 ("workspace", P), ("patch_sweeps", P), ("maxch_hist", P), ("evals", P),
                 ("info", P), ("ao3_fb", P), ("ao3_mask", P), ("ao3_count", P),
-                ("ao3_words", I32), ("options", I32), ("act_tol", D), ("inner_sweeps", I32), ("stream", P)]
+                ("ao3_words", I32), ("options", I32), ("act_tol", D), ("inner_sweeps", I32),
+                ("patch_counts", P), ("stream", P)]
 
 
 SOLVE_NO_PRUNE = 1  # PHJ_SOLVE_NO_PRUNE

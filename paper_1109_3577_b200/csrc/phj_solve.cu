@@ -75,6 +75,7 @@ struct SolveParams {
   TileGrid tg;
   int n_classes, nc, n_real;
   const int32_t* oct_start;
+  const int32_t* ctrl;  // original control per stencil entry (padding detection)
   const uint32_t* nzmask;
   const double* weights;
   const double* cost;
@@ -91,6 +92,7 @@ struct SolveParams {
   unsigned long long* maxch;  // [max_sweeps * R], double bits
   int32_t* patch_sweeps;
   unsigned long long* evals;
+  unsigned long long* pcount;  // [R][3] node relaxations, logical, executed evals (or NULL)
   int32_t* info;
   int prune;  // exact octant pruning on (PHJ_SOLVE_NO_PRUNE clears it)
   double act;  // a node change marks the neighbour blocks only if > act (0 = exact)
@@ -109,11 +111,12 @@ struct StencilSmem {
   T* b;          // [nent] 1 - beta
   uint32_t* nz;  // [nent]
   int* oct;      // [ncls][2^D + 1]
+  int* oreal;    // [ncls][2^D] real (non-padding) entries per octant (solve kernels)
   static __host__ __device__ int64_t bytes(int ncls, int nc) {
     int64_t nent = (int64_t)ncls * nc;
     int64_t b = nent * (1 << D) * sizeof(T) + 2 * nent * sizeof(T);
     b = (b + 15) / 16 * 16;
-    b += nent * 4 + (int64_t)ncls * ((1 << D) + 1) * 4;
+    b += nent * 4 + (int64_t)ncls * ((1 << D) + 1) * 4 + (int64_t)ncls * (1 << D) * 4;
     return (b + 15) / 16 * 16;
   }
 };
@@ -129,6 +132,7 @@ __device__ inline StencilSmem<D, T> carve_stencil(unsigned char* base, int ncls,
   p = base + ((p - base + 15) / 16 * 16);
   s.nz = (uint32_t*)p;
   s.oct = (int*)(s.nz + nent);
+  s.oreal = s.oct + (int64_t)ncls * ((1 << D) + 1);
   return s;
 }
 
@@ -180,12 +184,28 @@ __host__ __device__ inline int64_t solve_stencil_bytes(int ncls, int nc) {
   return ncls > 1 ? kWarps * solve_stencil_slot<D, T>(nc) : StencilSmem<D, T>::bytes(ncls, nc);
 }
 
+// Real (non-padding) entries of octant group [e0, e1): the host pads a group
+// by repeating its last entry (dynamics.build_stencil), every control lies in
+// one octant, so an entry is padding iff it repeats its predecessor's control.
+__device__ inline int real_entries(const int32_t* ctrl, int e0, int e1) {
+  if (!ctrl) return e1 - e0;
+  int n = 0;
+  for (int e = e0; e < e1; ++e) n += (e == e0 || __ldg(&ctrl[e]) != __ldg(&ctrl[e - 1]));
+  return n;
+}
+
 template <int D, typename T, int RULE>
 __device__ inline void stage_stencil(const StencilSmem<D, T>& s, int ncls, int nc,
                                      const int32_t* oct_start, const uint32_t* nzmask,
-                                     const double* weights, const double* cost) {
+                                     const double* weights, const double* cost,
+                                     const int32_t* ctrl = nullptr) {
+  constexpr int NC = 1 << D;
   stage_entries<D, T, RULE>(s, 0, 0, ncls * nc, threadIdx.x, blockDim.x, nzmask, weights, cost);
-  for (int i = threadIdx.x; i < ncls * ((1 << D) + 1); i += blockDim.x) s.oct[i] = oct_start[i];
+  for (int i = threadIdx.x; i < ncls * (NC + 1); i += blockDim.x) s.oct[i] = oct_start[i];
+  for (int i = threadIdx.x; i < ncls * NC; i += blockDim.x) {
+    const int cls = i / NC, O = i % NC;
+    s.oreal[i] = real_entries(ctrl, oct_start[cls * (NC + 1) + O], oct_start[cls * (NC + 1) + O + 1]);
+  }
 }
 
 // One class of a multi-class stencil (Dubins: one per heading) into a
@@ -193,10 +213,14 @@ __device__ inline void stage_stencil(const StencilSmem<D, T>& s, int ncls, int n
 template <int D, typename T, int RULE>
 __device__ inline void stage_class(const StencilSmem<D, T>& s, int cls, int nc, int lane,
                                    const int32_t* oct_start, const uint32_t* nzmask,
-                                   const double* weights, const double* cost) {
+                                   const double* weights, const double* cost,
+                                   const int32_t* ctrl = nullptr) {
   constexpr int NC = 1 << D;
   stage_entries<D, T, RULE>(s, 0, cls * nc, nc, lane, 32, nzmask, weights, cost);
   if (lane <= NC) s.oct[lane] = oct_start[cls * (NC + 1) + lane] - cls * nc;
+  if (lane < NC)
+    s.oreal[lane] = real_entries(ctrl, oct_start[cls * (NC + 1) + lane],
+                                 oct_start[cls * (NC + 1) + lane + 1]);
 }
 
 // Neighbourhood sources.  Evaluation code asks a source for corner K of
@@ -649,15 +673,16 @@ __device__ __forceinline__ int preferred_octant(const T* lt) {
 // Sweep evaluation of one block from its staged tile: with per-node costs
 // the warp's preferred octant first, then the others unless pruned; with
 // per-control costs every octant in order.  `hook` runs once, after the
-// first octant.  Returns the stencil entries evaluated per node.
+// first octant.  Returns the stencil entries evaluated per node; `n_real`
+// gets the real (non-padding) ones among them.
 template <int D, typename T, int NB, int RULE, int COST, bool SLOW, typename Hook,
           bool AO3 = false>
 __device__ __forceinline__ int eval_sweep(const T* lt, bool prune_on, const StencilSmem<D, T>& s,
                                           const int* os, const uint32_t (&fm)[NB],
                                           const T (&ncoef)[NB], const bool (&comp)[NB],
                                           MinAcc<T> (&mn)[NB], T (&best)[NB], int (&bidx)[NB],
-                                          const Hook& hook, const Allowed<NB>* al = nullptr,
-                                          bool warm = false) {
+                                          const Hook& hook, int& n_real,
+                                          const Allowed<NB>* al = nullptr, bool warm = false) {
 #if PHJ_CTRL_REGNB
   if constexpr (COST == PHJ_COST_CTRL) {
     // per-control costs (no pruning), few controls: the whole neighbourhood
@@ -678,6 +703,9 @@ __device__ __forceinline__ int eval_sweep(const T* lt, bool prune_on, const Sten
           for (int dx = 0; dx < NB + 2; ++dx) nb.v[dz * 3 + dy][dx] = lt[(dz * S::RB + dy) * S::C + dx];
     }
     EvalAll<D, T, NB, RULE, COST, SLOW, 0>::run(nb, s, os, fm, ncoef, nullptr, mn, best, bidx, hook);
+    n_real = 0;
+#pragma unroll
+    for (int O = 0; O < (1 << D); ++O) n_real += s.oreal[O];
     return os[1 << D] - os[0];
   }
 #endif
@@ -687,6 +715,7 @@ __device__ __forceinline__ int eval_sweep(const T* lt, bool prune_on, const Sten
   OctNb<D, T, NB> cell;
   cell.load(lt, first);
   int n_ent = 0;
+  n_real = 0;
   // warm: the running minima start at the previous block-local relaxation's
   // minima (an upper bound of the new ones: values only decreased), so the
   // preferred octant is prunable too
@@ -695,6 +724,7 @@ __device__ __forceinline__ int eval_sweep(const T* lt, bool prune_on, const Sten
                                                                      ncoef, nullptr, mn, best,
                                                                      bidx, al);
     n_ent = os[first + 1] - os[first];
+    n_real = s.oreal[first];
   }
   hook();
 #pragma unroll 1
@@ -709,6 +739,7 @@ __device__ __forceinline__ int eval_sweep(const T* lt, bool prune_on, const Sten
     eval_octant<D, T, NB, RULE, COST, SLOW, 0, OctNb<D, T, NB>, AO3>(cell, O, s, os, fm, ncoef,
                                                                      nullptr, mn, best, bidx, al);
     n_ent += os[O + 1] - os[O];
+    n_real += s.oreal[O];
   }
   return n_ent;
 }
@@ -905,6 +936,53 @@ __device__ __forceinline__ void flush_patch_max(const SolveParams& p, PatchMax& 
   pm.m = 0.0;
 }
 
+// Per-patch work counters of one block visit (SweepStats per patch, also
+// under the asynchronous schedule): node relaxations, logical candidate
+// evaluations (admissible controls of each relaxation), executed candidate
+// evaluations (real stencil entries after pruning).  Warp-aggregated when
+// every computing node of the warp is in one patch; per-CTA shared counters
+// for R <= kSmemPatchReduce.
+template <int NB>
+__device__ __forceinline__ void add_patch_counts(const SolveParams& p, unsigned long long* s_pc,
+                                                 const bool (&comp)[NB], const int (&labv)[NB],
+                                                 const int (&fc)[NB], int iters,
+                                                 unsigned real_it) {
+  const unsigned FULL = 0xffffffffu;
+  unsigned long long* cnt = p.R <= kSmemPatchReduce ? s_pc : p.pcount;
+  int l0 = -1, ncomp = 0;
+  unsigned n = 0, e = 0;
+#pragma unroll
+  for (int r = 0; r < NB; ++r) {
+    if (!comp[r]) continue;
+    l0 = labv[r];
+    ++ncomp;
+    n += (unsigned)iters;
+    e += (unsigned)(fc[r] * iters);
+  }
+  const int lref = __reduce_max_sync(FULL, l0);
+  bool uni = true;
+#pragma unroll
+  for (int r = 0; r < NB; ++r) uni &= !comp[r] || labv[r] == lref;
+  if (__all_sync(FULL, uni)) {
+    const unsigned wn = __reduce_add_sync(FULL, n);
+    const unsigned we = __reduce_add_sync(FULL, e);
+    const unsigned wx = __reduce_add_sync(FULL, real_it * (unsigned)ncomp);
+    if ((threadIdx.x & 31) == 0 && lref >= 0) {
+      atomicAdd(&cnt[lref * 3 + 0], (unsigned long long)wn);
+      atomicAdd(&cnt[lref * 3 + 1], (unsigned long long)we);
+      atomicAdd(&cnt[lref * 3 + 2], (unsigned long long)wx);
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < NB; ++r) {
+      if (!comp[r]) continue;
+      atomicAdd(&cnt[labv[r] * 3 + 0], (unsigned long long)iters);
+      atomicAdd(&cnt[labv[r] * 3 + 1], (unsigned long long)(fc[r] * iters));
+      atomicAdd(&cnt[labv[r] * 3 + 2], (unsigned long long)real_it);
+    }
+  }
+}
+
 // One block of the value sweep, processed by one warp from its staged halo
 // tile and node inputs.  `hook` (the next block's loads, deferred marks)
 // runs exactly once.  Returns (warp-uniform) whether any node changed.
@@ -914,6 +992,7 @@ __device__ __forceinline__ int sweep_block(const SolveParams& p, const StencilSm
                                             T* __restrict__ vout, const int* s_done,
                                             unsigned long long* s_max, unsigned long long* gmax_row,
                                             unsigned long long& evals, unsigned long long& exec,
+                                            unsigned long long& xreal, unsigned long long* s_pc,
                                             PatchMax& pm, PhaseTimer& tm, const Hook& hook) {
   using B = Blk<D>;
   using S = TileShape<D>;
@@ -991,16 +1070,23 @@ __device__ __forceinline__ int sweep_block(const SolveParams& p, const StencilSm
       }
     }
     unsigned long long fcnt_sum = 0;
+    int fc[NB];
+    int ncomp = 0;
 #pragma unroll
     for (int r = 0; r < NB; ++r) {
+      fc[r] = 0;
       if (!comp[r]) continue;
       int fcnt = nadm;
       if (p.ao3_fb) {
         const int f = ns->fb[ly * B::BX + lx * NB + r];
         if (f >= 0) fcnt = __ldg(&p.ao3_count[f]);
       }
+      fc[r] = fcnt;
+      ++ncomp;
       fcnt_sum += (unsigned long long)fcnt;
     }
+    unsigned real_it = 0;
+    int iters = 0;
     // old values, then up to p.inner block-local relaxations: the halo ring
     // stays at the sweep's input, the block's own nodes are relaxed in the
     // staged tile (deterministic: independent of the schedule)
@@ -1034,19 +1120,22 @@ __device__ __forceinline__ int sweep_block(const SolveParams& p, const StencilSm
         bidx[r] = 0;
       }
       const bool warm = it > 0;
-      int n_ent;
+      int n_ent, n_real;
       if (p.ao3_fb) {
         n_ent = eval_sweep<D, T, NB, RULE, COST, true, decltype(once), true>(
-            lt, p.prune != 0, s, os, fm, ncoef, comp, mn, best, bidx, once, &al, warm);
+            lt, p.prune != 0, s, os, fm, ncoef, comp, mn, best, bidx, once, n_real, &al, warm);
       } else if (slow) {
         n_ent = eval_sweep<D, T, NB, RULE, COST, true>(lt, p.prune != 0, s, os, fm, ncoef, comp,
-                                                       mn, best, bidx, once, nullptr, warm);
+                                                       mn, best, bidx, once, n_real, nullptr, warm);
       } else {
         n_ent = eval_sweep<D, T, NB, RULE, COST, false>(lt, p.prune != 0, s, os, fm, ncoef, comp,
-                                                        mn, best, bidx, once, nullptr, warm);
+                                                        mn, best, bidx, once, n_real, nullptr,
+                                                        warm);
       }
       exec += (unsigned long long)n_ent * NB;
       evals += fcnt_sum;
+      real_it += (unsigned)n_real;
+      ++iters;
       bool moved = false;
 #pragma unroll
       for (int r = 0; r < NB; ++r) {
@@ -1076,6 +1165,8 @@ __device__ __forceinline__ int sweep_block(const SolveParams& p, const StencilSm
       __syncwarp();
     }
     tm.mark(3);
+    xreal += (unsigned long long)real_it * (unsigned long long)ncomp;
+    if (p.pcount) add_patch_counts<NB>(p, s_pc, comp, labv, fc, iters, real_it);
 #pragma unroll
     for (int r = 0; r < NB; ++r) {
       if (!(comp[r] || copy[r])) continue;
@@ -1231,21 +1322,24 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __gri
            : carve_stencil<D, T>(smem, 1, p.nc);
   int* s_done = (int*)(smem + sbytes);
   unsigned long long* s_max = (unsigned long long*)(s_done + ((p.R + 1) / 2 * 2));
+  unsigned long long* s_pc = s_max + min(p.R, kSmemPatchReduce);  // [min(R,64)][3]
   T* tiles = (T*)(smem + align_up(sbytes + (int64_t)((p.R + 1) / 2 * 2) * 4 +
-                                      (int64_t)min(p.R, kSmemPatchReduce) * 8,
+                                      (int64_t)min(p.R, kSmemPatchReduce) * 8 * 4,
                                   16));
   T* wtile = tiles + (threadIdx.x >> 5) * 2 * S::N;
   NodeStage<D, T>* wnodes =
       (NodeStage<D, T>*)(tiles + kWarps * 2 * S::N) + (threadIdx.x >> 5) * 2;
   if (!warp_cls)
-    stage_stencil<D, T, RULE>(s, p.n_classes, p.nc, p.oct_start, p.nzmask, p.weights, p.cost);
+    stage_stencil<D, T, RULE>(s, p.n_classes, p.nc, p.oct_start, p.nzmask, p.weights, p.cost,
+                              p.ctrl);
   int wcls = -1;  // class held by this warp's slot
   for (int i = threadIdx.x; i < p.R; i += blockDim.x)
     s_done[i] = (p.mine == nullptr || p.mine[i]) ? 0x7fffffff : 0;
+  for (int i = threadIdx.x; i < min(p.R, kSmemPatchReduce) * 3; i += blockDim.x) s_pc[i] = 0ull;
   __syncthreads();
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
-  unsigned long long evals = 0, exec = 0;
+  unsigned long long evals = 0, exec = 0, xreal = 0;
   int blocks_done = 0;
   int sw = 0, buf = 0, stage = 0;
   const int nshared = min(p.R, kSmemPatchReduce);
@@ -1308,7 +1402,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __gri
         decode_block<D>(p.tg, blk, bc);
         if (bc[0] != wcls) {
           __syncwarp();
-          stage_class<D, T, RULE>(s, bc[0], p.nc, lane, p.oct_start, p.nzmask, p.weights, p.cost);
+          stage_class<D, T, RULE>(s, bc[0], p.nc, lane, p.oct_start, p.nzmask, p.weights, p.cost, p.ctrl);
           wcls = bc[0];
         }
       }
@@ -1332,8 +1426,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __gri
 #endif
       tm.mark(1);
       const int ch = sweep_block<D, T, RULE, COST>(p, s, blk, wtile + stage * S::N, wnodes + stage,
-                                                    vout, s_done, s_max, gmax_row, evals, exec, pm,
-                                                    tm, hook);
+                                                    vout, s_done, s_max, gmax_row, evals, exec,
+                                                    xreal, s_pc, pm, tm, hook);
       ++blocks_done;
       mq.issue(p.tg, p.g, blk, ch, lane, nxt_flags);
       tm.mark(6);
@@ -1388,23 +1482,29 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __gri
       p.info[1] = buf;
     }
   }
-  __shared__ unsigned long long s_ev, s_ex;
+  __shared__ unsigned long long s_ev, s_ex, s_xr;
   __shared__ int s_blk;
   if (threadIdx.x == 0) {
     s_ev = 0;
     s_ex = 0;
+    s_xr = 0;
     s_blk = 0;
   }
   __syncthreads();
   atomicAdd(&s_ev, evals);
   atomicAdd(&s_ex, exec);
+  atomicAdd(&s_xr, xreal);
   if (lane == 0) atomicAdd(&s_blk, blocks_done);
   __syncthreads();
   if (threadIdx.x == 0) {
     atomicAdd(&p.evals[0], s_ev);
     atomicAdd(&p.evals[1], s_ex);
+    atomicAdd(&p.evals[2], s_xr);
     atomicAdd(&p.info[2], s_blk);
   }
+  if (p.pcount && p.R <= kSmemPatchReduce)
+    for (int i = threadIdx.x; i < p.R * 3; i += blockDim.x)
+      if (s_pc[i]) atomicAdd(&p.pcount[i], s_pc[i]);
 }
 
 // ---------------------------------------------------------------------------
@@ -1563,18 +1663,21 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
            : carve_stencil<D, T>(smem, 1, p.nc);
   int* s_done = (int*)(smem + sbytes);
   unsigned long long* s_max = (unsigned long long*)(s_done + ((p.R + 1) / 2 * 2));
+  unsigned long long* s_pc = s_max + min(p.R, kSmemPatchReduce);  // [min(R,64)][3]
   T* tiles = (T*)(smem + align_up(sbytes + (int64_t)((p.R + 1) / 2 * 2) * 4 +
-                                      (int64_t)min(p.R, kSmemPatchReduce) * 8,
+                                      (int64_t)min(p.R, kSmemPatchReduce) * 8 * 4,
                                   16));
   T* wtile = tiles + (threadIdx.x >> 5) * 2 * S::N;
   NodeStage<D, T>* wnodes =
       (NodeStage<D, T>*)(tiles + kWarps * 2 * S::N) + (threadIdx.x >> 5) * 2;
   if (!warp_cls)
-    stage_stencil<D, T, RULE>(s, p.n_classes, p.nc, p.oct_start, p.nzmask, p.weights, p.cost);
+    stage_stencil<D, T, RULE>(s, p.n_classes, p.nc, p.oct_start, p.nzmask, p.weights, p.cost,
+                              p.ctrl);
   int wcls = -1;
   for (int i = threadIdx.x; i < p.R; i += blockDim.x)
     s_done[i] = (p.mine == nullptr || p.mine[i]) ? 0x7fffffff : 0;
   for (int i = threadIdx.x; i < min(p.R, kSmemPatchReduce); i += blockDim.x) s_max[i] = 0ull;
+  for (int i = threadIdx.x; i < min(p.R, kSmemPatchReduce) * 3; i += blockDim.x) s_pc[i] = 0ull;
   __syncthreads();
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
@@ -1583,7 +1686,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   const unsigned cap = (unsigned)p.tg.total + (unsigned)(gridDim.x * kWarps);
   unsigned swept_local = 0;
   unsigned long long* gmax_row = sweep_max_slots(p.ws, 0);
-  unsigned long long evals = 0, exec = 0;
+  unsigned long long evals = 0, exec = 0, xreal = 0;
   int blocks_done = 0;
   PatchMax pm{-1, 0.0};
   PhaseTimer tm;
@@ -1610,7 +1713,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       decode_block<D>(p.tg, blk, bc);
       if (bc[0] != wcls) {
         __syncwarp();
-        stage_class<D, T, RULE>(s, bc[0], p.nc, lane, p.oct_start, p.nzmask, p.weights, p.cost);
+        stage_class<D, T, RULE>(s, bc[0], p.nc, lane, p.oct_start, p.nzmask, p.weights, p.cost, p.ctrl);
         wcls = bc[0];
       }
     }
@@ -1620,7 +1723,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     tm.mark(1);
     auto hook = []() {};
     const int ch = sweep_block<D, T, RULE, COST>(p, s, blk, wtile, wnodes, (T*)p.v[0], s_done,
-                                                 s_max, gmax_row, evals, exec, pm, tm, hook);
+                                                 s_max, gmax_row, evals, exec, xreal, s_pc, pm,
+                                                 tm, hook);
     ++blocks_done;
 #ifdef PHJ_TIMING
     if (lane == 0) atomicAdd(&g_visit_kind[ch], 1ull);
@@ -1647,23 +1751,29 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   if (lane == 0)
     for (int i = 0; i < 12; ++i) atomicAdd(&g_phase_cycles[i], tm.acc[i]);
 #endif
-  __shared__ unsigned long long s_ev, s_ex;
+  __shared__ unsigned long long s_ev, s_ex, s_xr;
   __shared__ int s_blk;
   if (threadIdx.x == 0) {
     s_ev = 0;
     s_ex = 0;
+    s_xr = 0;
     s_blk = 0;
   }
   __syncthreads();
   atomicAdd(&s_ev, evals);
   atomicAdd(&s_ex, exec);
+  atomicAdd(&s_xr, xreal);
   if (lane == 0) atomicAdd(&s_blk, blocks_done);
   __syncthreads();
   if (threadIdx.x == 0) {
     atomicAdd(&p.evals[0], s_ev);
     atomicAdd(&p.evals[1], s_ex);
+    atomicAdd(&p.evals[2], s_xr);
     atomicAdd(&p.info[2], s_blk);
   }
+  if (p.pcount && p.R <= kSmemPatchReduce)
+    for (int i = threadIdx.x; i < p.R * 3; i += blockDim.x)
+      if (s_pc[i]) atomicAdd(&p.pcount[i], s_pc[i]);
 }
 
 // Per-patch results of an asynchronous solve: "sweeps" = blocks swept /
@@ -3102,6 +3212,7 @@ static int solve_impl(const phj_solve_args* a) {
   p.nc = a->st.n_controls;
   p.n_real = a->st.n_real;
   p.oct_start = a->st.oct_start;
+  p.ctrl = a->st.ctrl;
   p.nzmask = a->st.nzmask;
   p.weights = a->st.weights;
   p.cost = a->st.cost;
@@ -3119,6 +3230,7 @@ static int solve_impl(const phj_solve_args* a) {
   p.maxch = (unsigned long long*)a->maxch_hist;
   p.patch_sweeps = a->patch_sweeps;
   p.evals = a->evals;
+  p.pcount = a->patch_counts;
   p.info = a->info;
   p.prune = (a->options & PHJ_SOLVE_NO_PRUNE) ? 0 : 1;
   p.act = a->act_tol;
@@ -3132,7 +3244,10 @@ static int solve_impl(const phj_solve_args* a) {
   const bool async = (a->options & PHJ_SOLVE_ASYNC) != 0;
   PHJ_CUDA(cudaMemsetAsync(a->maxch_hist, 0, sizeof(double) * (size_t)a->max_sweeps * a->n_patches,
                            stream));
-  PHJ_CUDA(cudaMemsetAsync(a->evals, 0, 2 * sizeof(unsigned long long), stream));
+  PHJ_CUDA(cudaMemsetAsync(a->evals, 0, 3 * sizeof(unsigned long long), stream));
+  if (a->patch_counts)
+    PHJ_CUDA(cudaMemsetAsync(a->patch_counts, 0, 3 * sizeof(unsigned long long) * a->n_patches,
+                             stream));
   PHJ_CUDA(cudaMemsetAsync(a->info, 0, 4 * sizeof(int32_t), stream));
   // initial blocks: those that can move from the start field (exact: from
   // the unreached start a block with no reached value within its 3^D
@@ -3146,7 +3261,7 @@ static int solve_impl(const phj_solve_args* a) {
   PHJ_CUDA(cudaGetLastError());
   size_t smem = (size_t)align_up(solve_stencil_bytes<D, T>(p.n_classes, p.nc) +
                                      (int64_t)((p.R + 1) / 2 * 2) * 4 +
-                                     (int64_t)std::min(p.R, kSmemPatchReduce) * 8,
+                                     (int64_t)std::min(p.R, kSmemPatchReduce) * 8 * 4,
                                  16) +
                 (size_t)solve_tile_bytes<D, T>();
   if (async) {

@@ -201,8 +201,9 @@ def solve_full_internal(plan: StencilPlan, cfg: SolverConfig, work: Optional[tor
                            inner=cfg.inner_for(plan.grid.dim))
     n_free = int((plan.kind == KIND_FREE).sum().item())
     st = stats_for_patch(res, 0, n_free, plan.n_adm, cfg.tol)
-    st.node_relaxations = plan.grid.n_interior * st.sweeps
-    st.performed_evals = res.evals
+    if cfg.schedule == "jacobi":
+        st.node_relaxations = plan.grid.n_interior * st.sweeps
+    st.performed_evals = res.real
     return res.values, st
 
 
@@ -480,6 +481,7 @@ def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Te
     warnings = []
     stats = []
     performed = 0
+    logical = 0
     executed = 0
     kernel_ms = 0.0
     sweeps_total = 0
@@ -493,7 +495,8 @@ def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Te
                            act_tol=cfg.act_tol, schedule=cfg.schedule,
                            inner=cfg.inner_for(plan.grid.dim))
         out = res.values
-        performed = res.evals
+        performed = res.real
+        logical = res.evals
         executed = res.executed
         kernel_ms += res.device_ms
         sweeps_total = int(res.info[0])
@@ -535,7 +538,8 @@ def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Te
                            inner=cfg.inner_for(plan.grid.dim))
             oi = plan.interior_int(out)
             oi.copy_(torch.where(own, plan.interior_int(res.values), oi))
-            performed += res.evals
+            performed += res.real
+            logical += res.evals
             executed += res.executed
             kernel_ms += res.device_ms
             sweeps_total += int(res.info[0])
@@ -554,7 +558,8 @@ def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Te
     blocked = (col3 < 0) & (col3 != TARGET)
     oi.copy_(torch.where(blocked, torch.full_like(oi, unr), oi))
     _sync_periodic(plan, out)
-    return out, stats, warnings, {"performed": performed, "executed": executed,
+    return out, stats, warnings, {"performed": performed, "logical": logical,
+                                  "executed": executed,
                                   "kernel_ms": kernel_ms,
                                   "sweeps": sweeps_total, "tiles": tiles_total,
                                   "block_counts": block_counts}
@@ -741,7 +746,6 @@ def run_patchy(spec: ProblemSpec, pcfg: PatchyConfig, cfg: Optional[SolverConfig
         stats.warnings.extend(warnings)
         for st in pstats:
             stats.merge_counts(st)
-        stats.performed_evals += pinfo["performed"]
         stats.kernels["patch_solve"] = pinfo
     stats.candidate_evals += int(ev.item())
     value = NodeField(fine_grid, fplan.user_from_working(out, rule, dtype))

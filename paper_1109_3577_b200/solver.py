@@ -104,10 +104,14 @@ class SolverConfig:
 
 @dataclass
 class SweepStats:
-    """Outcome of one solve (solver.py:79-88).  ``candidate_evals`` keeps the
-    reference's dense count (nodes x admissible controls x sweeps);
-    ``performed_evals`` is what the device actually evaluated after
-    activity skipping."""
+    """Outcome of one solve (solver.py:79-88).  ``node_relaxations`` and
+    ``candidate_evals`` (admissible controls of every relaxation, the
+    reference's count, _kernels.py:76) are counted per patch by the device
+    under both schedules; ``performed_evals`` are the candidate evaluations
+    the device really executed (after activity skipping and the exact octant
+    pruning).  Asynchronous solves report ``sweeps`` as equivalent sweeps
+    (node relaxations / patch nodes) and keep no per-sweep max change
+    (``max_change`` is NaN: ``tol`` does not apply, ``activity_tol`` does)."""
 
     sweeps: int = 0
     node_relaxations: int = 0
@@ -412,6 +416,9 @@ class DeviceSolveResult:
     device_ms: float = 0.0
     block_counts: Optional[np.ndarray] = None
     executed: int = 0              # stencil-entry evaluations run (after octant pruning)
+    real: int = 0                  # real candidate evaluations executed (no padding)
+    patch_counts: Optional[np.ndarray] = None  # [R, 3] relaxations, logical, real evals
+    schedule: str = "jacobi"
 
 
 def device_solve(plan: StencilPlan, work: torch.Tensor, lab: torch.Tensor, fmask: torch.Tensor,
@@ -427,7 +434,8 @@ def device_solve(plan: StencilPlan, work: torch.Tensor, lab: torch.Tensor, fmask
     ws = torch.empty(int(wsb), dtype=torch.uint8, device=dev)
     ps = torch.zeros(n_patches, dtype=torch.int32, device=dev)
     mc = torch.zeros(max_sweeps * n_patches, dtype=torch.float64, device=dev)
-    ev = torch.zeros(2, dtype=torch.int64, device=dev)
+    ev = torch.zeros(3, dtype=torch.int64, device=dev)
+    pc = torch.zeros((n_patches, 3), dtype=torch.int64, device=dev)
     info = torch.zeros(4, dtype=torch.int32, device=dev)
     coef, coef0 = plan.coef(rule, dtype)
     a = _lib.SolveArgs()
@@ -454,6 +462,7 @@ def device_solve(plan: StencilPlan, work: torch.Tensor, lab: torch.Tensor, fmask
         _lib.SOLVE_ASYNC if schedule == "async" else 0)
     a.act_tol = float(act_tol)
     a.inner_sweeps = int(inner)
+    a.patch_counts = _lib.ptr(pc)
     if ao3 is not None:
         fbx, amask, acount, words = ao3
         a.ao3_fb = _lib.ptr(fbx)
@@ -472,12 +481,15 @@ def device_solve(plan: StencilPlan, work: torch.Tensor, lab: torch.Tensor, fmask
     last = mc.view(max_sweeps, n_patches)[
         (ps.abs().long() - 1).clamp(0, max_sweeps - 1), torch.arange(n_patches, device=dev)]
     pack = torch.cat([info.double(), ps.double(), ev.double(), last]).cpu().numpy()
+    # the per-patch counters as exact int64 (they can exceed 2^53 in sum only)
+    pc_h = pc.cpu().numpy()
     info_h = pack[:4].astype(np.int64)
     ps_h = pack[4:4 + n_patches].astype(np.int32)
-    ev_h = pack[4 + n_patches:6 + n_patches].astype(np.int64)
+    ev_h = pack[4 + n_patches:7 + n_patches].astype(np.int64)
     res = v1 if int(info_h[1]) == 1 else work
-    out = DeviceSolveResult(res, ps_h, pack[6 + n_patches:].copy(), int(ev_h[0]), info_h,
-                            executed=int(ev_h[1]))
+    out = DeviceSolveResult(res, ps_h, pack[7 + n_patches:].copy(), int(ev_h[0]), info_h,
+                            executed=int(ev_h[1]), real=int(ev_h[2]), patch_counts=pc_h,
+                            schedule=schedule)
     out.device_ms = e0.elapsed_time(e1)
     if _lib.DIAG:
         out.block_counts = active_blocks_per_sweep(plan, ws, max_sweeps, int(info_h[0]))
@@ -496,13 +508,32 @@ def active_blocks_per_sweep(plan: StencilPlan, ws: torch.Tensor, max_sweeps: int
 
 def stats_for_patch(res: DeviceSolveResult, p: int, n_nodes: int, n_adm: int, tol: float,
                     label: str = "", cands_per_sweep: Optional[int] = None) -> SweepStats:
+    """SweepStats of patch p from the device counters (per-patch node
+    relaxations and candidate evaluations counted by the solve kernels)."""
     s = int(res.patch_sweeps[p])
     st = SweepStats()
     if n_nodes == 0:
         return st
-    st.sweeps = abs(s)
     st.converged = s > 0
-    # asynchronous solves report equivalent sweeps and keep no per-sweep history
+    asyn = res.schedule == "async"
+    pc = res.patch_counts
+    if pc is not None:
+        st.performed_evals = int(pc[p, 2])
+    if asyn:
+        # no sweeps: the reference's counters are the device's per-patch counts
+        if pc is not None:
+            st.node_relaxations = int(pc[p, 0])
+            st.candidate_evals = int(pc[p, 1])
+        # equivalent sweeps of this patch: its node relaxations / its nodes
+        st.sweeps = max(1, -(-st.node_relaxations // n_nodes)) if pc is not None else abs(s)
+        st.max_change = float("nan")
+        if not st.converged:
+            st.warning = (f"{label}asynchronous solve stopped: block-visit budget exhausted "
+                          f"after {st.sweeps} equivalent sweeps")
+        return st
+    # Jacobi: the reference's dense counts for the same number of sweeps
+    # (every node relaxed every sweep, _kernels.py:57-76)
+    st.sweeps = abs(s)
     st.max_change = float(res.last_change[p]) if st.sweeps > 0 else 0.0
     st.node_relaxations = n_nodes * st.sweeps
     st.candidate_evals = (n_nodes * n_adm if cands_per_sweep is None
@@ -629,8 +660,9 @@ def solve(field: NodeField, spec: ProblemSpec, node_set=None,
             order_t = torch.as_tensor(order, device=dev)
             cands = int(cnt_user[order_t[free]].sum().item())
         st = stats_for_patch(res, 0, n_free, plan.n_adm, cfg.tol, cands_per_sweep=cands)
-        st.node_relaxations = order.size * st.sweeps
-        st.performed_evals = res.evals
+        if cfg.schedule == "jacobi":
+            st.node_relaxations = order.size * st.sweeps
+        st.performed_evals = res.real
     out_user = plan.user_from_working(res_vals, rule, dtype).view(-1)
     uflat = torch.as_tensor(grid.interior_flat()[order], device=dev)
     field.flat[uflat] = out_user[uflat]

@@ -1,0 +1,208 @@
+"""Parity certificates at the BASELINE sizes (configs 2-5, north_star: "matching
+the CPU oracle within tolerance on all five configs").
+
+The oracle cannot iterate these grids to convergence in test time (config 5:
+135 M nodes x 96 controls, ~500 Jacobi sweeps), so every stage of the device
+pipeline is checked against ONE oracle application on the device's own
+input -- the same stage boundaries as run_patchy (patchy.py:405-467):
+
+1. coarse solve: fixed-point residual r = |T(v) - v|_inf of the oracle map
+   (_kernels.py:57-100, unclamped) at the device's coarse field; the Kruzkov
+   map is a beta_max-contraction, so |v - v*| <= r / (1 - beta_max)
+   (oracle.pipeline.contraction_bound; reference rule: 2 r u_max / h_min);
+2. lift: the oracle lift (grid.py:242-261) of the device's coarse field equals
+   the device's lifted field (bit-exact in fp64);
+3. feedback: the oracle argmin (_kernels.py:109-167) on the device's lifted
+   field equals the device feedback except at argmin ties (best-vs-second gap
+   below tie_gap), counted;
+4. transport (tight color_tol): per colour the oracle transport residual
+   |phi - I[phi](foot)|_inf over movers (_kernels.py:179-204) of the device's
+   phi; the oracle's argmax + assembly (patchy.py:251-300) of those phi equals
+   the device's patch map except at colour-mass near-ties, counted;
+5. patch solves: fixed-point residual of the device's value field under the
+   state constraint of the device's patch map, and the contraction bound --
+   <= 1e-8 (fp64) / 1e-4 (fp32), the north_star bar; no node unreached that the
+   oracle reaches (and vice versa), targets 0, blocked nodes unreached.
+
+Each test prints one ``CERT {json}`` line with every residual and count.
+``PHJ_CERT_N`` (e.g. 129) shrinks every config for a quick run.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import time
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import has_gpu
+from oracle import pipeline as O
+import oracle_cases as C
+
+pytestmark = pytest.mark.gpu
+
+if has_gpu():
+    from paper_1109_3577_b200 import _lib, configs, patchy
+    from paper_1109_3577_b200.solver import feedback_internal, unreach_threshold
+
+SMALL = int(os.environ.get("PHJ_CERT_N", "0"))
+
+
+def _np(t: torch.Tensor) -> np.ndarray:
+    return t.detach().cpu().numpy().reshape(-1).astype(np.float64)
+
+
+def _workload(name: str, dtype: str, rule: str):
+    kw = {"dtype": dtype, "rule": rule}
+    if SMALL:
+        if name == "c4":
+            kw.update(nxy=SMALL, nth=max(16, SMALL // 2))
+        else:
+            kw["n"] = SMALL
+    return configs.CONFIGS[name](**kw)
+
+
+def certify(name: str, dtype: str = "float64", rule: str = "kruzkov"):
+    t_start = time.perf_counter()
+    w = _workload(name, dtype, rule)
+    spec, pcfg, cfg = w.spec, w.pcfg, w.cfg
+    f64 = dtype == "float64"
+    bar = 1e-8 if f64 else 1e-4
+    tie_gap = 1e-12 if f64 else 1e-5
+    color_tol = 1e-12 if f64 else 1e-6
+    fplan, cplan = patchy.make_plans(spec, pcfg)
+    fine = C.from_workload(w, "fine")
+    coarse = C.from_workload(w, "coarse")
+    fg, cg = fine.grid, coarse.grid
+    out = {"config": name, "dtype": dtype, "rule": rule, "fine": list(fg.shape)}
+    _, sent, unreach = O.rule_consts(rule)
+
+    # 1. coarse solve (deterministic block-Jacobi, patchy.coarse_cfg)
+    vc, cst = patchy.solve_full_internal(cplan, patchy.coarse_cfg(cfg))
+    vc_u = _np(cplan.to_user(vc))
+    lab_c = np.where(coarse.kind() == O.KIND_TARGET, O.TARGET,
+                     np.where(coarse.kind() == O.KIND_OBSTACLE, O.OBSTACLE, 0)).astype(np.int32)
+    rc = O.residual(vc_u, coarse, lab_c, rule=rule)
+    umax_c = float(vc_u[cg.interior_flat()][vc_u[cg.interior_flat()] < unreach].max())
+    bc = O.contraction_bound(coarse, rule, rc.r, umax_c)
+    out["coarse"] = {"sweeps": cst.sweeps, "residual": rc.r, "bound": bc,
+                     "missed": rc.missed, "spurious": rc.spurious, "certified": rc.n_certified}
+    assert (rc.missed, rc.spurious, rc.bad_target, rc.bad_blocked) == (0, 0, 0, 0), rc
+    assert bc <= bar, out
+
+    # 2. lift (device vs oracle on the same coarse field)
+    vf = patchy.lift_internal(cplan, vc, fplan, rule, dtype)
+    lift_d = _np(fplan.to_user(vf))
+    lift_o = O.lift(coarse, vc_u, fine, rule=rule)
+    fi = fg.interior_flat()
+    dl = float(np.abs(lift_d[fi] - lift_o[fi]).max())
+    out["lift_max_diff"] = dl
+    assert dl <= (0.0 if f64 else 1e-6), out
+
+    # 3. feedback on the device's lifted field
+    fb_i, _ = feedback_internal(fplan, vf, rule=rule, dtype=dtype)
+    fb_d = fplan.serial_to_user(fb_i).cpu().numpy().astype(np.int32)
+    fb_o, gaps, _ = O.feedback(lift_d, fine, rule=rule)
+    fdiff = fb_d != fb_o
+    ties = gaps < tie_gap
+    out["feedback"] = {"diffs": int(fdiff.sum()), "ties": int(ties.sum()),
+                       "diffs_off_ties": int((fdiff & ~ties).sum())}
+    assert not np.any(fdiff & ~ties), out
+    del fb_o, gaps
+
+    # 4. transport to a tight tol, then argmax + assembly
+    parts = patchy._resolve_parts(pcfg, spec, fplan.grid, fplan)
+    R = len(parts)
+    allp = np.concatenate([np.asarray(p, dtype=np.int64) for p in parts])
+    flat = fplan.user_serials_to_internal_flat(allp)
+    bnd = np.cumsum([0] + [len(p) for p in parts])
+    parts_flat = [flat[bnd[i]:bnd[i + 1]] for i in range(R)]
+    tsched = cfg.schedule if (fg.dim == 2 or patchy.TRANSPORT_ASYNC_3D) else "jacobi"
+    pdt = torch.float32 if (not f64 and patchy.TRANSPORT_PHI_FP32) else torch.float64
+    limit = 10 * max(fg.shape)
+    phi, _, csw, _ = patchy.transport_internal(fplan, fb_i, parts_flat, color_tol, limit,
+                                               tsched, pdt)
+    ni = fg.n_interior
+    best_val, second, best_idx = np.zeros(ni), np.zeros(ni), np.zeros(ni, dtype=np.int32)
+    r_phi = 0.0
+    for j in range(R):
+        pj = _np(fplan.to_user(phi[j]))
+        rj, n_movers = O.transport_residual(pj, fine, fb_d)
+        r_phi = max(r_phi, rj)
+        v = pj[fi]
+        take = v > best_val
+        second = np.where(take, best_val, np.maximum(second, v))
+        best_val[take] = v[take]
+        best_idx[take] = j
+    mask_o = lift_d[fi] >= unreach
+    col_o, unc_o = O.assemble_sparse(best_val, best_idx, R, mask_o, fg, fine.kind())
+    thr = unreach_threshold(rule)
+    bv_d, bi_d = patchy.argmax_batched(fplan.gs, phi, R, ni, fplan.device)
+    del phi
+    mask_d = patchy.plan_interior_serial(fplan, vf) >= thr
+    color, n_unc, _, lab = patchy.assemble_internal(fplan.gs, bv_d, bi_d, R, mask_d, fplan.kind,
+                                                    ni, fplan.device)
+    col_d = fplan.serial_to_user(color).cpu().numpy()
+    ldiff = col_d != col_o
+    near = (best_val - second) < (1e-9 if f64 else 1e-5)
+    out["transport"] = {"colours": R, "sweeps": [int(x) for x in csw], "movers": n_movers,
+                        "residual": r_phi, "color_tol": color_tol,
+                        "label_diffs": int(ldiff.sum()), "near_ties": int(near.sum()),
+                        "label_diffs_off_ties": int((ldiff & ~near).sum()),
+                        "uncovered": [int(n_unc), int(unc_o.size)]}
+    assert all(x > 0 for x in csw), out
+    assert r_phi <= 10 * color_tol, out
+    assert not np.any(ldiff & ~near), out
+
+    # 5. patch solves on the device's patch map
+    val, pstats, warns, pinfo = patchy.solve_patches_internal(fplan, color, lab, R, pcfg, cfg, vf)
+    v_u = _np(fplan.to_user(val))
+    rv = O.residual(v_u, fine, col_d, rule=rule)
+    live = col_d >= 0
+    umax = float(v_u[fi][live & (v_u[fi] < unreach)].max()) if live.any() else 0.0
+    bv = O.contraction_bound(fine, rule, rv.r, umax)
+    out["value"] = {"residual": rv.r, "bound": bv, "bar": bar, "certified": rv.n_certified,
+                    "missed": rv.missed, "spurious": rv.spurious,
+                    "bad_target": rv.bad_target, "bad_blocked": rv.bad_blocked,
+                    "patch_equivalent_sweeps": [int(s.sweeps) for s in pstats],
+                    "executed_evals": int(pinfo["performed"])}
+    out["seconds"] = round(time.perf_counter() - t_start, 1)
+    print("CERT " + json.dumps(out))
+    if os.environ.get("PHJ_CERT_LOG"):
+        with open(os.environ["PHJ_CERT_LOG"], "a") as fh:
+            fh.write(json.dumps(out) + "\n")
+    assert not warns, warns
+    assert (rv.missed, rv.spurious, rv.bad_target, rv.bad_blocked) == (0, 0, 0, 0), out
+    assert bv <= bar, out
+    return out
+
+
+def test_c2_fp64_certified():
+    certify("c2", "float64")
+
+
+def test_c2_fp32_certified():
+    certify("c2", "float32")
+
+
+def test_c2_reference_rule_certified():
+    certify("c2", "float64", "reference")
+
+
+def test_c3_fp64_certified():
+    certify("c3", "float64")
+
+
+def test_c4_fp64_certified():
+    certify("c4", "float64")
+
+
+def test_c5_fp64_certified():
+    certify("c5", "float64")
+
+
+def test_c5_fp32_certified():
+    certify("c5", "float32")
