@@ -214,13 +214,26 @@ def test_coarse_stage_is_deterministic_block_jacobi():
         ["async"] * 5
 
 
+def _header_fields(struct: str):
+    """Field names of a struct typedef in include/phj.h, in order."""
+    import re
+
+    src = open(os.path.join(ROOT, "include", "phj.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    body = src[src.index(f"typedef struct {struct} {{"):]
+    body = body[body.index("{") + 1:body.index(f"}} {struct};")]
+    names = []
+    for decl in body.split(";"):
+        decl = decl.strip()
+        if decl:
+            names.append(re.findall(r"([A-Za-z_][A-Za-z0-9_]*)\s*(?:\[[^\]]*\])?$", decl)[0])
+    return names
+
+
 def test_solve_args_layout_matches_header():
-    # the ctypes mirrors carry the async / transport fields in header order
-    names = [f[0] for f in _lib.SolveArgs._fields_]
-    assert names[-4:] == ["options", "act_tol", "inner_sweeps", "stream"]
-    tnames = [f[0] for f in _lib.TransportArgs._fields_]
-    assert tnames[-7:] == ["options", "inner_sweeps", "phi_dtype", "seed_flat", "seed_col",
-                           "n_seed", "stream"]
+    # the ctypes mirrors carry every field of the C structs in header order
+    assert [f[0] for f in _lib.SolveArgs._fields_] == _header_fields("phj_solve_args")
+    assert [f[0] for f in _lib.TransportArgs._fields_] == _header_fields("phj_transport_args")
 
 
 def test_vectorised_stencil_weights_bit_identical():
