@@ -129,17 +129,28 @@ class CpuPort:
         del X
         self.pr, self.g, self.threads = pr, g, threads
         self.u = O.init_field(pr, "reference")
+        self.u_in = self.u.copy()           # Jacobi input, allocated once
+        self.kind = pr.kind()
         self.hard = pr.hard_base()
         self.n = og.n_interior
         self.rate = None
 
     def sweep(self, lo: int, hi: int):
-        """One Jacobi sweep of serials [lo, hi); returns (evals, seconds)."""
+        """One Jacobi sweep of serials [lo, hi) (og_sweep, _kernels.py:18-106
+        semantics); returns (evals, seconds)."""
+        import ctypes
+
+        O = self.O
+        L = O.lib()
         order = np.arange(lo, hi, dtype=np.int64)
+        mc, nr, ne = ctypes.c_double(), ctypes.c_int64(), ctypes.c_int64()
         t0 = time.perf_counter()
-        _, _, ne = self.O.sweep(self.u, self.pr, order, rule="reference", mode="jacobi",
-                                hard=self.hard, nthreads=self.threads)
-        return ne, time.perf_counter() - t0
+        L.og_sweep(ctypes.byref(self.pr.grid.struct), ctypes.byref(self.pr._dyn),
+                   self.u.ctypes.data, self.u_in.ctypes.data, order.ctypes.data, order.size,
+                   self.kind.ctypes.data, None, None, self.hard.ctypes.data, None,
+                   O.SENTINEL, O.RULE_REF, self.threads, ctypes.byref(mc), ctypes.byref(nr),
+                   ctypes.byref(ne))
+        return ne.value, time.perf_counter() - t0
 
     def sample(self, seconds: float):
         """A slab of consecutive serials in the middle of the grid sized for

@@ -15,7 +15,7 @@
  *                        solver.extract_feedback    solver.py:413-443
  *   phj_transport        _kernels.transport_batch   _kernels.py:170-204,
  *                        patchy.transport_color     patchy.py:183-219
- *   phj_lift             grid.interpolate_many      grid.py:446-465 (patchy.py:146-148)
+ *   phj_lift             grid.interpolate_many      grid.py:242-261 (patchy.py:146-148)
  *   phj_argmax_update,   patchy.assemble_patches    patchy.py:236-301
  *   phj_assemble_*
  *   phj_classify         solver.classify_nodes      solver.py:101-108

@@ -7,11 +7,11 @@
  *
  * Followed line by line (all paths under /root/reference/pkg/src/patchyhjb/):
  *   og_point/og_foot  : solver.py:170-188 (F, |F|, h=k/|F|, foot=X+h F, cost)
- *                       grid.py:327-360 (locate_many: t, floor, clip, snap)
+ *                       grid.py:123-152 (locate_many: t, floor, clip, snap)
  *   og_sweep          : _kernels.py:18-106 (sweep_batch), GS in place or Jacobi
  *   og_feedback       : _kernels.py:109-167 (feedback_batch)
  *   og_transport      : _kernels.py:170-204 (transport_batch)
- *   og_lift           : grid.py:446-465 (interpolate_many, saturating)
+ *   og_lift           : grid.py:242-261 (interpolate_many, saturating)
  *
  * Extensions beyond the reference (documented in DESIGN.md):
  *   - rule OG_RULE_KRUZKOV: candidate value beta*I + (1-beta), beta=exp(-cost)
@@ -66,7 +66,7 @@ static void og_unravel(const og_grid* g, int64_t s, int64_t idx[3]) {
   }
 }
 
-/* flat extended index of interior serial s (grid.py:303-310) */
+/* flat extended index of interior serial s (grid.py:99-106) */
 static int64_t og_iflat(const og_grid* g, int64_t s) {
   int64_t idx[3];
   og_unravel(g, s, idx);
@@ -75,14 +75,14 @@ static int64_t og_iflat(const og_grid* g, int64_t s) {
   return f;
 }
 
-/* node coordinates: lo + i*spacing (grid.py:293-301) */
+/* node coordinates: lo + i*spacing (grid.py:89-97) */
 static void og_point(const og_grid* g, int64_t s, double X[3]) {
   int64_t idx[3];
   og_unravel(g, s, idx);
   for (int ax = 0; ax < g->dim; ++ax) X[ax] = g->lo[ax] + (double)idx[ax] * g->spacing[ax];
 }
 
-/* locate_many for one point (grid.py:341-356): ext-cell + snapped locals */
+/* locate_many for one point (grid.py:138-152): ext-cell + snapped locals */
 static void og_locate(const og_grid* g, const double P[3], int64_t cell[3], double loc[3]) {
   for (int ax = 0; ax < g->dim; ++ax) {
     double t = (P[ax] - g->ext_lo[ax]) / g->spacing[ax];
@@ -426,7 +426,7 @@ double og_transport(const og_grid* g, double* phi, const double* phi_in,
 
 /*
  * Saturating multilinear lift of a coarse field onto fine interior nodes
- * (interpolate_many, grid.py:446-465, used at patchy.py:146-148).  Corner
+ * (interpolate_many, grid.py:242-261, used at patchy.py:146-148).  Corner
  * sums follow numpy's reduction order: sequential for 4 terms, the pairwise
  * tree for 8 (np.add.reduce over a length-8 contiguous row).
  */
@@ -484,10 +484,11 @@ void og_lift(const og_grid* gc, const double* uc, const og_grid* gf, double* out
  * cnt[3] = blocked nodes with u < unreach
  * cnt[4] = free patch nodes with u < unreach (the certified set)
  * cnt[5] = candidate evaluations
+ * missed_list (optional, missed_cap entries): serials of the missed nodes
  */
 void og_residual(const og_grid* g, const og_dyn* dy, const double* u, const uint8_t* kind,
                  const int32_t* lab_ext, double unreach, int rule, int nthreads,
-                 double* out, int64_t* cnt) {
+                 double* out, int64_t* cnt, int64_t* missed_list, int64_t missed_cap) {
   const int64_t N = g->shape[0] * g->shape[1] * (g->dim == 3 ? g->shape[2] : 1);
   const int ncorner = 1 << g->dim;
   double rmax = 0.0;
@@ -535,7 +536,14 @@ void og_residual(const og_grid* g, const og_dyn* dy, const double* u, const uint
         if (v < best) best = v;
       }
       if (u[fi] >= unreach) {
-        if (best < unreach) missed += 1;
+        if (best < unreach) {
+          int64_t k;
+#ifdef _OPENMP
+#pragma omp atomic capture
+#endif
+          k = missed++;
+          if (missed_list && k < missed_cap) missed_list[k] = s;
+        }
         continue;
       }
       if (best >= unreach) { spurious += 1; continue; }

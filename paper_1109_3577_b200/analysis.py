@@ -186,3 +186,80 @@ def trace_trajectory(field: NodeField, spec, start, max_steps=None) -> Trajector
     if x.shape != (field.grid.dim,):
         raise ValueError(f"start must be a {field.grid.dim}-vector")
     return trace_trajectories(field, spec, x[None, :], max_steps)[0]
+
+
+# -- exports (analysis.py:140-238): host-side text formatting of one D2H copy --
+
+
+def _interior_host(field: NodeField) -> np.ndarray:
+    g = field.grid
+    vals = field.values
+    vals = vals.cpu().numpy() if isinstance(vals, torch.Tensor) else np.asarray(vals)
+    return vals.reshape(g.ext_shape)[tuple(slice(1, 1 + m) for m in g.shape)]
+
+
+def _first_axis_fastest(a: np.ndarray) -> np.ndarray:
+    return np.asarray(a).ravel(order="F")
+
+
+def _coordinate_columns(grid) -> list:
+    mesh = np.meshgrid(*[grid.axis_nodes(ax) for ax in range(grid.dim)], indexing="ij")
+    return [_first_axis_fastest(m) for m in mesh]
+
+
+def _export_rows(obj):
+    """(grid, values first-axis-fastest, value format, column name)."""
+    from .patchy import PatchMap
+
+    if isinstance(obj, PatchMap):
+        c = obj.color.cpu().numpy() if isinstance(obj.color, torch.Tensor) else obj.color
+        return obj.grid, _first_axis_fastest(np.asarray(c).reshape(obj.grid.shape)), "%d", "patch"
+    vals = _first_axis_fastest(_interior_host(obj)).copy()
+    return obj.grid, vals, "%.9g", "value"
+
+
+def export_field(obj, path, fmt: str = "csv") -> None:
+    """Write a value field or patch map as CSV or legacy ASCII VTK
+    (analysis.py:159-174).  CSV: one row per interior node, first coordinate
+    fastest, 9 significant digits, unreachable values as ``inf`` (patch maps:
+    their integer codes).  VTK: STRUCTURED_POINTS with the raw values."""
+    if fmt not in ("csv", "vtk"):
+        raise ValueError(f"unknown export format {fmt!r}")
+    grid, vals, vfmt, name = _export_rows(obj)
+    if fmt == "csv":
+        if name == "value":
+            vals[vals >= 0.5 * obj.sentinel] = np.inf
+        cols = _coordinate_columns(grid)
+        header = ",".join(f"x{i + 1}" for i in range(grid.dim)) + f",{name}"
+        np.savetxt(path, np.column_stack(cols + [vals]), fmt=["%.9g"] * grid.dim + [vfmt],
+                   delimiter=",", header=header, comments="")
+        return
+    pad = 3 - grid.dim
+    dims = list(grid.shape) + [1] * pad
+    origin = [float(x) for x in grid.lo] + [0.0] * pad
+    spacing = [float(x) for x in grid.spacing] + [1.0] * pad
+    scalar = "SCALARS patch int 1" if name == "patch" else "SCALARS value float 1"
+    lines = [("%d" % v) if name == "patch" else ("%.9g" % v) for v in vals]
+    head = ["# vtk DataFile Version 3.0", "minimum-time value field", "ASCII",
+            "DATASET STRUCTURED_POINTS", "DIMENSIONS {} {} {}".format(*dims),
+            "ORIGIN {:.9g} {:.9g} {:.9g}".format(*origin),
+            "SPACING {:.9g} {:.9g} {:.9g}".format(*spacing), f"POINT_DATA {vals.size}",
+            scalar, "LOOKUP_TABLE default"]
+    with open(path, "w") as fh:
+        fh.write("\n".join(head + lines) + "\n")
+
+
+def read_field_csv(path, grid=None):
+    """Read an exported CSV back (analysis.py:194-211): ``(points, values)``
+    without a grid, else a device NodeField with ``inf`` rows at the
+    sentinel."""
+    data = np.atleast_2d(np.genfromtxt(path, delimiter=",", skip_header=1))
+    points, values = data[:, :-1], data[:, -1]
+    if grid is None:
+        return points, values
+    field = NodeField(grid)
+    shaped = values.reshape(grid.shape, order="F")
+    vals = np.where(np.isfinite(shaped), shaped, field.sentinel).reshape(-1)
+    idx = torch.as_tensor(grid.interior_flat(), device=field.values.device)
+    field.flat[idx] = torch.as_tensor(vals, dtype=field.values.dtype, device=field.values.device)
+    return field

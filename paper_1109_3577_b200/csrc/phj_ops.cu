@@ -53,7 +53,7 @@ __device__ inline int64_t iflat(const phj_grid& g, const int c[3]) {
   return f;
 }
 
-// node coordinate lo + i*spacing with no FMA contraction (grid.py:293-295)
+// node coordinate lo + i*spacing with no FMA contraction (grid.py:89-91)
 __device__ inline double coord(const phj_grid& g, int ax, int i) {
   return __dadd_rn(g.lo[ax], __dmul_rn((double)i, g.spacing[ax]));
 }
@@ -67,7 +67,7 @@ inline int grid_blocks(int64_t n, int per = 256) {
 
 // ---------------------------------------------------------------------------
 // lift: saturating multilinear interpolation of the coarse field at fine
-// nodes (grid.py:446-465).  Locate/weights/sum orders reproduce numpy's
+// nodes (grid.py:242-261).  Locate/weights/sum orders reproduce numpy's
 // (sequential 4-term sum, pairwise 8-term tree) with explicit _rn intrinsics.
 template <typename T>
 __device__ inline T t_mul(T a, T b);

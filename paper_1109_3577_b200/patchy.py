@@ -209,7 +209,7 @@ def solve_full_internal(plan: StencilPlan, cfg: SolverConfig, work: Optional[tor
 
 def lift_internal(cplan: StencilPlan, vc: torch.Tensor, fplan: StencilPlan, rule: str,
                   dtype: str) -> torch.Tensor:
-    """Saturating lift onto the fine grid (grid.py:446-465, patchy.py:145-148)."""
+    """Saturating lift onto the fine grid (grid.py:242-261, patchy.py:145-148)."""
     vf = torch.full(fplan.int_ext, unreached_value(rule), dtype=vc.dtype, device=vc.device)
     thr = unreach_threshold(rule)
     _lib.check(_lib.load().phj_lift(ctypes_ref(cplan.gs), ctypes_ref(fplan.gs), _dtype_id(dtype),
@@ -775,7 +775,9 @@ def _resolve_parts(pcfg: PatchyConfig, spec: ProblemSpec, grid: Grid, plan=None)
     the plan)."""
     if pcfg.parts is not None and not callable(pcfg.parts):
         return [np.asarray(p, dtype=np.int64) for p in pcfg.parts]
-    key = ("parts", id(pcfg.parts), pcfg.n_patches)
+    # the callable itself is the key (kept alive by the cache): an id() of a
+    # collected callable could be reused by a new one
+    key = ("parts", pcfg.parts, pcfg.n_patches)
     cache = getattr(plan, "_parts_cache", None) if plan is not None else None
     if cache is not None and key in cache:
         return cache[key]

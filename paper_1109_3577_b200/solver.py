@@ -669,6 +669,131 @@ def solve(field: NodeField, spec: ProblemSpec, node_set=None,
     return st
 
 
+@dataclass
+class CandidateEvaluation:
+    """One (node, control) evaluation of the relaxation functional
+    (solver.py:92-98)."""
+
+    control_index: int
+    step_h: float
+    foot: np.ndarray
+    value: float
+
+
+def _node_serial(grid: Grid, index) -> int:
+    return int(index) if np.ndim(index) == 0 else grid.index_to_serial(index)
+
+
+def _ext_mask(grid: Grid, active_set) -> Optional[np.ndarray]:
+    """Flat ext-layout bool mask from an ext/flat array or a predicate over
+    interior-relative multi-indices (solver.py:291-305)."""
+    if active_set is None:
+        return None
+    if callable(active_set):
+        g = grid.ghost_width
+        idx = np.indices(grid.ext_shape).reshape(grid.dim, -1).T - g
+        return np.array([bool(active_set(tuple(int(i) for i in row))) for row in idx])
+    arr = active_set.cpu().numpy() if isinstance(active_set, torch.Tensor) else np.asarray(
+        active_set)
+    return arr.reshape(-1).astype(bool)
+
+
+def evaluate_candidates(field: NodeField, spec: ProblemSpec, index, active_set=None,
+                        frozen: Optional[NodeField] = None,
+                        eps_speed: Optional[float] = None) -> list:
+    """All admissible candidate evaluations at ONE node (solver.py:308-363):
+    the single-node inspection path of the reference, not the sweep.
+
+    The node's 2^d x (controls) corner values are gathered from the device
+    field in one copy; locate / weights follow grid.py:123-152, 227-239
+    (``Grid.locate_many``); a foot leaning with nonzero weight on a ghost or
+    obstacle corner, or on a corner outside ``active_set`` without ``frozen``
+    data, evaluates to the sentinel; otherwise value = sum w * corner + h *
+    running cost (1 for minimum time)."""
+    grid = field.grid
+    serial = _node_serial(grid, index)
+    x = grid.interior_points()[serial]
+    controls = np.asarray(spec.control_set.controls, dtype=float)
+    F = np.stack([np.asarray(spec.dynamics(x[None, :], a), dtype=float)[0] for a in controls])
+    speeds = np.array([float(np.linalg.norm(f)) for f in F])
+    if eps_speed is None:
+        eps_speed = 1.0e-12 * float(speeds.max())
+    ok = np.nonzero(speeds >= eps_speed)[0]
+    if ok.size == 0:
+        return []
+    h = grid.k_step / speeds[ok]
+    feet = x[None, :] + h[:, None] * F[ok]
+    cell, local = grid.locate_many(feet)
+    corners = grid.cell_flat_base(cell)[:, None] + grid.corner_offsets[None, :]
+    w = _reference_weights(local)
+    dev = field.values.device
+    idx = torch.as_tensor(corners.reshape(-1), device=dev)
+    cv = field.flat[idx].cpu().numpy().reshape(corners.shape)
+    fv = None if frozen is None else frozen.flat[idx].cpu().numpy().reshape(corners.shape)
+    hard = np.ones(grid.n_ext, dtype=bool)
+    kind = classify_nodes(grid, spec)
+    hard[grid.interior_flat()] = kind == KIND_OBSTACLE
+    act = _ext_mask(grid, active_set)
+    out = []
+    for i, c in enumerate(ok):
+        value = 0.0
+        blocked = False
+        for k in range(corners.shape[1]):
+            wc = w[i, k]
+            if wc == 0.0:
+                continue
+            f2 = corners[i, k]
+            if hard[f2]:
+                blocked = True
+                break
+            if act is None or act[f2]:
+                value += wc * cv[i, k]
+            elif fv is not None:
+                value += wc * fv[i, k]
+            else:
+                blocked = True
+                break
+        if blocked:
+            value = field.sentinel
+        else:
+            cost = 1.0 if spec.running_cost is None else float(
+                np.asarray(spec.running_cost(x[None, :], controls[c]))[0])
+            value += h[i] * cost
+        out.append(CandidateEvaluation(int(c), float(h[i]), feet[i], float(value)))
+    return out
+
+
+def _reference_weights(local: np.ndarray) -> np.ndarray:
+    from .grid import interpolation_weights
+
+    return interpolation_weights(local)
+
+
+def relax_node(field: NodeField, spec: ProblemSpec, index, active_set=None,
+               frozen: Optional[NodeField] = None, eps_speed: Optional[float] = None):
+    """One node relaxation, pure (solver.py:366-394): ``(new_value,
+    control_index)``; target -> (0, None), obstacle -> (sentinel, None); the
+    best live candidate (ties to the lowest control index) only if it beats
+    the current value."""
+    grid = field.grid
+    serial = _node_serial(grid, index)
+    x = grid.interior_points()[serial][None, :]
+    if spec.obstacles is not None and bool(spec.obstacles.contains(x)[0]):
+        return field.sentinel, None
+    if bool(spec.target.contains(x)[0]):
+        return 0.0, None
+    cands = evaluate_candidates(field, spec, serial, active_set=active_set, frozen=frozen,
+                                eps_speed=eps_speed)
+    live = [c for c in cands if c.value < 0.5 * field.sentinel]
+    current = float(field.flat[int(grid.interior_flat()[serial])])
+    if not live:
+        return current, None
+    best = min(live, key=lambda c: (c.value, c.control_index))
+    if best.value >= current:
+        return current, None
+    return best.value, best.control_index
+
+
 def extract_feedback(field: NodeField, spec: ProblemSpec, table: Optional[StencilPlan] = None,
                      strategy: Optional[ExecutionStrategy] = None, allowed=None, *,
                      rule: str = "reference", dtype: str = "float64"):
