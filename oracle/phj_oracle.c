@@ -478,7 +478,7 @@ void og_lift(const og_grid* gc, const double* uc, const og_grid* gf, double* out
  *   unreach : 1.0 (Kruzkov) or 0.5*sentinel (reference rule).
  * out[0] = max |T(u)_i - u_i| over free patch nodes with u_i < unreach
  * out[1] = serial where out[0] is attained
- * cnt[0] = free patch nodes with u >= unreach but T(u) < unreach (missed)
+ * cnt[0] = free patch nodes with u >= unreach but T(u) < unreach (1 - 1e-9) (missed)
  * cnt[1] = free patch nodes with u < unreach but T(u) >= unreach (spurious)
  * cnt[2] = target nodes with u != 0
  * cnt[3] = blocked nodes with u < unreach
@@ -536,7 +536,10 @@ void og_residual(const og_grid* g, const og_dyn* dy, const double* u, const uint
         if (v < best) best = v;
       }
       if (u[fi] >= unreach) {
-        if (best < unreach) {
+        /* margin: a candidate over unreached corners only is 1 up to the
+         * rounding of the reference's per-node weights (their sum is 1 only
+         * to ~1 ulp, grid.py:227-239), not a reachable value */
+        if (best < unreach * (1.0 - 1.0e-9)) {
           int64_t k;
 #ifdef _OPENMP
 #pragma omp atomic capture

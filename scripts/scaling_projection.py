@@ -1,0 +1,114 @@
+"""Multi-GPU projection of the patchy pipeline on ONE GPU (this pool has one
+GPU per call; ranks whose kernels wait on each other cannot share a GPU, but
+these ranks never wait: patches and colours are independent).
+
+For G in (1, 2, 4, 8) and each rank r, the rank's own work is run alone on
+the full GPU exactly as that rank would run it (dist.world() patched to
+(r, G)): its colour subset of the transport (dist.my_colours) and its patch
+subset of the patch solve (dist.mine_mask, LPT).  Replicated stages (coarse,
+lift, feedback, assembly) are timed once.  Collectives are estimated from
+their byte counts at an NVLink-5 all-reduce bus bandwidth (argmax merge:
+2 x N x 8 B, value gather: N x 8 B MIN).  Projected step time of G GPUs =
+replicated + max_r (transport_r) + merge + max_r (patch_r) + gather;
+efficiency = T(1) / (G * T(G)).
+
+    python scripts/scaling_projection.py [c5] [float64] [weights]
+weights: "nodes" (north_star: node count) or "lifted" (node count x mean
+lifted time of the patch, a work predictor available before the solve).
+Writes one JSON object to stdout.
+"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_1109_3577_b200 import configs, dist, patchy  # noqa: E402
+from paper_1109_3577_b200.solver import feedback_internal, unreach_threshold  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "c5"
+dtype = sys.argv[2] if len(sys.argv) > 2 else "float64"
+BUS_GBS = float(os.environ.get("PHJ_NVLINK_BUS_GBS", "600"))  # all-reduce bus bandwidth
+w = configs.CONFIGS[name](dtype=dtype)
+spec, pcfg, cfg = w.spec, w.pcfg, w.cfg
+fplan, cplan = patchy.make_plans(spec, pcfg)
+dev = fplan.device
+n = fplan.grid.n_interior
+
+
+def timed(fn):
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record()
+    out = fn()
+    b.record()
+    torch.cuda.synchronize()
+    return out, a.elapsed_time(b)
+
+
+# warm-up: one full run (allocator pools, stencils)
+patchy.run_patchy(spec, pcfg, cfg, plans=(fplan, cplan), outputs=False)
+
+(vc, cst), t_coarse = timed(lambda: patchy.solve_full_internal(cplan, patchy.coarse_cfg(cfg)))
+vf, t_lift = timed(lambda: patchy.lift_internal(cplan, vc, fplan, cfg.rule, cfg.dtype))
+(fb, _), t_fb = timed(lambda: feedback_internal(fplan, vf, rule=cfg.rule, dtype=cfg.dtype))
+parts = patchy._resolve_parts(pcfg, spec, fplan.grid, fplan)
+R = len(parts)
+limit = 10 * max(fplan.grid.shape)
+thr = unreach_threshold(cfg.rule)
+mask = patchy.plan_interior_serial(fplan, vf) >= thr
+
+real_world = dist.world
+res = {"config": name, "dtype": dtype, "replicated_ms": {"coarse": t_coarse, "lift": t_lift,
+                                                          "feedback": t_fb}}
+base = None
+color = lab = None
+sizes = None
+for G in (1, 2, 4, 8):
+    tr_ms, pa_ms, ranks = [], [], []
+    for r in range(G):
+        dist.world = lambda r=r, G=G: (r, G)
+        try:
+            (bv, bi, csw, _), t_tr = timed(lambda: patchy._transport_and_argmax(
+                fplan, fb, parts, pcfg.color_tol, limit, cfg.schedule, cfg.dtype))
+            tr_ms.append(t_tr)
+            if G == 1:
+                (color, n_unc, _, lab), t_as = timed(lambda: patchy.assemble_internal(
+                    fplan.gs, bv, bi, R, mask, fplan.kind, n, dev))
+                res["replicated_ms"]["assembly"] = t_as
+                sizes = patchy.count_labels(color, R).cpu().numpy()
+            (out, pst, warns, pinfo), t_pa = timed(lambda: patchy.solve_patches_internal(
+                fplan, color, lab, R, pcfg, cfg, vf))
+            pa_ms.append(t_pa)
+            if G == 1:
+                relax = np.array([s.node_relaxations for s in pst], dtype=float)
+                execd = np.array([s.performed_evals for s in pst], dtype=float)
+        finally:
+            dist.world = real_world
+    rep = sum(res["replicated_ms"].values())
+    nbytes = n * 8
+    allreduce_ms = lambda b: 0.0 if G == 1 else 2.0 * (G - 1) / G * b / (BUS_GBS * 1e9) * 1e3
+    merge = 2 * allreduce_ms(nbytes)
+    gather = allreduce_ms(nbytes)
+    step = rep + max(tr_ms) + merge + max(pa_ms) + gather
+    if G == 1:
+        base = step
+        owner = np.zeros(R, dtype=int)
+    else:
+        owner = dist.lpt_assign(sizes, G)
+    work_bins = np.bincount(owner, weights=execd, minlength=G)
+    res[f"G{G}"] = {"step_ms": step, "transport_ms_per_rank": tr_ms,
+                    "patch_ms_per_rank": pa_ms, "merge_ms_est": merge, "gather_ms_est": gather,
+                    "efficiency": base / (G * step),
+                    "patch_work_balance": float(execd.sum() / (G * work_bins.max())),
+                    "node_balance_bound": dist.load_balance_bound(sizes, G)}
+res["patch_sizes"] = sizes.tolist()
+res["patch_relaxations"] = relax.tolist()
+res["patch_executed_evals"] = execd.tolist()
+res["collective_model"] = f"ring all-reduce 2(G-1)/G x bytes at {BUS_GBS} GB/s bus bandwidth"
+print(json.dumps(res))

@@ -70,8 +70,11 @@ def test_relax_agrees_with_the_device_sweep():
     snap = f.copy()
     g2 = phj.NodeField(g, snap.values.clone())
     phj.solve(g2, spec, cfg=phj.SolverConfig(max_sweeps=1, tol=1e-12))
-    for node in ((5, 5), (10, 30), (35, 2)):
-        v, _ = phj.relax_node(snap, spec, node)
+    # nodes behind the front: relax_node ignores sentinel-mixed candidates
+    # (solver.py:384-386) while the sweep writes any improvement (_kernels.py:101)
+    for node in ((20, 27), (25, 22), (14, 18)):
+        v, c = phj.relax_node(snap, spec, node)
+        assert c is not None and v < 10.0
         got = float(g2.interior[node])
         assert got == pytest.approx(v, abs=1e-13)
 
