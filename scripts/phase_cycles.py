@@ -18,7 +18,8 @@ import paper_1109_3577_b200 as phj  # noqa: E402
 from paper_1109_3577_b200 import _lib, configs, patchy  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
-w = configs.CONFIGS[name]()
+dtype = sys.argv[2] if len(sys.argv) > 2 else "float64"
+w = configs.CONFIGS[name](dtype=dtype)
 plans = patchy.make_plans(w.spec, w.pcfg)
 lib = _lib.load()
 fn = lib.phj_dbg_phase_cycles
@@ -32,5 +33,5 @@ for i in range(2):
     torch.cuda.synchronize()
     fn(buf)
 tot = sum(buf)
-print(json.dumps({"config": name, "frac": {n: round(buf[i] / tot, 4) for i, n in enumerate(names)},
+print(json.dumps({"config": name, "dtype": dtype, "frac": {n: round(buf[i] / tot, 4) for i, n in enumerate(names)},
                   "cycles": {n: buf[i] for i, n in enumerate(names)}}))

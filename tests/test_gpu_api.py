@@ -70,13 +70,21 @@ def test_relax_agrees_with_the_device_sweep():
     snap = f.copy()
     g2 = phj.NodeField(g, snap.values.clone())
     phj.solve(g2, spec, cfg=phj.SolverConfig(max_sweeps=1, tol=1e-12))
-    # nodes behind the front: relax_node ignores sentinel-mixed candidates
-    # (solver.py:384-386) while the sweep writes any improvement (_kernels.py:101)
-    for node in ((20, 27), (25, 22), (14, 18)):
+    # nodes the sweep improved to finite values, and converged finite nodes;
+    # relax_node ignores sentinel-mixed candidates (solver.py:384-386) while
+    # the sweep writes any improvement (_kernels.py:101), so compare < 10
+    before = snap.interior.cpu().numpy()
+    after = g2.interior.cpu().numpy()
+    moved = np.argwhere((after < before) & (after < 10.0))
+    still = np.argwhere((after == before) & (after < 10.0) & (after > 0.0))
+    assert len(moved) > 0 and len(still) > 0
+    for node in list(map(tuple, moved[:: max(1, len(moved) // 6)])):
         v, c = phj.relax_node(snap, spec, node)
-        assert c is not None and v < 10.0
-        got = float(g2.interior[node])
-        assert got == pytest.approx(v, abs=1e-13)
+        assert c is not None
+        assert float(after[node]) == pytest.approx(v, abs=1e-13)
+    for node in list(map(tuple, still[:: max(1, len(still) // 3)])):
+        v, c = phj.relax_node(snap, spec, node)
+        assert c is None and v == float(before[node])
 
 
 def test_csv_rows_are_first_axis_fastest(tmp_path):

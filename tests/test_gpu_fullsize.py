@@ -46,7 +46,10 @@ import oracle_cases as C
 pytestmark = pytest.mark.gpu
 
 if has_gpu():
-    from paper_1109_3577_b200 import _lib, configs, patchy
+    import dataclasses
+
+    from paper_1109_3577_b200 import configs, patchy
+    from paper_1109_3577_b200.dynamics import Dubins
     from paper_1109_3577_b200.solver import feedback_internal, unreach_threshold
 
 SMALL = int(os.environ.get("PHJ_CERT_N", "0"))
@@ -128,7 +131,9 @@ def certify(name: str, dtype: str = "float64", rule: str = "kruzkov"):
     parts_flat = [flat[bnd[i]:bnd[i + 1]] for i in range(R)]
     tsched = cfg.schedule if (fg.dim == 2 or patchy.TRANSPORT_ASYNC_3D) else "jacobi"
     pdt = torch.float32 if (not f64 and patchy.TRANSPORT_PHI_FP32) else torch.float64
-    limit = 10 * max(fg.shape)
+    # config 4's Dubins transport contracts slowly: a larger sweep cap for
+    # the tight certificate tolerance (the workload itself stops at 1e-2)
+    limit = (40 if isinstance(spec.model, Dubins) else 10) * max(fg.shape)
     phi, _, csw, _ = patchy.transport_internal(fplan, fb_i, parts_flat, color_tol, limit,
                                                tsched, pdt)
     ni = fg.n_interior
@@ -159,9 +164,9 @@ def certify(name: str, dtype: str = "float64", rule: str = "kruzkov"):
                         "label_diffs": int(ldiff.sum()), "near_ties": int(near.sum()),
                         "label_diffs_off_ties": int((ldiff & ~near).sum()),
                         "uncovered": [int(n_unc), int(unc_o.size)]}
-    assert all(x > 0 for x in csw), out
-    assert r_phi <= 10 * color_tol, out
-    assert not np.any(ldiff & ~near), out
+    checks = [("transport converged", all(x > 0 for x in csw)),
+              ("transport residual <= 10 color_tol", r_phi <= 10 * color_tol),
+              ("labels equal off colour-mass near-ties", not np.any(ldiff & ~near))]
 
     # 5. patch solves on the device's patch map
     val, pstats, warns, pinfo = patchy.solve_patches_internal(fplan, color, lab, R, pcfg, cfg, vf)
@@ -175,11 +180,27 @@ def certify(name: str, dtype: str = "float64", rule: str = "kruzkov"):
                     "bad_target": rv.bad_target, "bad_blocked": rv.bad_blocked,
                     "patch_equivalent_sweeps": [int(s.sweeps) for s in pstats],
                     "executed_evals": int(pinfo["performed"])}
+    if not f64:
+        # fp32: |v32 - v*| <= |v32 - v64| + |v64 - v*| with v64 the fp64 device
+        # solve on the SAME patch map, itself certified by its residual
+        cfg64 = dataclasses.replace(cfg, dtype="float64", activity_tol=None)
+        val64, _, _, _ = patchy.solve_patches_internal(fplan, color, lab, R, pcfg, cfg64, None)
+        v64 = _np(fplan.to_user(val64))
+        r64 = O.residual(v64, fine, col_d, rule=rule)
+        b64 = O.contraction_bound(fine, rule, r64.r, umax)
+        d = float(np.abs(v_u[fi] - v64[fi])[live].max()) if live.any() else 0.0
+        out["value"]["fp64_same_labels"] = {"residual": r64.r, "bound": b64, "max_diff": d,
+                                            "bound_via_fp64": b64 + d,
+                                            "missed": r64.missed, "spurious": r64.spurious}
+        bv = min(bv, b64 + d)
+        out["value"]["bound_used"] = bv
     out["seconds"] = round(time.perf_counter() - t_start, 1)
     print("CERT " + json.dumps(out))
     if os.environ.get("PHJ_CERT_LOG"):
         with open(os.environ["PHJ_CERT_LOG"], "a") as fh:
             fh.write(json.dumps(out) + "\n")
+    for what, ok in checks:
+        assert ok, (what, out)
     assert not warns, warns
     assert (rv.missed, rv.spurious, rv.bad_target, rv.bad_blocked) == (0, 0, 0, 0), out
     assert bv <= bar, out
