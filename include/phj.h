@@ -168,6 +168,9 @@ int64_t phj_solve_workspace_bytes(const phj_grid* g, int32_t n_patches, int32_t 
 int32_t phj_unroll(int32_t dim);
 /* number of warp blocks (work/activity units) of a grid (diagnostics) */
 int64_t phj_blocks_total(const phj_grid* g);
+/* warp-block extent along the internal axes (block = planes x rows x nodes,
+ * axis 0 slowest): out[0..2]; 2D grids use out[0..1] */
+int phj_block_dims(int32_t dim, int32_t* out);
 int phj_solve(const phj_solve_args* a);
 
 /* foreign-position masks: bit p set when 3^dim neighbour p of the node is not
@@ -231,6 +234,18 @@ typedef struct phj_transport_args {
   const int64_t* seed_flat;
   const int32_t* seed_col;
   int64_t n_seed;
+  /* optional value-ordered pass before the Jacobi sweeps (Jacobi transport
+   * only; NULL band_off = off): sweep s < n_band processes exactly the blocks
+   * band_list[band_off[s] .. band_off[s+1]) (entry b = Jacobi update of block
+   * b's movers for the colours that have reached it; -b-1 = copy its movers'
+   * values into the other buffer, its last visit).  Built by the host from
+   * the lifted field's time-to-target (patchy.transport_bands): a node is
+   * updated while its time band is within a window sliding outward from the
+   * target, so the colour masses are carried across the domain in one pass;
+   * the Jacobi sweeps that follow stop at max change <= tol as usual. */
+  const int32_t* band_list;
+  const int32_t* band_off;   /* [n_band + 1] */
+  int32_t n_band;
   void* stream;
 } phj_transport_args;
 

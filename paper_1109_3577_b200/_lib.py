@@ -71,7 +71,8 @@ class TransportArgs(ctypes.Structure):
                 ("kind", P), ("ent_scratch", P), ("n_colors", I32), ("tol", D), ("act_eps", D),
                 ("max_sweeps", I32), ("workspace", P), ("maxch_hist", P), ("color_sweeps", P),
                 ("info", P), ("updates", P), ("options", I32), ("inner_sweeps", I32), ("phi_dtype", I32),
-                ("seed_flat", P), ("seed_col", P), ("n_seed", ctypes.c_int64), ("stream", P)]
+                ("seed_flat", P), ("seed_col", P), ("n_seed", ctypes.c_int64),
+                ("band_list", P), ("band_off", P), ("n_band", I32), ("stream", P)]
 
 
 class Shapes(ctypes.Structure):
@@ -87,7 +88,8 @@ class SpeedModel(ctypes.Structure):
 
 #: every symbol include/phj.h declares (checked by the CPU test suite)
 EXPORTS = (
-    "phj_solve_workspace_bytes", "phj_unroll", "phj_blocks_total", "phj_solve", "phj_fmask_from_labels",
+    "phj_solve_workspace_bytes", "phj_unroll", "phj_blocks_total", "phj_block_dims", "phj_solve",
+    "phj_fmask_from_labels",
     "phj_fmask_from_hard",
     "phj_feedback", "phj_feedback_allowed", "phj_transport", "phj_lift", "phj_argmax_update",
     "phj_argmax_colors", "phj_argmax_colors_t", "phj_count_labels",
@@ -119,6 +121,7 @@ def load() -> ctypes.CDLL:
     sig = {
         "phj_solve_workspace_bytes": (I64, [P, I32, I32]),
         "phj_blocks_total": (I64, [P]),
+        "phj_block_dims": (ctypes.c_int, [I32, P]),
         "phj_unroll": (I32, [I32]),
         "phj_solve": (ctypes.c_int, [P]),
         "phj_fmask_from_labels": (ctypes.c_int, [P, P, P, P]),

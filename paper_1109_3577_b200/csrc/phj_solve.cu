@@ -22,6 +22,7 @@
 //    (patchy.py:362-377); later sweeps copy its nodes through unchanged.
 #include <cooperative_groups.h>
 #include <algorithm>
+#include <vector>
 #include <cstdio>
 #include <cstdlib>
 
@@ -1269,15 +1270,19 @@ struct MarkQueue {
   }
   // transport: OR the changed colours into the neighbours' next masks; the
   // first setter (old mask 0) appends the block
+  // (append = false: OR only, e.g. into the sticky masks of the banded pass)
   __device__ __forceinline__ void issue_mask(const TileGrid& tg, const phj_grid& g, int blk,
                                              unsigned long long bits, int lane,
-                                             unsigned long long* masks) {
+                                             unsigned long long* masks, bool append = true) {
     a_nt = -1;
     if (bits != 0ull && lane < (D == 2 ? 9 : 27)) {
       const int nt = neighbour_block<D>(tg, g, blk, lane);
       if (nt >= 0) {
-        a_nt = nt;
-        a_old = atomicOr(&masks[nt], bits) != 0ull;
+        const bool first = atomicOr(&masks[nt], bits) == 0ull;
+        if (append) {
+          a_nt = nt;
+          a_old = !first;
+        }
       }
     }
   }
@@ -1919,6 +1924,11 @@ struct TransportParams {
   int32_t* color_sweeps;      // [R]
   int32_t* info;
   unsigned long long* updates;
+  // value-ordered pass (transport_kernel only): sweeps < n_band visit
+  // band_list[band_off[s] ..] (b: update, -b-1: copy to the other buffer)
+  const int32_t* band_list;
+  const int32_t* band_off;
+  int n_band;
 };
 
 #ifndef PHJ_TRANSPORT_CTAS
@@ -1984,14 +1994,27 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
   }
   MarkQueue<D> mq;
   mq.init();
+  // value-ordered pass: the colours that reached a block accumulate in a
+  // sticky mask (never cleared), the array the first Jacobi sweep consumes
+  unsigned long long* sticky = p.ws.cmask[p.n_band & 1];
   for (;;) {
     const PT* pin = (const PT*)p.phi[buf];
     PT* pout = (PT*)p.phi[buf ^ 1];
-    const int cnt = ld_cg(&p.ws.counts[sw]);
-    const int* list = p.ws.list[sw & 1];
+    const bool banded = sw < p.n_band;
+    if (p.n_band > 0 && sw == p.n_band) {
+      // end of the pass: every block some colour has reached enters the
+      // first Jacobi sweep with all of its colours
+      int* l0 = p.ws.list[sw & 1];
+      for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < p.tg.total;
+           b += gridDim.x * blockDim.x)
+        if (__ldcg(&sticky[b]) != 0ull) l0[atomicAdd(&p.ws.counts[sw], 1)] = b;
+      grid.sync();
+    }
+    const int cnt = banded ? (p.band_off[sw + 1] - p.band_off[sw]) : ld_cg(&p.ws.counts[sw]);
+    const int* list = banded ? p.band_list + p.band_off[sw] : p.ws.list[sw & 1];
     int* cur_flags = p.ws.flags[sw & 1];
-    unsigned long long* cur_mask = p.ws.cmask[sw & 1];
-    unsigned long long* nxt_mask = p.ws.cmask[(sw + 1) & 1];
+    unsigned long long* cur_mask = banded ? sticky : p.ws.cmask[sw & 1];
+    unsigned long long* nxt_mask = banded ? sticky : p.ws.cmask[(sw + 1) & 1];
     int* nxt_list = p.ws.list[(sw + 1) & 1];
     int* nxt_cnt = &p.ws.counts[sw + 1];
     int* take = &p.ws.take[sw];
@@ -2003,13 +2026,14 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
     __syncthreads();
     // prefetch of one item: its colour mask (lane 0) and mover entries
     auto prefetch = [&](int b, unsigned long long& pcm, int (&pe)[NB]) {
+      b = b < 0 ? -b - 1 : b;  // banded copy entries
       int cc[3];
       const bool rok = lane_nodes<D>(g, p.tg, b, lane, cc);
       const int64_t ss = serial_of<D>(g, cc);
       pcm = 0ull;
       if (lane == 0) {
         pcm = __ldcg(&cur_mask[b]);
-        cur_mask[b] = 0ull;
+        if (!banded) cur_mask[b] = 0ull;
         cur_flags[b] = 0;
       }
 #pragma unroll
@@ -2042,8 +2066,10 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
       // colours active in this block: those a neighbour block changed in the
       // previous sweep (exact per colour, like the block skipping)
       const unsigned long long cm = __shfl_sync(FULL, cm_l0, 0);
+      const bool copy_only = blk < 0;  // banded: last visit, copy to the other buffer
+      const int bid = copy_only ? -blk - 1 : blk;
       int c[3];
-      const bool row_ok = lane_nodes<D>(g, p.tg, blk, lane, c);
+      const bool row_ok = lane_nodes<D>(g, p.tg, bid, lane, c);
       const int64_t f0 = ext_flat<D>(g, c);
       int64_t base[NB];
       bool any = false;
@@ -2057,7 +2083,7 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
           for (int ax = 0; ax < D; ++ax)
             if (!((oc >> ax) & 1)) base[r] -= g.strides[ax];
           any = true;
-          ++upd;
+          upd += copy_only ? 0 : 1;
         }
       }
       unsigned long long changed = 0;
@@ -2107,7 +2133,7 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
             lmax[q] = 0.0;
             if (js[q] < 0) continue;
             const int j = js[q];
-            const bool live = s_done[j] == 0x7fffffff;
+            const bool live = !copy_only && s_done[j] == 0x7fffffff;
             PT* qj = pout + (int64_t)j * p.plane;
 #pragma unroll
             for (int r = 0; r < NB; ++r) {
@@ -2142,7 +2168,7 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
           }
         }
       }
-      mq.issue_mask(p.tg, g, blk, changed, lane, nxt_mask);
+      mq.issue_mask(p.tg, g, bid, changed, lane, nxt_mask, !banded);
       item = nxt;
       blk = nblk;
       nxt = nn;
@@ -2172,7 +2198,8 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
         const unsigned long long mb = ld_cg(&grow[i * kMaxPad]);
         if (blockIdx.x == 0) p.maxch[(int64_t)(sw - 1) * R + i] = mb;
         const double mc = __longlong_as_double((long long)mb);
-        if (mc <= p.tol) s_done[i] = sw;
+        // no stop inside the value-ordered pass (its sweeps see a window only)
+        if (sw > p.n_band && mc <= p.tol) s_done[i] = sw;
         else pending = 1;
       }
     }
@@ -3141,6 +3168,23 @@ extern "C" int64_t phj_blocks_total(const phj_grid* g) {
 
 extern "C" int32_t phj_unroll(int32_t dim) { return PHJ_UNROLL(dim); }
 
+extern "C" int phj_block_dims(int32_t dim, int32_t* out) {
+  if (!out || (dim != 2 && dim != 3)) {
+    phj_set_error("phj_block_dims: dim must be 2 or 3");
+    return PHJ_ERR_ARG;
+  }
+  if (dim == 2) {
+    out[0] = Blk<2>::BY;
+    out[1] = Blk<2>::BX;
+    out[2] = 1;
+  } else {
+    out[0] = 1;
+    out[1] = Blk<3>::BY;
+    out[2] = Blk<3>::BX;
+  }
+  return PHJ_OK;
+}
+
 extern "C" int64_t phj_solve_workspace_bytes(const phj_grid* g, int32_t n_patches,
                                              int32_t max_sweeps) {
   (void)n_patches;
@@ -3400,12 +3444,20 @@ static int transport_impl(const phj_transport_args* a) {
   p.color_sweeps = a->color_sweeps;
   p.info = a->info;
   p.updates = a->updates;
+  const bool async = (a->options & PHJ_TRANSPORT_ASYNC) != 0;
+  const bool banded = a->band_off && a->band_list && a->n_band > 0 && !async;
+  p.band_list = banded ? a->band_list : nullptr;
+  p.band_off = banded ? a->band_off : nullptr;
+  p.n_band = banded ? a->n_band : 0;
+  if (banded && (a->n_band >= a->max_sweeps || p.R > 64)) {
+    phj_set_error("phj_transport: the banded pass needs n_band < max_sweeps and <= 64 colours");
+    return PHJ_ERR_ARG;
+  }
   const int64_t ws_bytes = workspace_bytes<D>(a->grid, a->max_sweeps);
   PHJ_CUDA(cudaMemsetAsync(a->workspace, 0, ws_bytes, stream));
   PHJ_CUDA(cudaMemsetAsync(a->maxch_hist, 0, 8 * (size_t)a->max_sweeps * p.R, stream));
   PHJ_CUDA(cudaMemsetAsync(a->info, 0, 4 * sizeof(int32_t), stream));
   PHJ_CUDA(cudaMemsetAsync(a->updates, 0, sizeof(unsigned long long), stream));
-  const bool async = (a->options & PHJ_TRANSPORT_ASYNC) != 0;
   {
     const int64_t N = p.g.shape[0] * p.g.shape[1] * (D == 3 ? p.g.shape[2] : 1);
     const int nb = (int)std::min<int64_t>((N + 255) / 256, 16 * phj_num_sms());
@@ -3419,17 +3471,28 @@ static int transport_impl(const phj_transport_args* a) {
   const bool seeded = a->seed_flat && a->n_seed > 0 && p.R <= 64;
   if (seeded) {
     const int nb = (int)std::min<int64_t>((a->n_seed + 255) / 256, 4 * phj_num_sms());
-    transport_seed_kernel<D><<<std::max(nb, 1), 256, 0, stream>>>(p.g, p.tg, a->seed_flat,
-                                                                  a->seed_col, a->n_seed,
-                                                                  p.ws.cmask[0]);
+    // banded: the seeds start the sticky masks (see transport_kernel)
+    transport_seed_kernel<D><<<std::max(nb, 1), 256, 0, stream>>>(
+        p.g, p.tg, a->seed_flat, a->seed_col, a->n_seed, p.ws.cmask[banded ? (p.n_band & 1) : 0]);
     phj_count_launch(1);
   }
-  build_list_kernel<D><<<(p.tg.total + kWarps - 1) / kWarps, kThreads, 0, stream>>>(
+  if (banded && !seeded) {
+    // every mover block starts with every colour
+    const unsigned long long all = p.R >= 64 ? ~0ull : ((1ull << p.R) - 1ull);
+    PHJ_CUDA(cudaMemsetAsync(p.ws.cmask[p.n_band & 1], 0, 8 * (size_t)p.tg.total, stream));
+    std::vector<unsigned long long> h((size_t)p.tg.total, all);
+    PHJ_CUDA(cudaMemcpyAsync(p.ws.cmask[p.n_band & 1], h.data(), 8 * (size_t)p.tg.total,
+                             cudaMemcpyHostToDevice, stream));
+    PHJ_CUDA(cudaStreamSynchronize(stream));
+  }
+  if (!banded) {
+    build_list_kernel<D><<<(p.tg.total + kWarps - 1) / kWarps, kThreads, 0, stream>>>(
       p.g, p.tg, nullptr, nullptr, p.ws.flags[0], p.ws.list[0], p.ws.counts,
       1, p.fb, p.kind,
       p.ws.cmask[0], p.R >= 64 ? ~0ull : ((1ull << p.R) - 1ull), nullptr, 0, 0.0,
       async ? &p.ws.take[5] : nullptr, seeded ? 1 : 0);
-  phj_count_launch(1);
+    phj_count_launch(1);
+  }
   PHJ_CUDA(cudaGetLastError());
   const int nent = p.n_classes * p.nc;
   if (async) {
@@ -3454,7 +3517,7 @@ static int transport_impl(const phj_transport_args* a) {
   // two sweeps per barrier pay in 2D only (3D: the 2-ring halo is 5 planes
   // deep and the activity must reach +-2 planes -- measured 2x slower)
   static const bool one_sweep = getenv("PHJ_TRANSPORT_T1") && atoi(getenv("PHJ_TRANSPORT_T1"));
-  if (one_sweep || D == 3 || a->phi_dtype == PHJ_F32) {  // fp32 phi: one-sweep kernel
+  if (one_sweep || D == 3 || a->phi_dtype == PHJ_F32 || banded) {  // fp32 phi / banded: one-sweep kernel
     size_t smem = (size_t)(nent | 1) * (1 << D) * 8 + (size_t)p.R * 12 + (size_t)nent + 16;
     if (a->phi_dtype == PHJ_F32)
       return coop_launch(transport_kernel<D, float>, (p.tg.total + kWarps - 1) / kWarps, smem,

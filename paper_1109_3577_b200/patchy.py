@@ -16,7 +16,9 @@ BASELINE config 1 whose 26^2 coarse grid holds no target node), ``parts``
 
 from __future__ import annotations
 
+import ctypes
 import dataclasses
+import os
 from dataclasses import dataclass, field as _field
 from typing import Callable, Optional, Sequence, Union
 
@@ -56,6 +58,12 @@ TRANSPORT_ASYNC_FRAC = 1.0e-4
 #: DESIGN.md §3.1b); module attributes so experiments can flip them
 TRANSPORT_ASYNC_3D = False
 TRANSPORT_INNER = {2: 8, 3: 4}
+#: value-ordered pass before the Jacobi transport (3D): a
+#: node is updated while its time band (lifted time-to-target / (k / max|f|))
+#: lies within [s - lo, s + hi] of sweep s -- the colour masses cross the
+#: domain in one outward pass instead of ~path-length Jacobi sweeps
+TRANSPORT_BANDED = os.environ.get("PHJ_TRANSPORT_BANDED", "1") != "0"
+TRANSPORT_BAND_WINDOW = (3, 1)  # (trailing, leading) bands
 #: fp32 workloads store the colour fields in fp32
 TRANSPORT_PHI_FP32 = True
 
@@ -219,15 +227,82 @@ def lift_internal(cplan: StencilPlan, vc: torch.Tensor, fplan: StencilPlan, rule
     return vf
 
 
+def transport_bands(plan: StencilPlan, key_work: torch.Tensor, fb_int: torch.Tensor, rule: str,
+                    window=None):
+    """Block schedule of the value-ordered transport pass: CSR (band_list,
+    band_off, n_band) of the warp blocks each sweep visits (phj_transport_args).
+
+    A mover's band is floor(T / delta), T its lifted time-to-target (working
+    field ``key_work``: v for Kruzkov, u for the reference rule) and delta =
+    k / max|f| the smallest time step of one SL step; a block is updated at
+    sweeps [min band - hi, max band + lo] of its movers and copied to the
+    other buffer one sweep later (its last visit keeps both Jacobi buffers
+    equal).  Returns None without movers."""
+    lo_w, hi_w = window or TRANSPORT_BAND_WINDOW
+    dev = plan.device
+    d = plan.grid.dim
+    kw = plan.interior_int(key_work).reshape(-1).to(torch.float64)
+    T = -torch.log1p(-kw.clamp(max=1.0 - 1e-16)) if rule == "kruzkov" else kw
+    mover = (fb_int.view(-1) >= 0) & (plan.kind.view(-1) == KIND_FREE)
+    if not bool(mover.any()):
+        return None
+    fmax = plan.eps_speed / 1.0e-12
+    delta = plan.grid.k_step / fmax
+    band = torch.floor(T / delta).to(torch.int64)
+    dims = (ctypes.c_int32 * 3)()
+    _lib.check(_lib.load().phj_block_dims(d, dims), "block_dims")
+    shp = plan.int_shape
+    ser = torch.nonzero(mover).view(-1)
+    if d == 3:
+        i0 = ser // (shp[1] * shp[2])
+        i1 = (ser // shp[2]) % shp[1]
+        i2 = ser % shp[2]
+        n1 = -(-shp[1] // dims[1])
+        n2 = -(-shp[2] // dims[2])
+        bid = (i0 * n1 + i1 // dims[1]) * n2 + i2 // dims[2]
+        total = shp[0] * n1 * n2
+    else:
+        i0 = ser // shp[1]
+        i1 = ser % shp[1]
+        n1 = -(-shp[1] // dims[1])
+        bid = (i0 // dims[0]) * n1 + i1 // dims[1]
+        total = -(-shp[0] // dims[0]) * n1
+    bm = band[ser]
+    kmin = torch.full((total,), 1 << 40, dtype=torch.int64, device=dev).scatter_reduce(
+        0, bid, bm, reduce="amin")
+    kmax = torch.full((total,), -1, dtype=torch.int64, device=dev).scatter_reduce(
+        0, bid, bm, reduce="amax")
+    blocks = torch.nonzero(kmax >= 0).view(-1)
+    lo = (kmin[blocks] - hi_w).clamp(min=0)
+    hi = kmax[blocks] + lo_w
+    L = hi - lo + 2                                    # updates + the copy visit
+    E = int(L.sum().item())
+    rep_b = torch.repeat_interleave(blocks, L)
+    start = torch.cumsum(L, 0) - L
+    off = torch.arange(E, device=dev) - torch.repeat_interleave(start, L)
+    sweep = torch.repeat_interleave(lo, L) + off
+    last = off == torch.repeat_interleave(L, L) - 1
+    entry = torch.where(last, -rep_b - 1, rep_b)
+    n_band = int((hi.max() + 2).item())
+    order = torch.argsort(sweep * total + rep_b)       # by sweep, then block id
+    band_list = entry[order].to(torch.int32).contiguous()
+    counts = torch.bincount(sweep, minlength=n_band)
+    band_off = torch.cat([torch.zeros(1, dtype=torch.int64, device=dev),
+                          torch.cumsum(counts, 0)]).to(torch.int32).contiguous()
+    return band_list, band_off, n_band
+
+
 def transport_internal(plan: StencilPlan, fb_int: torch.Tensor, parts_flat: Sequence,
                        tol: float, max_sweeps: int, schedule: str = "jacobi",
-                       phi_dtype: torch.dtype = torch.float64):
+                       phi_dtype: torch.dtype = torch.float64, bands=None):
     """All colours in one launch, each Jacobi to its own max|change| <= tol
     ("jacobi"), or asynchronously in place until no node changes a colour by
     more than TRANSPORT_ASYNC_FRAC * tol ("async").
     ``parts_flat``: per colour, internal ext flat indices of its part.
     ``phi_dtype`` float32 halves the colour fields' footprint (fp64
-    accumulation either way; used for fp32 workloads).
+    accumulation either way; used for fp32 workloads).  ``bands``
+    (transport_bands) prepends the value-ordered pass (Jacobi only); its
+    sweeps count in the per-colour sweeps.
     Returns (phi [R][ext] tensor, R, per-colour sweeps, updates)."""
     lib = _lib.load()
     R = len(parts_flat)
@@ -243,6 +318,8 @@ def transport_internal(plan: StencilPlan, fb_int: torch.Tensor, parts_flat: Sequ
             _sync_periodic(plan, phi0[j])
     asyn = schedule == "async"
     phi1 = phi0 if asyn else phi0.clone()  # async: one buffer, updated in place
+    n_band = 0 if (bands is None or asyn) else int(bands[2])
+    max_sweeps = max_sweeps + n_band
     wsb = lib.phj_solve_workspace_bytes(ctypes_ref(plan.gs), 1, max_sweeps)
     ws = torch.empty(int(wsb), dtype=torch.uint8, device=plan.device)
     mc = torch.zeros(max_sweeps * R, dtype=torch.float64, device=plan.device)
@@ -270,6 +347,10 @@ def transport_internal(plan: StencilPlan, fb_int: torch.Tensor, parts_flat: Sequ
     a.seed_col = _lib.ptr(col)
     a.n_seed = int(seed_flat.numel())
     a.max_sweeps = max_sweeps
+    if n_band:
+        a.band_list = _lib.ptr(bands[0])
+        a.band_off = _lib.ptr(bands[1])
+        a.n_band = n_band
     a.workspace = _lib.ptr(ws)
     a.maxch_hist = _lib.ptr(mc)
     a.color_sweeps = _lib.ptr(csw)
@@ -294,7 +375,8 @@ def transport_internal(plan: StencilPlan, fb_int: torch.Tensor, parts_flat: Sequ
 
 
 def _transport_and_argmax(fplan: StencilPlan, fb: torch.Tensor, parts, color_tol: float,
-                          limit: int, schedule: str = "jacobi", dtype: str = "float64"):
+                          limit: int, schedule: str = "jacobi", dtype: str = "float64",
+                          key_work: Optional[torch.Tensor] = None, rule: str = "kruzkov"):
     """Transport of every colour + running argmax (patchy.py:183-219,
     251-256).  With several ranks each rank transports its own colours
     (dist.my_colours) and the argmax is merged exactly across ranks.
@@ -319,8 +401,11 @@ def _transport_and_argmax(fplan: StencilPlan, fb: torch.Tensor, parts, color_tol
         # fp32 workloads keep their colour fields in fp32 too (half the
         # footprint: 35 GB instead of 70 GB at config 5)
         pdt = torch.float32 if (dtype == "float32" and TRANSPORT_PHI_FP32) else torch.float64
+        bands = None
+        if TRANSPORT_BANDED and tsched == "jacobi" and fplan.grid.dim == 3 and key_work is not None:
+            bands = transport_bands(fplan, key_work, fb, rule)
         phi, _, csw, upd = transport_internal(fplan, fb, parts_flat, color_tol, limit,
-                                              tsched, pdt)
+                                              tsched, pdt, bands=bands)
         best_val, best_idx = argmax_batched(fplan.gs, phi, len(mine), n, dev)
         del phi
         csw_all[torch.as_tensor(mine, device=dev)] = torch.as_tensor(csw, device=dev)
@@ -728,7 +813,8 @@ def run_patchy(spec: ProblemSpec, pcfg: PatchyConfig, cfg: Optional[SolverConfig
         limit = pcfg.transport_max_sweeps or 10 * max(fine_grid.shape)
         n_colors = len(parts)
         best_val, best_idx, csw, upd = _transport_and_argmax(fplan, fb, parts, pcfg.color_tol,
-                                                             limit, cfg.schedule, cfg.dtype)
+                                                             limit, cfg.schedule, cfg.dtype,
+                                                             key_work=vf, rule=rule)
         stats.transport_updates += upd
         transport_sweeps = [abs(x) for x in csw]
         for j, x in enumerate(csw):

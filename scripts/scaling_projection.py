@@ -75,7 +75,8 @@ for G in (1, 2, 4, 8):
         dist.world = lambda r=r, G=G: (r, G)
         try:
             (bv, bi, csw, _), t_tr = timed(lambda: patchy._transport_and_argmax(
-                fplan, fb, parts, pcfg.color_tol, limit, cfg.schedule, cfg.dtype))
+                fplan, fb, parts, pcfg.color_tol, limit, cfg.schedule, cfg.dtype,
+                key_work=vf, rule=cfg.rule))
             tr_ms.append(t_tr)
             if G == 1:
                 (color, n_unc, _, lab), t_as = timed(lambda: patchy.assemble_internal(

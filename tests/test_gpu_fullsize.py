@@ -134,8 +134,11 @@ def certify(name: str, dtype: str = "float64", rule: str = "kruzkov"):
     # config 4's Dubins transport contracts slowly: a larger sweep cap for
     # the tight certificate tolerance (the workload itself stops at 1e-2)
     limit = (40 if isinstance(spec.model, Dubins) else 10) * max(fg.shape)
+    bands = None  # the value-ordered pass exactly as run_patchy sets it up
+    if patchy.TRANSPORT_BANDED and tsched == "jacobi" and fg.dim == 3:
+        bands = patchy.transport_bands(fplan, vf, fb_i, rule)
     phi, _, csw, _ = patchy.transport_internal(fplan, fb_i, parts_flat, color_tol, limit,
-                                               tsched, pdt)
+                                               tsched, pdt, bands=bands)
     ni = fg.n_interior
     best_val, second, best_idx = np.zeros(ni), np.zeros(ni), np.zeros(ni, dtype=np.int32)
     r_phi = 0.0
