@@ -108,6 +108,15 @@ for G in (1, 2, 4, 8):
                     "efficiency": base / (G * step),
                     "patch_work_balance": float(execd.sum() / (G * work_bins.max())),
                     "node_balance_bound": dist.load_balance_bound(sizes, G)}
+# work predictors available before the patch solve (from the lifted field)
+col = color.long()
+live = col >= 0
+Tl = patchy.plan_interior_serial(fplan, vf).to(torch.float64)
+if cfg.rule == "kruzkov":
+    Tl = -torch.log1p(-Tl.clamp(max=1 - 1e-16))
+res["patch_sum_T"] = torch.bincount(col[live], weights=Tl[live], minlength=R).cpu().tolist()
+res["patch_max_T"] = torch.zeros(R, dtype=torch.float64, device=dev).scatter_reduce(
+    0, col[live], Tl[live], reduce="amax").cpu().tolist()
 res["patch_sizes"] = sizes.tolist()
 res["patch_relaxations"] = relax.tolist()
 res["patch_executed_evals"] = execd.tolist()
