@@ -151,6 +151,17 @@ typedef struct phj_solve_args {
    * the reference's per-patch SweepStats counters (solver.py:79-88) under both
    * schedules */
   unsigned long long* patch_counts;
+  /* optional value-ordered pass (NULL band_off = off):
+   * sweep s < n_band visits exactly the blocks band_list[band_off[s] ..
+   * band_off[s+1]) (entry b = relax block b, -b-1 = copy its nodes into the
+   * other buffer: its last visit), sweep n_band visits row n_band (every
+   * block of the pass) as an ordinary Jacobi sweep; per-patch stopping starts
+   * after it.  With PHJ_SOLVE_ASYNC the pass runs alone and the asynchronous
+   * relaxation continues from its result.  Rows come from the lifted field's
+   * time-to-target (patchy.band_schedule); n_band < max_sweeps. */
+  const int32_t* band_list;
+  const int32_t* band_off;   /* [n_band + 2] */
+  int32_t n_band;
   void* stream;               /* cudaStream_t */
 } phj_solve_args;
 

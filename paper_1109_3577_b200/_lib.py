@@ -58,7 +58,8 @@ class SolveArgs(ctypes.Structure):
                 ("workspace", P), ("patch_sweeps", P), ("maxch_hist", P), ("evals", P),
                 ("info", P), ("ao3_fb", P), ("ao3_mask", P), ("ao3_count", P),
                 ("ao3_words", I32), ("options", I32), ("act_tol", D), ("inner_sweeps", I32),
-                ("patch_counts", P), ("stream", P)]
+                ("patch_counts", P), ("band_list", P), ("band_off", P), ("n_band", I32),
+                ("stream", P)]
 
 
 SOLVE_NO_PRUNE = 1  # PHJ_SOLVE_NO_PRUNE

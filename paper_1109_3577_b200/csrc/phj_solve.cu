@@ -103,7 +103,17 @@ struct SolveParams {
   const unsigned long long* ao3_mask;
   const int32_t* ao3_count;
   int ao3_words;
+  // value-ordered pass (solve_kernel): sweeps < n_band visit band_list rows
+  // (b: relax block b, -b-1: copy its nodes to the other buffer); sweep
+  // n_band visits row n_band (every block of the pass) as a normal sweep;
+  // band_only ends the launch there (the asynchronous schedule continues)
+  const int32_t* band_list;
+  const int32_t* band_off;
+  int n_band;
+  int band_only;
 };
+
+__device__ __forceinline__ int entry_block(int e) { return e < 0 ? -e - 1 : e; }
 
 template <int D, typename T>
 struct StencilSmem {
@@ -994,7 +1004,8 @@ __device__ __forceinline__ int sweep_block(const SolveParams& p, const StencilSm
                                             unsigned long long* s_max, unsigned long long* gmax_row,
                                             unsigned long long& evals, unsigned long long& exec,
                                             unsigned long long& xreal, unsigned long long* s_pc,
-                                            PatchMax& pm, PhaseTimer& tm, const Hook& hook) {
+                                            PatchMax& pm, PhaseTimer& tm, const Hook& hook,
+                                            bool force_copy = false) {
   using B = Blk<D>;
   using S = TileShape<D>;
   using NS = NodeStage<D, T>;
@@ -1033,7 +1044,8 @@ __device__ __forceinline__ int sweep_block(const SolveParams& p, const StencilSm
     comp[r] = false;
     copy[r] = false;
     if (labv[r] >= 0) {
-      if (s_done[labv[r]] != 0x7fffffff || (COST == PHJ_COST_NODE && ncoef[r] < T(0))) {
+      if (force_copy || s_done[labv[r]] != 0x7fffffff ||
+          (COST == PHJ_COST_NODE && ncoef[r] < T(0))) {
         copy[r] = true;
       } else {
         comp[r] = true;
@@ -1365,8 +1377,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __gri
   for (;;) {
     const T* vin = (const T*)p.v[buf];
     T* vout = (T*)p.v[buf ^ 1];
-    const int cnt = ld_cg(&p.ws.counts[sw]);
-    const int* list = p.ws.list[sw & 1];
+    const bool banded = sw < p.n_band;               // value-ordered pass
+    const bool csr = p.n_band > 0 && sw <= p.n_band;  // list from the band schedule
+    const int cnt = csr ? (p.band_off[sw + 1] - p.band_off[sw]) : ld_cg(&p.ws.counts[sw]);
+    const int* list = csr ? p.band_list + p.band_off[sw] : p.ws.list[sw & 1];
     int* cur_flags = p.ws.flags[sw & 1];
     int* nxt_flags = p.ws.flags[(sw + 1) & 1];
     int* nxt_list = p.ws.list[(sw + 1) & 1];
@@ -1380,8 +1394,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __gri
     for (int i = threadIdx.x; i < nshared; i += blockDim.x) s_max[i] = 0ull;
     __syncthreads();
     int item = gwarp;
-    int blk = item < cnt ? __ldcg(&list[item]) : 0;
-    if (item < cnt) stage_block<D, T, COST>(p, vin, blk, wtile + stage * S::N, wnodes + stage, lane);
+    int blk = item < cnt ? __ldcg(&list[item]) : 0;  // raw entry (banded: -b-1 = copy)
+    if (item < cnt)
+      stage_block<D, T, COST>(p, vin, entry_block(blk), wtile + stage * S::N, wnodes + stage, lane);
     PatchMax pm{-1, 0.0};
 #if PHJ_EARLY_STAGE
     // block ids are read two ahead so the next block's staging can start as
@@ -1401,10 +1416,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __gri
       const int nblk = nxt < cnt ? __ldcg(&list[nxt]) : 0;
       if (lane == 0 && nxt < cnt) ticket = atomicAdd(take, 1);
 #endif
-      if (lane == 0) cur_flags[blk] = 0;
+      const bool copy_visit = blk < 0;
+      const int bid = entry_block(blk);
+      if (lane == 0) cur_flags[bid] = 0;
       if (warp_cls) {
         int bc[3];
-        decode_block<D>(p.tg, blk, bc);
+        decode_block<D>(p.tg, bid, bc);
         if (bc[0] != wcls) {
           __syncwarp();
           stage_class<D, T, RULE>(s, bc[0], p.nc, lane, p.oct_start, p.nzmask, p.weights, p.cost, p.ctrl);
@@ -1417,24 +1434,25 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __gri
       mq.store(nxt_list);
       mq.reserve(lane, nxt_cnt);
       if (nxt < cnt)
-        stage_block<D, T, COST>(p, vin, nblk, wtile + (stage ^ 1) * S::N, wnodes + (stage ^ 1),
-                                lane);
+        stage_block<D, T, COST>(p, vin, entry_block(nblk), wtile + (stage ^ 1) * S::N,
+                                wnodes + (stage ^ 1), lane);
       auto hook = []() {};
 #else
       auto hook = [&]() {
         mq.store(nxt_list);
         mq.reserve(lane, nxt_cnt);
         if (nxt < cnt)
-          stage_block<D, T, COST>(p, vin, nblk, wtile + (stage ^ 1) * S::N, wnodes + (stage ^ 1),
-                                  lane);
+          stage_block<D, T, COST>(p, vin, entry_block(nblk), wtile + (stage ^ 1) * S::N,
+                                  wnodes + (stage ^ 1), lane);
       };
 #endif
       tm.mark(1);
-      const int ch = sweep_block<D, T, RULE, COST>(p, s, blk, wtile + stage * S::N, wnodes + stage,
+      const int ch = sweep_block<D, T, RULE, COST>(p, s, bid, wtile + stage * S::N, wnodes + stage,
                                                     vout, s_done, s_max, gmax_row, evals, exec,
-                                                    xreal, s_pc, pm, tm, hook);
+                                                    xreal, s_pc, pm, tm, hook, copy_visit);
       ++blocks_done;
-      mq.issue(p.tg, p.g, blk, ch, lane, nxt_flags);
+      // the band schedule, not the activity, drives the pass
+      mq.issue(p.tg, p.g, bid, banded ? 0 : ch, lane, nxt_flags);
       tm.mark(6);
       __syncwarp();  // the buffers of this block are refilled two blocks later
       item = nxt;
@@ -1465,12 +1483,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __gri
         const unsigned long long mb = ld_cg(&gmax_row[i * kMaxPad]);
         if (blockIdx.x == 0) p.maxch[(int64_t)(sw - 1) * p.R + i] = mb;
         const double mc = __longlong_as_double((long long)mb);
-        if (mc <= p.tol) s_done[i] = sw;
+        // no per-patch stop inside the value-ordered pass (its sweeps see a
+        // window of the patch only)
+        if (sw > p.n_band && mc <= p.tol) s_done[i] = sw;
         else pending = 1;
       }
     }
     const int any_pending = __syncthreads_or(pending);
     tm.mark(7);
+    if (p.band_only && sw >= p.n_band) break;
     if (!any_pending || sw >= p.max_sweeps) break;
   }
 #ifdef PHJ_TIMING
@@ -3283,9 +3304,18 @@ static int solve_impl(const phj_solve_args* a) {
   p.ao3_mask = a->ao3_mask;
   p.ao3_count = a->ao3_count;
   p.ao3_words = a->ao3_words;
+  const bool async = (a->options & PHJ_SOLVE_ASYNC) != 0;
+  const bool banded = a->band_off && a->band_list && a->n_band > 0;
+  p.band_list = banded ? a->band_list : nullptr;
+  p.band_off = banded ? a->band_off : nullptr;
+  p.n_band = banded ? a->n_band : 0;
+  p.band_only = 0;
+  if (banded && a->n_band >= a->max_sweeps) {
+    phj_set_error("phj_solve: the band schedule needs n_band < max_sweeps");
+    return PHJ_ERR_ARG;
+  }
   const int64_t ws_bytes = workspace_bytes<D>(a->grid, a->max_sweeps);
   PHJ_CUDA(cudaMemsetAsync(a->workspace, 0, ws_bytes, stream));
-  const bool async = (a->options & PHJ_SOLVE_ASYNC) != 0;
   PHJ_CUDA(cudaMemsetAsync(a->maxch_hist, 0, sizeof(double) * (size_t)a->max_sweeps * a->n_patches,
                            stream));
   PHJ_CUDA(cudaMemsetAsync(a->evals, 0, 3 * sizeof(unsigned long long), stream));
@@ -3293,21 +3323,41 @@ static int solve_impl(const phj_solve_args* a) {
     PHJ_CUDA(cudaMemsetAsync(a->patch_counts, 0, 3 * sizeof(unsigned long long) * a->n_patches,
                              stream));
   PHJ_CUDA(cudaMemsetAsync(a->info, 0, 4 * sizeof(int32_t), stream));
-  // initial blocks: those that can move from the start field (exact: from
-  // the unreached start a block with no reached value within its 3^D
-  // neighbourhood reproduces itself)
-  build_list_kernel<D><<<(p.tg.total + kWarps - 1) / kWarps, kThreads, 0, stream>>>(
-      p.g, p.tg, p.lab, p.mine, p.ws.flags[0], p.ws.list[0], p.ws.counts, 0,
-      nullptr, nullptr,
-      nullptr, 0ull, a->v0, sizeof(T) == 4, RULE == PHJ_RULE_KRUZKOV ? 1.0 : 1.0e9,
-      async ? &p.ws.take[5] : nullptr);
-  phj_count_launch(1);
-  PHJ_CUDA(cudaGetLastError());
   size_t smem = (size_t)align_up(solve_stencil_bytes<D, T>(p.n_classes, p.nc) +
                                      (int64_t)((p.R + 1) / 2 * 2) * 4 +
                                      (int64_t)std::min(p.R, kSmemPatchReduce) * 8 * 4,
                                  16) +
                 (size_t)solve_tile_bytes<D, T>();
+  if (banded && async) {
+    // the value-ordered pass alone (cooperative Jacobi sweeps over the band
+    // schedule), then the asynchronous relaxation from its result: both
+    // buffers hold the pass's values (every block ends with a copy visit)
+    SolveParams pb = p;
+    pb.band_only = 1;
+    void* bargs[] = {(void*)&pb};
+    int rc = (D == 3 && p.n_classes > 1)
+                 ? coop_launch(solve_kernel<D, T, RULE, COST, D == 3>,
+                               (p.tg.total + kWarps - 1) / kWarps, smem, bargs, stream, nullptr)
+                 : coop_launch(solve_kernel<D, T, RULE, COST, false>,
+                               (p.tg.total + kWarps - 1) / kWarps, smem, bargs, stream, nullptr);
+    if (rc) return rc;
+    PHJ_CUDA(cudaMemsetAsync(a->workspace, 0, ws_bytes, stream));
+    p.n_band = 0;
+    p.band_list = nullptr;
+    p.band_off = nullptr;
+  }
+  // initial blocks: those that can move from the start field (exact: from
+  // the unreached start a block with no reached value within its 3^D
+  // neighbourhood reproduces itself)
+  if (!(banded && !async)) {
+    build_list_kernel<D><<<(p.tg.total + kWarps - 1) / kWarps, kThreads, 0, stream>>>(
+      p.g, p.tg, p.lab, p.mine, p.ws.flags[0], p.ws.list[0], p.ws.counts, 0,
+      nullptr, nullptr,
+      nullptr, 0ull, a->v0, sizeof(T) == 4, RULE == PHJ_RULE_KRUZKOV ? 1.0 : 1.0e9,
+      async ? &p.ws.take[5] : nullptr);
+    phj_count_launch(1);
+  }
+  PHJ_CUDA(cudaGetLastError());
   if (async) {
     const long long want = (long long)a->max_sweeps * (long long)p.tg.total;
     unsigned int budget = (unsigned int)std::min(want, (long long)0x7fffffff);

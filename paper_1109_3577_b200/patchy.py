@@ -64,6 +64,12 @@ TRANSPORT_INNER = {2: 8, 3: 4}
 #: domain in one outward pass instead of ~path-length Jacobi sweeps
 TRANSPORT_BANDED = os.environ.get("PHJ_TRANSPORT_BANDED", "1") != "0"
 TRANSPORT_BAND_WINDOW = (3, 1)  # (trailing, leading) bands
+#: value-ordered pass before the patch solves: the same
+#: band schedule over the patch nodes, keyed by the lifted field; the
+#: schedule (async / jacobi) then continues from its result
+SOLVE_BANDED = os.environ.get("PHJ_SOLVE_BANDED", "1") != "0"
+SOLVE_BAND_WINDOW = (6, 2)
+BAND_CAP_PER_NODE = 1.5
 #: fp32 workloads store the colour fields in fp32
 TRANSPORT_PHI_FP32 = True
 
@@ -227,32 +233,41 @@ def lift_internal(cplan: StencilPlan, vc: torch.Tensor, fplan: StencilPlan, rule
     return vf
 
 
-def transport_bands(plan: StencilPlan, key_work: torch.Tensor, fb_int: torch.Tensor, rule: str,
-                    window=None):
-    """Block schedule of the value-ordered transport pass: CSR (band_list,
-    band_off, n_band) of the warp blocks each sweep visits (phj_transport_args).
+def band_schedule(plan: StencilPlan, key_work: torch.Tensor, nodes: torch.Tensor, rule: str,
+                  window, final_row: bool = False):
+    """Block schedule of a value-ordered pass: CSR (band_list, band_off,
+    n_band) of the warp blocks each sweep visits (phj_transport_args /
+    phj_solve_args band fields).
 
-    A mover's band is floor(T / delta), T its lifted time-to-target (working
+    A node's band is floor(T / delta), T its lifted time-to-target (working
     field ``key_work``: v for Kruzkov, u for the reference rule) and delta =
-    k / max|f| the smallest time step of one SL step; a block is updated at
-    sweeps [min band - hi, max band + lo] of its movers and copied to the
-    other buffer one sweep later (its last visit keeps both Jacobi buffers
-    equal).  Returns None without movers."""
-    lo_w, hi_w = window or TRANSPORT_BAND_WINDOW
+    k / max|f| the smallest time step of one SL step; a block holding any of
+    ``nodes`` (bool per internal serial) is visited at sweeps [min band - hi,
+    max band + lo] of those nodes and copied to the other buffer one sweep
+    later (its last visit keeps both Jacobi buffers equal).  ``final_row``
+    appends row n_band with every block of the pass (the solve's first
+    ordinary sweep).  Returns None when ``nodes`` is empty."""
+    lo_w, hi_w = window
     dev = plan.device
     d = plan.grid.dim
     kw = plan.interior_int(key_work).reshape(-1).to(torch.float64)
     T = -torch.log1p(-kw.clamp(max=1.0 - 1e-16)) if rule == "kruzkov" else kw
-    mover = (fb_int.view(-1) >= 0) & (plan.kind.view(-1) == KIND_FREE)
-    if not bool(mover.any()):
+    if not bool(nodes.any()):
         return None
     fmax = plan.eps_speed / 1.0e-12
     delta = plan.grid.k_step / fmax
-    band = torch.floor(T / delta).to(torch.int64)
+    # at most BAND_CAP_PER_NODE x the longest grid axis bands (one sweep each):
+    # slow dynamics (Dubins turns) would otherwise need thousands of sweeps
+    Tn = torch.where(nodes.view(-1), T, torch.zeros_like(T))
+    t_max = float(Tn.max().item())
+    cap = BAND_CAP_PER_NODE * max(plan.int_shape)
+    if t_max / delta > cap:
+        delta = t_max / cap
+    band = torch.floor(T / delta).clamp(max=1 << 30).to(torch.int64)
     dims = (ctypes.c_int32 * 3)()
     _lib.check(_lib.load().phj_block_dims(d, dims), "block_dims")
     shp = plan.int_shape
-    ser = torch.nonzero(mover).view(-1)
+    ser = torch.nonzero(nodes.view(-1)).view(-1)
     if d == 3:
         i0 = ser // (shp[1] * shp[2])
         i1 = (ser // shp[2]) % shp[1]
@@ -284,12 +299,24 @@ def transport_bands(plan: StencilPlan, key_work: torch.Tensor, fb_int: torch.Ten
     last = off == torch.repeat_interleave(L, L) - 1
     entry = torch.where(last, -rep_b - 1, rep_b)
     n_band = int((hi.max() + 2).item())
+    if final_row:
+        entry = torch.cat([entry, blocks])
+        sweep = torch.cat([sweep, torch.full_like(blocks, n_band)])
+        rep_b = torch.cat([rep_b, blocks])
+    rows = n_band + (1 if final_row else 0)
     order = torch.argsort(sweep * total + rep_b)       # by sweep, then block id
     band_list = entry[order].to(torch.int32).contiguous()
-    counts = torch.bincount(sweep, minlength=n_band)
+    counts = torch.bincount(sweep, minlength=rows)
     band_off = torch.cat([torch.zeros(1, dtype=torch.int64, device=dev),
                           torch.cumsum(counts, 0)]).to(torch.int32).contiguous()
     return band_list, band_off, n_band
+
+
+def transport_bands(plan: StencilPlan, key_work: torch.Tensor, fb_int: torch.Tensor, rule: str,
+                    window=None):
+    """band_schedule over the transport's movers (feedback >= 0, free)."""
+    mover = (fb_int.view(-1) >= 0) & (plan.kind.view(-1) == KIND_FREE)
+    return band_schedule(plan, key_work, mover, rule, window or TRANSPORT_BAND_WINDOW)
 
 
 def transport_internal(plan: StencilPlan, fb_int: torch.Tensor, parts_flat: Sequence,
@@ -574,8 +601,15 @@ def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Te
     block_counts = None
     if pcfg.bc_mode == STATE_CONSTRAINT:
         fmask = plan.fmask_from_labels(lab)
+        bands = None
+        if SOLVE_BANDED and lifted_work is not None and not pcfg.warm_start:
+            nodes = (color >= 0) & (plan.kind.view(-1) == KIND_FREE)
+            if mine is not None:
+                nodes &= mine.bool()[color.clamp(min=0).long()]
+            bands = band_schedule(plan, lifted_work, nodes, rule, SOLVE_BAND_WINDOW,
+                                  final_row=True)
         res = device_solve(plan, work, lab, fmask, n_patches, rule=rule, dtype=dtype, tol=cfg.tol,
-                           ao3=ao3,
+                           ao3=ao3, bands=bands,
                            max_sweeps=cfg.sweep_limit(plan.grid), mine=mine,
                            act_tol=cfg.act_tol, schedule=cfg.schedule,
                            inner=cfg.inner_for(plan.grid.dim))

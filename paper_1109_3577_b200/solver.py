@@ -425,10 +425,13 @@ def device_solve(plan: StencilPlan, work: torch.Tensor, lab: torch.Tensor, fmask
                  n_patches: int, *, rule: str, dtype: str, tol: float, max_sweeps: int,
                  mine: Optional[torch.Tensor] = None, sync: bool = True,
                  prune: bool = True, ao3=None, act_tol: float = 0.0,
-                 schedule: str = "jacobi", inner: int = 1) -> DeviceSolveResult:
-    """One phj_solve launch: all patches of `lab`, to per-patch convergence."""
+                 schedule: str = "jacobi", inner: int = 1, bands=None) -> DeviceSolveResult:
+    """One phj_solve launch: all patches of `lab`, to per-patch convergence.
+    ``bands`` (patchy.band_schedule) prepends the value-ordered pass."""
     lib = _lib.load()
     dev = plan.device
+    n_band = 0 if bands is None else int(bands[2])
+    max_sweeps = max_sweeps + (n_band + 1 if n_band else 0)
     v1 = work.clone()
     wsb = lib.phj_solve_workspace_bytes(ctypes_ref(plan.gs), n_patches, max_sweeps)
     ws = torch.empty(int(wsb), dtype=torch.uint8, device=dev)
@@ -463,6 +466,10 @@ def device_solve(plan: StencilPlan, work: torch.Tensor, lab: torch.Tensor, fmask
     a.act_tol = float(act_tol)
     a.inner_sweeps = int(inner)
     a.patch_counts = _lib.ptr(pc)
+    if n_band:
+        a.band_list = _lib.ptr(bands[0])
+        a.band_off = _lib.ptr(bands[1])
+        a.n_band = n_band
     if ao3 is not None:
         fbx, amask, acount, words = ao3
         a.ao3_fb = _lib.ptr(fbx)
