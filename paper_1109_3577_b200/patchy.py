@@ -233,6 +233,14 @@ def lift_internal(cplan: StencilPlan, vc: torch.Tensor, fplan: StencilPlan, rule
     return vf
 
 
+def banded_applies(plan: StencilPlan) -> bool:
+    """The value-ordered passes pay on 3D single-class stencils (configs 3
+    and 5: patch solve 2-3x, transport up to 3.5x, profiles/r2_banded_ab.jsonl);
+    2D sweeps are too thin to hide the per-sweep latency (config 2: 16 -> 54
+    ms) and the Dubins headings (config 4) span thousands of bands."""
+    return plan.grid.dim == 3 and plan.stencils.n_classes == 1
+
+
 def band_schedule(plan: StencilPlan, key_work: torch.Tensor, nodes: torch.Tensor, rule: str,
                   window, final_row: bool = False):
     """Block schedule of a value-ordered pass: CSR (band_list, band_off,
@@ -429,7 +437,8 @@ def _transport_and_argmax(fplan: StencilPlan, fb: torch.Tensor, parts, color_tol
         # footprint: 35 GB instead of 70 GB at config 5)
         pdt = torch.float32 if (dtype == "float32" and TRANSPORT_PHI_FP32) else torch.float64
         bands = None
-        if TRANSPORT_BANDED and tsched == "jacobi" and fplan.grid.dim == 3 and key_work is not None:
+        if (TRANSPORT_BANDED and tsched == "jacobi" and banded_applies(fplan) and
+                key_work is not None):
             bands = transport_bands(fplan, key_work, fb, rule)
         phi, _, csw, upd = transport_internal(fplan, fb, parts_flat, color_tol, limit,
                                               tsched, pdt, bands=bands)
@@ -602,7 +611,8 @@ def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Te
     if pcfg.bc_mode == STATE_CONSTRAINT:
         fmask = plan.fmask_from_labels(lab)
         bands = None
-        if SOLVE_BANDED and lifted_work is not None and not pcfg.warm_start:
+        if (SOLVE_BANDED and lifted_work is not None and not pcfg.warm_start and
+                banded_applies(plan) and cfg.schedule == "async"):
             nodes = (color >= 0) & (plan.kind.view(-1) == KIND_FREE)
             if mine is not None:
                 nodes &= mine.bool()[color.clamp(min=0).long()]

@@ -545,3 +545,35 @@ def test_solve_dd_reaches_single_domain_fixed_point(R):
     # one box = the single-domain Jacobi iteration (same sweep count up to the stop)
     if R == 1:
         assert abs(dst.sweeps - sst.sweeps) <= 1
+
+
+@pytest.mark.parametrize("R", [2, 4, 8])
+def test_solve_dd_matches_oracle_schwarz_iteration(R):
+    # the device Schwarz iteration against the oracle's restatement of
+    # decomp.py:101-190 with the same (Jacobi) box sweep: identical outer
+    # iteration counts, fields equal to rounding; and the oracle's GS form
+    # (the reference's box sweep, pinned bit-exact to its solve_dd fixture in
+    # tests/test_oracle_golden.py) reaches the same fixed point within 1e-8
+    if R == 8:
+        pr = C.fib3d(n=17, radius=0.25)
+        spec = _eik_spec((-1.0,) * 3, (1.0,) * 3, C.fib_sphere(48), 0.25)
+        g = phj.Grid(spec.box_lo, spec.box_hi, (17, 17, 17))
+    else:
+        pr = C.eikonal((-2.0, -2.0), (2.0, 2.0), (41, 41), C.circle(32), 0.3)
+        spec = _eik_spec((-2.0, -2.0), (2.0, 2.0), C.circle(32), 0.3)
+        g = phj.Grid(spec.box_lo, spec.box_hi, (41, 41))
+    cfg = phj.SolverConfig(tol=1e-9)
+    dd, dst = phj.solve_dd(spec, g, phj.make_static_decomposition(g, R), cfg)
+    uj = O.init_field(pr, "reference")
+    sj = O.solve_dd(uj, pr, R, rule="reference", mode="jacobi", tol=1e-9)
+    ug = O.init_field(pr, "reference")
+    sg = O.solve_dd(ug, pr, R, rule="reference", mode="gs", tol=1e-9)
+    got = _flat(dd.numpy())
+    assert dst.converged and sj.converged and sg.converged
+    assert dst.sweeps == sj.sweeps, (dst.sweeps, sj.sweeps)
+    live = uj < 0.5e9
+    assert np.array_equal(got < 0.5e9, live)
+    assert np.abs(got[live] - uj[live]).max() <= 1e-12
+    assert np.abs(got[live] - ug[live]).max() <= 1e-8
+    print(f"R={R}: outer iterations device {dst.sweeps} = oracle Jacobi {sj.sweeps}; "
+          f"reference GS {sg.sweeps}")

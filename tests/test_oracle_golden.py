@@ -93,6 +93,17 @@ def test_c1_patchy_pipeline_stagewise_bit_exact():
     assert [s.sweeps for s in pst] == [int(s) for s in c["patch_sweeps"]]
 
 
+def test_c1_coarse_solve_dd_bit_exact():
+    # the oracle's Schwarz iteration (decomp.py:101-190) reproduces the
+    # reference's solve_dd(R=4) coarse field of the fixture bit for bit
+    c = golden("c1_patchy.npz")
+    prc = C.c1_coarse(float(c["coarse_radius"]))
+    u = P.init_field(prc, "reference")
+    st = P.solve_dd(u, prc, 4, rule="reference", mode="gs", tol=1e-8)
+    assert st.converged and st.sweeps == int(c["coarse_sweeps"])
+    assert np.array_equal(u, _flat(c["coarse"]))
+
+
 def test_c1_jacobi_patchy_within_parity_of_gs():
     # Jacobi (the GPU iteration) reaches the same fixed point within 1e-8
     c = golden("c1_patchy.npz")
