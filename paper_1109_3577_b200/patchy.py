@@ -68,8 +68,11 @@ TRANSPORT_BAND_WINDOW = (3, 1)  # (trailing, leading) bands
 #: band schedule over the patch nodes, keyed by the lifted field; the
 #: schedule (async / jacobi) then continues from its result
 SOLVE_BANDED = os.environ.get("PHJ_SOLVE_BANDED", "1") != "0"
-SOLVE_BAND_WINDOW = (6, 2)
+SOLVE_BAND_WINDOW = tuple(int(x) for x in os.environ.get("PHJ_SOLVE_BAND_WINDOW", "6,2").split(","))
 BAND_CAP_PER_NODE = 1.5
+#: band width in units of the smallest SL time step (coarser bands: fewer,
+#: thicker sweeps)
+BAND_SCALE = float(os.environ.get("PHJ_BAND_SCALE", "1"))
 #: fp32 workloads store the colour fields in fp32
 TRANSPORT_PHI_FP32 = True
 
@@ -263,7 +266,7 @@ def band_schedule(plan: StencilPlan, key_work: torch.Tensor, nodes: torch.Tensor
     if not bool(nodes.any()):
         return None
     fmax = plan.eps_speed / 1.0e-12
-    delta = plan.grid.k_step / fmax
+    delta = BAND_SCALE * plan.grid.k_step / fmax
     # at most BAND_CAP_PER_NODE x the longest grid axis bands (one sweep each):
     # slow dynamics (Dubins turns) would otherwise need thousands of sweeps
     Tn = torch.where(nodes.view(-1), T, torch.zeros_like(T))

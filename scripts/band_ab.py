@@ -1,0 +1,43 @@
+"""A/B of the value-ordered patch-solve pass on one GPU: patch-solve kernel
+time at G=1 and for rank 0 of G=8 (its patch subset alone), per setting of
+PHJ_BAND_SCALE / PHJ_SOLVE_BAND_WINDOW / PHJ_BAND_INNER (env, set by caller)."""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+from paper_1109_3577_b200 import configs, dist, patchy  # noqa: E402
+from paper_1109_3577_b200.solver import feedback_internal  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "c5"
+w = configs.CONFIGS[name](dtype="float64")
+spec, pcfg, cfg = w.spec, w.pcfg, w.cfg
+fplan, cplan = patchy.make_plans(spec, pcfg)
+patchy.run_patchy(spec, pcfg, cfg, plans=(fplan, cplan), outputs=False)
+vc, _ = patchy.solve_full_internal(cplan, patchy.coarse_cfg(cfg))
+vf = patchy.lift_internal(cplan, vc, fplan, cfg.rule, cfg.dtype)
+fb, _ = feedback_internal(fplan, vf, rule=cfg.rule, dtype=cfg.dtype)
+parts = patchy._resolve_parts(pcfg, spec, fplan.grid, fplan)
+bv, bi, _, _ = patchy._transport_and_argmax(fplan, fb, parts, pcfg.color_tol,
+                                             10 * max(fplan.grid.shape), cfg.schedule, cfg.dtype,
+                                             key_work=vf, rule=cfg.rule)
+mask = patchy.plan_interior_serial(fplan, vf) >= 1.0
+color, _, _, lab = patchy.assemble_internal(fplan.gs, bv, bi, len(parts), mask, fplan.kind,
+                                            fplan.grid.n_interior, fplan.device)
+out = {"config": name, "scale": patchy.BAND_SCALE, "window": patchy.SOLVE_BAND_WINDOW,
+       "inner": os.environ.get("PHJ_BAND_INNER", "default")}
+real = dist.world
+for G in (1, 8):
+    dist.world = lambda G=G: (0, G)
+    try:
+        for rep in range(2):
+            _, pst, _, pinfo = patchy.solve_patches_internal(fplan, color, lab, len(parts), pcfg,
+                                                             cfg, vf)
+    finally:
+        dist.world = real
+    out[f"G{G}_kernel_ms"] = pinfo["kernel_ms"]
+    out[f"G{G}_executed"] = pinfo["performed"]
+print(json.dumps(out), flush=True)
