@@ -162,6 +162,8 @@ typedef struct phj_solve_args {
   const int32_t* band_list;
   const int32_t* band_off;   /* [n_band + 2] */
   int32_t n_band;
+  int32_t band_inner;        /* block-local relaxations per visit in the pass
+                                (0 = inner_sweeps) */
   void* stream;               /* cudaStream_t */
 } phj_solve_args;
 

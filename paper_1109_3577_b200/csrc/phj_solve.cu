@@ -3334,10 +3334,8 @@ static int solve_impl(const phj_solve_args* a) {
     // buffers hold the pass's values (every block ends with a copy visit)
     SolveParams pb = p;
     pb.band_only = 1;
-    // block-local relaxations per visit in the pass (tuning knob; default:
-    // the schedule's)
-    static const int band_inner = getenv("PHJ_BAND_INNER") ? atoi(getenv("PHJ_BAND_INNER")) : 0;
-    if (band_inner > 0) pb.inner = band_inner;
+    // block-local relaxations per visit in the pass (0: the schedule's)
+    if (a->band_inner > 0) pb.inner = a->band_inner;
     void* bargs[] = {(void*)&pb};
     int rc = (D == 3 && p.n_classes > 1)
                  ? coop_launch(solve_kernel<D, T, RULE, COST, D == 3>,

@@ -63,12 +63,15 @@ TRANSPORT_INNER = {2: 8, 3: 4}
 #: lies within [s - lo, s + hi] of sweep s -- the colour masses cross the
 #: domain in one outward pass instead of ~path-length Jacobi sweeps
 TRANSPORT_BANDED = os.environ.get("PHJ_TRANSPORT_BANDED", "1") != "0"
-TRANSPORT_BAND_WINDOW = (3, 1)  # (trailing, leading) bands
+TRANSPORT_BAND_WINDOW = tuple(int(x) for x in os.environ.get("PHJ_TRANSPORT_BAND_WINDOW", "3,1").split(","))  # (trailing, leading)
 #: value-ordered pass before the patch solves: the same
 #: band schedule over the patch nodes, keyed by the lifted field; the
 #: schedule (async / jacobi) then continues from its result
 SOLVE_BANDED = os.environ.get("PHJ_SOLVE_BANDED", "1") != "0"
 SOLVE_BAND_WINDOW = tuple(int(x) for x in os.environ.get("PHJ_SOLVE_BAND_WINDOW", "6,2").split(","))
+#: block-local relaxations per visit in the solve's pass (A/B on config 5,
+#: profiles/r2_band_ab.jsonl: 1 -> 2.7 s, 2 -> 341 ms, 3 -> 401 ms)
+SOLVE_BAND_INNER = int(os.environ.get("PHJ_BAND_INNER", "2"))
 BAND_CAP_PER_NODE = 1.5
 #: band width in units of the smallest SL time step (coarser bands: fewer,
 #: thicker sweeps)
@@ -621,6 +624,8 @@ def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Te
                 nodes &= mine.bool()[color.clamp(min=0).long()]
             bands = band_schedule(plan, lifted_work, nodes, rule, SOLVE_BAND_WINDOW,
                                   final_row=True)
+            if bands is not None:
+                bands = (*bands, SOLVE_BAND_INNER)
         res = device_solve(plan, work, lab, fmask, n_patches, rule=rule, dtype=dtype, tol=cfg.tol,
                            ao3=ao3, bands=bands,
                            max_sweeps=cfg.sweep_limit(plan.grid), mine=mine,

@@ -470,6 +470,7 @@ def device_solve(plan: StencilPlan, work: torch.Tensor, lab: torch.Tensor, fmask
         a.band_list = _lib.ptr(bands[0])
         a.band_off = _lib.ptr(bands[1])
         a.n_band = n_band
+        a.band_inner = int(bands[3]) if len(bands) > 3 else 0
     if ao3 is not None:
         fbx, amask, acount, words = ao3
         a.ao3_fb = _lib.ptr(fbx)

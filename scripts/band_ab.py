@@ -28,8 +28,18 @@ mask = patchy.plan_interior_serial(fplan, vf) >= 1.0
 color, _, _, lab = patchy.assemble_internal(fplan.gs, bv, bi, len(parts), mask, fplan.kind,
                                             fplan.grid.n_interior, fplan.device)
 out = {"config": name, "scale": patchy.BAND_SCALE, "window": patchy.SOLVE_BAND_WINDOW,
-       "inner": os.environ.get("PHJ_BAND_INNER", "default")}
+       "inner": patchy.SOLVE_BAND_INNER, "twindow": patchy.TRANSPORT_BAND_WINDOW}
 real = dist.world
+for G in (1, 8):
+    dist.world = lambda G=G: (0, G)
+    try:
+        for rep in range(2):
+            patchy._transport_and_argmax(fplan, fb, parts, pcfg.color_tol,
+                                         10 * max(fplan.grid.shape), cfg.schedule, cfg.dtype,
+                                         key_work=vf, rule=cfg.rule)
+    finally:
+        dist.world = real
+    out[f"G{G}_transport_ms"] = patchy.TRANSPORT_DIAG["kernel_ms"]
 for G in (1, 8):
     dist.world = lambda G=G: (0, G)
     try:
