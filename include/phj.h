@@ -184,6 +184,26 @@ int64_t phj_blocks_total(const phj_grid* g);
 /* warp-block extent along the internal axes (block = planes x rows x nodes,
  * axis 0 slowest): out[0..2]; 2D grids use out[0..1] */
 int phj_block_dims(int32_t dim, int32_t* out);
+
+/* Schedule of a value-ordered pass (the band_list / band_off rows of
+ * phj_solve_args and phj_transport_args).  `key` is the
+ * lifted working field (ext layout, dtype; Kruzkov v is turned into
+ * T = -log(1 - v)), `nodes` one byte per internal serial (1 = scheduled).
+ * Bands are floor(T / delta) with delta = max(delta_min, T_max / max_bands);
+ * a block is relaxed at sweeps [min band - hi_w, max band + lo_w] of its nodes
+ * and copied one sweep later.  phj_band_count synchronises the stream and
+ * returns out[0] = entries (without the final row), out[1] = n_band,
+ * out[2] = scheduled blocks, out[3] = delta (double bits); phj_band_fill then
+ * writes band_list [out[0] (+ out[2] with final_row)] and band_off
+ * [n_band + 1 (+ 1)] (final_row: row n_band = every scheduled block).
+ * Rows are in no particular block order. */
+int64_t phj_band_scratch_bytes(const phj_grid* g, int32_t max_bands, int32_t lo_w, int32_t hi_w);
+int phj_band_count(const phj_grid* g, int32_t dtype, int32_t rule, const void* key,
+                   const uint8_t* nodes, double delta_min, int32_t max_bands, int32_t lo_w,
+                   int32_t hi_w, void* scratch, int64_t* out, void* stream);
+int phj_band_fill(const phj_grid* g, int32_t max_bands, int32_t lo_w, int32_t hi_w,
+                  int32_t n_band, int32_t n_blocks, int32_t final_row, void* scratch,
+                  int32_t* band_list, int32_t* band_off, void* stream);
 int phj_solve(const phj_solve_args* a);
 
 /* foreign-position masks: bit p set when 3^dim neighbour p of the node is not

@@ -89,7 +89,8 @@ class SpeedModel(ctypes.Structure):
 
 #: every symbol include/phj.h declares (checked by the CPU test suite)
 EXPORTS = (
-    "phj_solve_workspace_bytes", "phj_unroll", "phj_blocks_total", "phj_block_dims", "phj_solve",
+    "phj_solve_workspace_bytes", "phj_unroll", "phj_blocks_total", "phj_block_dims",
+    "phj_band_scratch_bytes", "phj_band_count", "phj_band_fill", "phj_solve",
     "phj_fmask_from_labels",
     "phj_fmask_from_hard",
     "phj_feedback", "phj_feedback_allowed", "phj_transport", "phj_lift", "phj_argmax_update",
@@ -123,6 +124,9 @@ def load() -> ctypes.CDLL:
         "phj_solve_workspace_bytes": (I64, [P, I32, I32]),
         "phj_blocks_total": (I64, [P]),
         "phj_block_dims": (ctypes.c_int, [I32, P]),
+        "phj_band_scratch_bytes": (I64, [P, I32, I32, I32]),
+        "phj_band_count": (ctypes.c_int, [P, I32, I32, P, P, D, I32, I32, I32, P, P, P]),
+        "phj_band_fill": (ctypes.c_int, [P, I32, I32, I32, I32, I32, I32, P, P, P, P]),
         "phj_unroll": (I32, [I32]),
         "phj_solve": (ctypes.c_int, [P]),
         "phj_fmask_from_labels": (ctypes.c_int, [P, P, P, P]),

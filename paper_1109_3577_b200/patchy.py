@@ -30,7 +30,7 @@ from .grid import SENTINEL, ConfigurationError, Grid, NodeField, require_cuda
 from .problems import (ProblemSpec, TargetSpec, _check_parts, device_partition_codes,
                        partition_target)
 from .runtime import ExecutionStrategy, RunStats
-from .solver import (DIRICHLET, KIND_FREE, KIND_OBSTACLE, KIND_TARGET, STATE_CONSTRAINT,
+from .solver import (_rule_id, DIRICHLET, KIND_FREE, KIND_OBSTACLE, KIND_TARGET, STATE_CONSTRAINT,
                      FeedbackField, SolverConfig, StencilPlan, SweepStats, ctypes_ref,
                      device_solve, feedback_internal, stats_for_patch, unreach_threshold,
                      unreached_value, _dtype_id)
@@ -249,80 +249,44 @@ def banded_applies(plan: StencilPlan) -> bool:
 
 def band_schedule(plan: StencilPlan, key_work: torch.Tensor, nodes: torch.Tensor, rule: str,
                   window, final_row: bool = False):
-    """Block schedule of a value-ordered pass: CSR (band_list, band_off,
-    n_band) of the warp blocks each sweep visits (phj_transport_args /
-    phj_solve_args band fields).
+    """Block schedule of a value-ordered pass on the device (phj_band_count /
+    phj_band_fill): CSR (band_list, band_off, n_band) of the warp blocks each
+    sweep visits (phj_transport_args / phj_solve_args band fields).
 
     A node's band is floor(T / delta), T its lifted time-to-target (working
-    field ``key_work``: v for Kruzkov, u for the reference rule) and delta =
-    k / max|f| the smallest time step of one SL step; a block holding any of
-    ``nodes`` (bool per internal serial) is visited at sweeps [min band - hi,
-    max band + lo] of those nodes and copied to the other buffer one sweep
-    later (its last visit keeps both Jacobi buffers equal).  ``final_row``
-    appends row n_band with every block of the pass (the solve's first
-    ordinary sweep).  Returns None when ``nodes`` is empty."""
-    lo_w, hi_w = window
+    field ``key_work``: v for Kruzkov, u for the reference rule), delta =
+    BAND_SCALE x k / max|f| (the smallest time one SL step covers), widened so
+    that at most BAND_CAP_PER_NODE x the longest axis bands exist; a block
+    holding any of ``nodes`` (bool per internal serial) is relaxed at sweeps
+    [min band - hi, max band + lo] of those nodes and copied to the other
+    buffer one sweep later.  ``final_row`` appends row n_band with every
+    scheduled block (the solve's first ordinary sweep).  Returns None when
+    ``nodes`` is empty."""
+    lo_w, hi_w = (int(x) for x in window)
     dev = plan.device
-    d = plan.grid.dim
-    kw = plan.interior_int(key_work).reshape(-1).to(torch.float64)
-    T = -torch.log1p(-kw.clamp(max=1.0 - 1e-16)) if rule == "kruzkov" else kw
-    if not bool(nodes.any()):
-        return None
+    lib = _lib.load()
     fmax = plan.eps_speed / 1.0e-12
-    delta = BAND_SCALE * plan.grid.k_step / fmax
-    # at most BAND_CAP_PER_NODE x the longest grid axis bands (one sweep each):
-    # slow dynamics (Dubins turns) would otherwise need thousands of sweeps
-    Tn = torch.where(nodes.view(-1), T, torch.zeros_like(T))
-    t_max = float(Tn.max().item())
-    cap = BAND_CAP_PER_NODE * max(plan.int_shape)
-    if t_max / delta > cap:
-        delta = t_max / cap
-    band = torch.floor(T / delta).clamp(max=1 << 30).to(torch.int64)
-    dims = (ctypes.c_int32 * 3)()
-    _lib.check(_lib.load().phj_block_dims(d, dims), "block_dims")
-    shp = plan.int_shape
-    ser = torch.nonzero(nodes.view(-1)).view(-1)
-    if d == 3:
-        i0 = ser // (shp[1] * shp[2])
-        i1 = (ser // shp[2]) % shp[1]
-        i2 = ser % shp[2]
-        n1 = -(-shp[1] // dims[1])
-        n2 = -(-shp[2] // dims[2])
-        bid = (i0 * n1 + i1 // dims[1]) * n2 + i2 // dims[2]
-        total = shp[0] * n1 * n2
-    else:
-        i0 = ser // shp[1]
-        i1 = ser % shp[1]
-        n1 = -(-shp[1] // dims[1])
-        bid = (i0 // dims[0]) * n1 + i1 // dims[1]
-        total = -(-shp[0] // dims[0]) * n1
-    bm = band[ser]
-    kmin = torch.full((total,), 1 << 40, dtype=torch.int64, device=dev).scatter_reduce(
-        0, bid, bm, reduce="amin")
-    kmax = torch.full((total,), -1, dtype=torch.int64, device=dev).scatter_reduce(
-        0, bid, bm, reduce="amax")
-    blocks = torch.nonzero(kmax >= 0).view(-1)
-    lo = (kmin[blocks] - hi_w).clamp(min=0)
-    hi = kmax[blocks] + lo_w
-    L = hi - lo + 2                                    # updates + the copy visit
-    E = int(L.sum().item())
-    rep_b = torch.repeat_interleave(blocks, L)
-    start = torch.cumsum(L, 0) - L
-    off = torch.arange(E, device=dev) - torch.repeat_interleave(start, L)
-    sweep = torch.repeat_interleave(lo, L) + off
-    last = off == torch.repeat_interleave(L, L) - 1
-    entry = torch.where(last, -rep_b - 1, rep_b)
-    n_band = int((hi.max() + 2).item())
-    if final_row:
-        entry = torch.cat([entry, blocks])
-        sweep = torch.cat([sweep, torch.full_like(blocks, n_band)])
-        rep_b = torch.cat([rep_b, blocks])
-    rows = n_band + (1 if final_row else 0)
-    order = torch.argsort(sweep * total + rep_b)       # by sweep, then block id
-    band_list = entry[order].to(torch.int32).contiguous()
-    counts = torch.bincount(sweep, minlength=rows)
-    band_off = torch.cat([torch.zeros(1, dtype=torch.int64, device=dev),
-                          torch.cumsum(counts, 0)]).to(torch.int32).contiguous()
+    delta_min = BAND_SCALE * plan.grid.k_step / fmax
+    max_bands = int(BAND_CAP_PER_NODE * max(plan.int_shape))
+    nb = nodes.view(-1).to(torch.uint8).contiguous()
+    scratch = torch.empty(int(lib.phj_band_scratch_bytes(ctypes_ref(plan.gs), max_bands, lo_w,
+                                                          hi_w)),
+                          dtype=torch.uint8, device=dev)
+    out = (ctypes.c_int64 * 4)()
+    dt = _lib.F32 if key_work.dtype == torch.float32 else _lib.F64
+    kw = key_work.contiguous()
+    _lib.check(lib.phj_band_count(ctypes_ref(plan.gs), dt, _rule_id(rule), _lib.ptr(kw),
+                                  _lib.ptr(nb), delta_min, max_bands, lo_w, hi_w,
+                                  _lib.ptr(scratch), out, _lib.stream_handle()), "band_count")
+    entries, n_band, n_blocks = int(out[0]), int(out[1]), int(out[2])
+    if n_blocks == 0:
+        return None
+    band_list = torch.empty(entries + (n_blocks if final_row else 0), dtype=torch.int32,
+                            device=dev)
+    band_off = torch.empty(n_band + (2 if final_row else 1), dtype=torch.int32, device=dev)
+    _lib.check(lib.phj_band_fill(ctypes_ref(plan.gs), max_bands, lo_w, hi_w, n_band, n_blocks,
+                                 int(final_row), _lib.ptr(scratch), _lib.ptr(band_list),
+                                 _lib.ptr(band_off), _lib.stream_handle()), "band_fill")
     return band_list, band_off, n_band
 
 

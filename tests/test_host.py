@@ -267,42 +267,33 @@ def test_device_partition_codes_match_numpy_partitions():
 
 
 def test_transport_band_schedule():
-    # the value-ordered pass visits a block at sweeps [min band - hi, max band
-    # + lo] of its movers, then once more as a copy (-b-1), sweep-sorted CSR
-    import types
-
+    # the pass visits a block at sweeps [min band - hi, max band + lo] of its
+    # nodes, then once more as a copy (-b-1); reference construction of the
+    # rows the device builds (phj_band_count / phj_band_fill, tested against
+    # it in tests/test_gpu_bands.py)
     import torch
 
-    from paper_1109_3577_b200 import patchy
+    from band_reference import schedule_rows
 
     shape = (3, 9, 17)  # internal (planes, rows, nodes): blocks 1 x 8 x 8
-    n = int(np.prod(shape))
     k = 0.125
-    # reference rule: the key is the time itself; band = node index along axis 2
     T = torch.zeros(shape, dtype=torch.float64) + torch.arange(shape[2], dtype=torch.float64) * k
-    work = torch.full(tuple(m + 2 for m in shape), 1.0e9, dtype=torch.float64)
-    work[1:-1, 1:-1, 1:-1] = T
-    fb = torch.zeros(n, dtype=torch.int32)
-    fb[0] = -1  # not a mover
-    plan = types.SimpleNamespace(
-        device=torch.device("cpu"), grid=types.SimpleNamespace(dim=3, k_step=k),
-        kind=torch.zeros(n, dtype=torch.int8), eps_speed=1.0e-12, int_shape=shape,
-        interior_int=lambda t: t[1:-1, 1:-1, 1:-1])
-    lst, off, n_band = patchy.transport_bands(plan, work, fb, "reference", window=(2, 1))
-    lst, off = lst.numpy(), off.numpy()
-    n1, n2 = 2, 3
+    nodes = torch.ones(shape, dtype=torch.bool)
+    nodes.view(-1)[0] = False  # not scheduled
+    rows, n_band, delta = schedule_rows(T, nodes, shape, (1, 8, 8), k, 100, (2, 1))
     visits = {}
-    for s in range(n_band):
-        for e in lst[off[s]:off[s + 1]]:
-            visits.setdefault(int(e), []).append(s)
-    # block (plane 0, row-block 0, node-block 2): nodes 16 -> bands 16..16
-    b = (0 * n1 + 0) * n2 + 2
+    for s, entries in rows.items():
+        for e in entries:
+            visits.setdefault(e, []).append(s)
+    n1, n2 = 2, 3
+    b = (0 * n1 + 0) * n2 + 2  # plane 0, rows 0-7, nodes 16 -> band 16
     assert visits[b] == list(range(15, 19)) and visits[-b - 1] == [19]
-    # block (plane 1, row-block 1, node-block 0): bands 0..7 (node 0 is a mover here)
-    b = (1 * n1 + 1) * n2 + 0
+    b = (1 * n1 + 1) * n2 + 0  # plane 1, rows 8, nodes 0-7 -> bands 0..7
     assert visits[b] == list(range(0, 10)) and visits[-b - 1] == [10]
-    assert n_band == 20 and off[-1] == lst.size
-    for s in range(n_band):  # one visit per block and sweep
-        ids = np.where(lst[off[s]:off[s + 1]] < 0, -lst[off[s]:off[s + 1]] - 1,
-                       lst[off[s]:off[s + 1]])
-        assert np.unique(ids).size == ids.size
+    assert n_band == 20 and delta == k
+    for s, entries in rows.items():  # one visit per block and sweep
+        ids = [e if e >= 0 else -e - 1 for e in entries]
+        assert len(set(ids)) == len(ids)
+    # the band cap widens delta: at most max_bands bands
+    rows, n_band, delta = schedule_rows(T, nodes, shape, (1, 8, 8), k, 4, (2, 1))
+    assert delta == 16 * k / 4 and n_band <= 4 + 2 + 1 + 1
