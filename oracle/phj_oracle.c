@@ -484,7 +484,8 @@ void og_lift(const og_grid* gc, const double* uc, const og_grid* gf, double* out
  * cnt[3] = blocked nodes with u < unreach
  * cnt[4] = free patch nodes with u < unreach (the certified set)
  * cnt[5] = candidate evaluations
- * missed_list (optional, missed_cap entries): serials of the missed nodes
+ * missed_list (optional, 2 x missed_cap entries): serials of the missed nodes,
+ *   then (from missed_cap on) of the spurious ones
  */
 void og_residual(const og_grid* g, const og_dyn* dy, const double* u, const uint8_t* kind,
                  const int32_t* lab_ext, double unreach, int rule, int nthreads,
@@ -549,7 +550,15 @@ void og_residual(const og_grid* g, const og_dyn* dy, const double* u, const uint
         }
         continue;
       }
-      if (best >= unreach) { spurious += 1; continue; }
+      if (best >= unreach) {
+        int64_t k;
+#ifdef _OPENMP
+#pragma omp atomic capture
+#endif
+        k = spurious++;
+        if (missed_list && k < missed_cap) missed_list[missed_cap + k] = s;
+        continue;
+      }
       ncert += 1;
       double r = best - u[fi];
       if (r < 0.0) r = -r;
