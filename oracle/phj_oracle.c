@@ -536,11 +536,14 @@ void og_residual(const og_grid* g, const og_dyn* dy, const double* u, const uint
         v = og_apply_rule(rule, v, cost);
         if (v < best) best = v;
       }
+      /* margin: values within 1e-9 (relative) of the unreached level are at
+       * the floating-point floor of the Kruzkov transform (v = 1 - 1 ulp is
+       * T ~ 37), and a candidate over unreached corners only is 1 up to the
+       * rounding of the reference's per-node weights (their sum is 1 only
+       * to ~1 ulp, grid.py:227-239): neither side counts them as reached */
+      const double thr = unreach * (1.0 - 1.0e-9);
       if (u[fi] >= unreach) {
-        /* margin: a candidate over unreached corners only is 1 up to the
-         * rounding of the reference's per-node weights (their sum is 1 only
-         * to ~1 ulp, grid.py:227-239), not a reachable value */
-        if (best < unreach * (1.0 - 1.0e-9)) {
+        if (best < thr) {
           int64_t k;
 #ifdef _OPENMP
 #pragma omp atomic capture
@@ -550,7 +553,7 @@ void og_residual(const og_grid* g, const og_dyn* dy, const double* u, const uint
         }
         continue;
       }
-      if (best >= unreach) {
+      if (best >= unreach && u[fi] < thr) {
         int64_t k;
 #ifdef _OPENMP
 #pragma omp atomic capture
@@ -559,6 +562,7 @@ void og_residual(const og_grid* g, const og_dyn* dy, const double* u, const uint
         if (missed_list && k < missed_cap) missed_list[missed_cap + k] = s;
         continue;
       }
+      if (best > unreach) best = unreach;
       ncert += 1;
       double r = best - u[fi];
       if (r < 0.0) r = -r;
