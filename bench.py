@@ -303,6 +303,9 @@ def run_ours(args):
         # PHJ_DIST_BACKEND=gloo: two ranks on one GPU for functional checks of
         # the multi-rank bench path (NCCL needs one device per rank)
         backend = os.environ.get("PHJ_DIST_BACKEND", "nccl")
+        # NCCL's init lines (ranks, NVLink/NVLS transport) in the run log
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         if backend == "nccl":
             td.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -465,6 +468,8 @@ def run_ours(args):
                      "issued_entry_tflops": issued,
                      "peak_source": "measured here: phj_peak_flops FMA-chain probe"},
         "cpu_baseline": cpu,
+        "process_group": ({"backend": td.get_backend(), "world_size": td.get_world_size()}
+                          if world > 1 else None),
         "clocks": clocks,
         "gpu_launches": int(launches),
     }

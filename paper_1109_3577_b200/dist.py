@@ -5,7 +5,10 @@ conditions, so ranks solve disjoint patch sets with no halo exchange; the
 final gather of v is an element-wise MIN all-reduce (every rank's non-owned
 nodes still hold the unreached value, which is >= the owner's result; target
 nodes are 0 everywhere).  Patches are placed by LPT (longest processing time
-first) on node counts, as north_star asks.
+first) on node counts, as north_star asks, for the first solve of a patch
+map; repeated solves of the same map (the benchmark's steps, parameter
+sweeps) weight LPT by the per-patch executed evaluations the previous solve
+measured (summed over ranks, so every rank derives the same assignment).
 
 The colour transport (the labelling stage, a third of a step on one GPU) is
 split by colour: colours are independent linear fixed points with their own
@@ -57,11 +60,14 @@ def load_balance_bound(sizes: Sequence[int], n_ranks: int) -> float:
     return float(sizes.sum() / (n_ranks * bins.max())) if bins.max() > 0 else 1.0
 
 
-def mine_mask(sizes: Sequence[int], rank: int, n_ranks: int, device) -> Optional[torch.Tensor]:
-    """uint8 per patch: 1 where this rank sweeps the patch (None = all)."""
+def mine_mask(sizes: Sequence[int], rank: int, n_ranks: int, device,
+              weights: Optional[Sequence[float]] = None) -> Optional[torch.Tensor]:
+    """uint8 per patch: 1 where this rank sweeps the patch (None = all).
+    LPT on ``weights`` (identical on every rank) when given, else on the
+    node counts."""
     if n_ranks <= 1:
         return None
-    owner = lpt_assign(sizes, n_ranks)
+    owner = lpt_assign(sizes, n_ranks, weights)
     m = (owner == rank) & (np.asarray(sizes) > 0)
     return torch.as_tensor(m.astype(np.uint8), device=device)
 

@@ -121,3 +121,20 @@ def test_colour_split_argmax_merge_world2():
     for _, v, i in out:
         assert np.array_equal(np.array(v), want_v)
         assert np.array_equal(np.array(i)[pos], want_i[pos])  # index only matters where v > 0
+
+
+def test_lpt_weights_change_the_assignment():
+    # measured per-patch work (not node counts) decides the LPT bins when given
+    from paper_1109_3577_b200 import dist
+
+    sizes = [100, 90, 80, 10]
+    work = [10.0, 90.0, 80.0, 100.0]
+    by_nodes = dist.lpt_assign(sizes, 2)
+    by_work = dist.lpt_assign(sizes, 2, work)
+    assert by_nodes.tolist() == [0, 1, 1, 0]
+    load = lambda owner: np.bincount(owner, weights=work, minlength=2).max()
+    assert load(by_work) <= load(by_nodes)
+    assert by_work[3] == 0  # the heaviest measured patch is placed first
+    m0 = dist.mine_mask(sizes, 0, 2, "cpu", work).numpy()
+    m1 = dist.mine_mask(sizes, 1, 2, "cpu", work).numpy()
+    assert np.array_equal(m0 + m1, np.ones(4, dtype=np.uint8))
