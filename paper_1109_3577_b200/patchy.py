@@ -47,7 +47,7 @@ TRANSPORT_DIAG: dict = {}
 #: above this fraction of color_tol: the geometric tails of
 #: the Jacobi transport, orders of magnitude below the stopping tolerance,
 #: no longer keep the whole domain busy.  0 gives exact Jacobi activity.
-TRANSPORT_ACT_FRAC = 1.0e-3
+TRANSPORT_ACT_FRAC = float(os.environ.get("PHJ_TRANSPORT_ACT_FRAC", "1e-3"))
 #: asynchronous transport: a colour change re-queues the neighbourhood only
 #: above this fraction of color_tol; relaxations per block visit by dimension
 # 1e-4: labels run-to-run identical at full config-2 size (1e-3: 1-3 of 4.2 M
