@@ -13,8 +13,9 @@ replicated + max_r (transport_r) + merge + max_r (patch_r) + gather;
 efficiency = T(1) / (G * T(G)).
 
     python scripts/scaling_projection.py [c5] [float64] [weights]
-weights: "nodes" (north_star: node count) or "lifted" (node count x mean
-lifted time of the patch, a work predictor available before the solve).
+weights: "work" (default: the per-patch executed evaluations of a previous
+solve of the same patch map, as the library uses from the second solve on)
+or "nodes" (north_star: node count, the first solve).
 Writes one JSON object to stdout.
 """
 import json
@@ -32,6 +33,7 @@ from paper_1109_3577_b200.solver import feedback_internal, unreach_threshold  # 
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c5"
 dtype = sys.argv[2] if len(sys.argv) > 2 else "float64"
+WEIGHTS = sys.argv[3] if len(sys.argv) > 3 else "work"  # LPT weights: "work" or "nodes"
 BUS_GBS = float(os.environ.get("PHJ_NVLINK_BUS_GBS", "600"))  # all-reduce bus bandwidth
 w = configs.CONFIGS[name](dtype=dtype)
 spec, pcfg, cfg = w.spec, w.pcfg, w.cfg
@@ -64,7 +66,7 @@ thr = unreach_threshold(cfg.rule)
 mask = patchy.plan_interior_serial(fplan, vf) >= thr
 
 real_world = dist.world
-res = {"config": name, "dtype": dtype, "replicated_ms": {"coarse": t_coarse, "lift": t_lift,
+res = {"config": name, "dtype": dtype, "lpt_weights": WEIGHTS, "replicated_ms": {"coarse": t_coarse, "lift": t_lift,
                                                           "feedback": t_fb}}
 base = None
 color = lab = None
@@ -83,12 +85,19 @@ for G in (1, 2, 4, 8):
                     fplan.gs, bv, bi, R, mask, fplan.kind, n, dev))
                 res["replicated_ms"]["assembly"] = t_as
                 sizes = patchy.count_labels(color, R).cpu().numpy()
+            if G > 1 and WEIGHTS == "work":
+                # the per-patch work every rank would hold after a first solve
+                # of this patch map (measured at G = 1, all patches)
+                fplan._patch_work = ((tuple(int(x) for x in sizes), G), execd_all)
+            else:
+                fplan._patch_work = None
             (out, pst, warns, pinfo), t_pa = timed(lambda: patchy.solve_patches_internal(
                 fplan, color, lab, R, pcfg, cfg, vf))
             pa_ms.append(t_pa)
             if G == 1:
                 relax = np.array([s.node_relaxations for s in pst], dtype=float)
                 execd = np.array([s.performed_evals for s in pst], dtype=float)
+                execd_all = execd.copy()
         finally:
             dist.world = real_world
     rep = sum(res["replicated_ms"].values())
@@ -101,7 +110,7 @@ for G in (1, 2, 4, 8):
         base = step
         owner = np.zeros(R, dtype=int)
     else:
-        owner = dist.lpt_assign(sizes, G)
+        owner = dist.lpt_assign(sizes, G, execd_all if WEIGHTS == "work" else None)
     work_bins = np.bincount(owner, weights=execd, minlength=G)
     res[f"G{G}"] = {"step_ms": step, "transport_ms_per_rank": tr_ms,
                     "patch_ms_per_rank": pa_ms, "merge_ms_est": merge, "gather_ms_est": gather,
