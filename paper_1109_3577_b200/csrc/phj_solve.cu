@@ -1955,9 +1955,6 @@ struct TransportParams {
 #ifndef PHJ_TRANSPORT_CTAS
 #define PHJ_TRANSPORT_CTAS 2
 #endif
-#ifndef PHJ_TCB2
-#define PHJ_TCB2 1  // colours per gather batch in 2D (3D: 2)
-#endif
 template <int D, typename PT>
 __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel(const __grid_constant__ TransportParams p) {
   using B = Blk<D>;
@@ -1975,13 +1972,6 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
   unsigned long long* s_max = (unsigned long long*)(s_w + (int64_t)wpitch * NC);   // [R]
   int* s_done = (int*)(s_max + R);                                                 // [R]
   signed char* s_oct = (signed char*)(s_done + R);                                 // [nent]
-  // per warp: the halo tiles of a colour batch (TileShape, PT), staged with
-  // cp.async -- corner reads come from shared memory instead of scattered
-  // global gathers
-  using TS = TileShape<D>;
-  constexpr int TCB = (D == 2) ? PHJ_TCB2 : 2;  // colours per batch (= CB below)
-  PT* s_ttile = (PT*)(smem + align_up((int64_t)wpitch * NC * 8 + (int64_t)R * 12 + nent, 16)) +
-                (int64_t)(threadIdx.x >> 5) * TCB * TS::N;
   for (int i = threadIdx.x; i < nent * NC; i += blockDim.x)
     s_w[(i % NC) * wpitch + i / NC] = p.weights[i];
   for (int i = threadIdx.x; i < R; i += blockDim.x) s_done[i] = 0x7fffffff;
@@ -2126,6 +2116,9 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
         for (int r = 0; r < NB; ++r) kself[r] = e[r] >= 0 ? (~s_oct[e[r]]) & (NC - 1) : 0;
         // colours in batches of CB: all corner loads of a batch are in flight
         // together (the sweep is latency-bound on these gathers)
+#ifndef PHJ_TCB2
+#define PHJ_TCB2 1
+#endif
         constexpr int CB = (D == 2) ? PHJ_TCB2 : 2;
         const bool masked = R <= 64;
         unsigned long long todo = masked ? cm : 0ull;
@@ -2146,67 +2139,15 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
           }
           if (!anyj) break;
           double cv[CB][NB][NC];
-          // stage the block's halo tile of each colour of the batch (rows of
-          // the tile origin plane/row/col - 1, clamped to the ext array like
-          // the solve's stage_block), then read the corners from it
-          {
-            int b[3];
-            decode_block<D>(p.tg, bid, b);
-            const int row0 = (D == 2) ? b[0] * B::BY : b[1] * B::BY;
-            const int col0 = (D == 2) ? b[1] * B::BX : b[2] * B::BX;
-            const int rmax = (int)g.ext[D - 2] - 1, cmax = (int)g.ext[D - 1] - 1;
-            const int64_t rs = g.strides[D - 2];
-            constexpr int W = B::BX + 2;
-#pragma unroll
-            for (int q = 0; q < CB; ++q) {
-              if (js[q] < 0) continue;
-              const PT* pj = pin + (int64_t)js[q] * p.plane;
-              PT* tq = s_ttile + q * TS::N;
-              for (int i = lane; i < TS::R * W; i += 32) {
-                const int r = i / W, c = i - r * W;
-                int pl = 0, rr = r;
-                if constexpr (D == 3) {
-                  pl = r / TS::RB;
-                  rr = r - pl * TS::RB;
-                }
-                const int er = min(row0 + rr, rmax), ec = min(col0 + c, cmax);
-                int64_t src = (int64_t)er * rs + ec;
-                if constexpr (D == 3) src += (int64_t)(b[0] + pl) * g.strides[0];
-                cp_async<sizeof(PT)>(tq + r * TS::C + c, pj + src);
-              }
-            }
-            cp_async_commit();
-            cp_async_wait_all();
-            __syncwarp();
-          }
 #pragma unroll
           for (int q = 0; q < CB; ++q) {
-            const PT* tq = s_ttile + q * TS::N;
+            const PT* pj = pin + (int64_t)max(js[q], 0) * p.plane;
 #pragma unroll
-            for (int r = 0; r < NB; ++r) {
-              // tile index of the foot cell's lower corner (node at tile
-              // (1, ly + 1, lx NB + r + 1), minus one on axes of a lower octant)
-              int tp = 0;
-              if (e[r] >= 0) {
-                const int oc = s_oct[e[r]];
-                const int ly = lane / B::LX, lx = lane % B::LX;
-                if constexpr (D == 2) {
-                  tp = (ly + 1 - !(oc & 1)) * TS::C + lx * NB + r + 1 - !((oc >> 1) & 1);
-                } else {
-                  tp = ((1 - !(oc & 1)) * TS::RB + ly + 1 - !((oc >> 1) & 1)) * TS::C +
-                       lx * NB + r + 1 - !((oc >> 2) & 1);
-                }
-              }
+            for (int r = 0; r < NB; ++r)
 #pragma unroll
-              for (int k = 0; k < NC; ++k) {
-                int to;
-                if constexpr (D == 2) to = ((k & 1) ? TS::C : 0) + ((k >> 1) & 1);
-                else to = ((k & 1) ? TS::RB * TS::C : 0) + (((k >> 1) & 1) ? TS::C : 0) + ((k >> 2) & 1);
-                cv[q][r][k] = (js[q] >= 0 && e[r] >= 0) ? (double)tq[tp + to] : 0.0;
-              }
-            }
+              for (int k = 0; k < NC; ++k)
+                cv[q][r][k] = (js[q] >= 0 && e[r] >= 0) ? (double)pj[base[r] + coff[k]] : 0.0;
           }
-          __syncwarp();  // the tiles are restaged by the next batch
           double lmax[CB];
 #pragma unroll
           for (int q = 0; q < CB; ++q) {
@@ -3629,13 +3570,7 @@ static int transport_impl(const phj_transport_args* a) {
   // deep and the activity must reach +-2 planes -- measured 2x slower)
   static const bool one_sweep = getenv("PHJ_TRANSPORT_T1") && atoi(getenv("PHJ_TRANSPORT_T1"));
   if (one_sweep || D == 3 || a->phi_dtype == PHJ_F32 || banded) {  // fp32 phi / banded: one-sweep kernel
-    // weights, per-colour max / done, entry octants, then per warp the halo
-    // tiles of one colour batch
-    const size_t tcb = D == 2 ? PHJ_TCB2 : 2;
-    const size_t pts = a->phi_dtype == PHJ_F32 ? 4 : 8;
-    size_t smem = (size_t)align_up((int64_t)(nent | 1) * (1 << D) * 8 + (int64_t)p.R * 12 + nent,
-                                   16) +
-                  (size_t)kWarps * tcb * TileShape<D>::N * pts + 16;
+    size_t smem = (size_t)(nent | 1) * (1 << D) * 8 + (size_t)p.R * 12 + (size_t)nent + 16;
     if (a->phi_dtype == PHJ_F32)
       return coop_launch(transport_kernel<D, float>, (p.tg.total + kWarps - 1) / kWarps, smem,
                          args, stream, nullptr);
