@@ -95,7 +95,8 @@ struct SolveParams {
   unsigned long long* evals;
   unsigned long long* pcount;  // [R][3] node relaxations, logical, executed evals (or NULL)
   int32_t* info;
-  int prune;  // exact octant pruning on (PHJ_SOLVE_NO_PRUNE clears it)
+  int prune;  // bit 0: exact octant pruning (PHJ_SOLVE_NO_PRUNE clears it),
+              // bit 1: fp32 screening (PHJ_SOLVE_NO_SCREEN clears it)
   double act;  // a node change marks the neighbour blocks only if > act (0 = exact)
   int inner;   // block-local relaxations per sweep (>= 1)
   // AO3 conical reduction (NULL ao3_fb = off)
@@ -786,7 +787,7 @@ __device__ __forceinline__ int preferred_octant(const T* lt) {
 // gets the real (non-padding) ones among them.
 template <int D, typename T, int NB, int RULE, int COST, bool SLOW, typename Hook,
           bool AO3 = false>
-__device__ __forceinline__ int eval_sweep(const T* lt, bool prune_on, const StencilSmem<D, T>& s,
+__device__ __forceinline__ int eval_sweep(const T* lt, int prune_on, const StencilSmem<D, T>& s,
                                           const int* os, const uint32_t (&fm)[NB],
                                           const T (&ncoef)[NB], const bool (&comp)[NB],
                                           MinAcc<T> (&mn)[NB], T (&best)[NB], int (&bidx)[NB],
@@ -821,7 +822,8 @@ __device__ __forceinline__ int eval_sweep(const T* lt, bool prune_on, const Sten
   constexpr bool CAN_PRUNE = COST == PHJ_COST_NODE && PHJ_PRUNE;
   constexpr bool SCREEN = PHJ_SCREEN && sizeof(T) == 8 && RULE == PHJ_RULE_KRUZKOV &&
                           COST == PHJ_COST_NODE && !AO3;
-  const bool prune = CAN_PRUNE && prune_on;
+  const bool prune = CAN_PRUNE && (prune_on & 1);
+  const bool screen = SCREEN && (prune_on & 2);
   const int first = prune ? preferred_octant<D, T>(lt) : 0;
   OctNb<D, T, NB> cell;
   cell.load(lt, first);
@@ -836,9 +838,14 @@ __device__ __forceinline__ int eval_sweep(const T* lt, bool prune_on, const Sten
   // minima (an upper bound of the new ones: values only decreased), so the
   // preferred octant is prunable too
   if (!(prune && warm) || __any_sync(0xffffffffu, octant_needed<D, T, NB>(cell, comp, mn))) {
-    if constexpr (SCREEN)
-      eval_octant_screened<D, NB, SLOW>(cell, first, s, os, fm, mn, m32);
-    else
+    bool done = false;
+    if constexpr (SCREEN) {
+      if (screen) {
+        eval_octant_screened<D, NB, SLOW>(cell, first, s, os, fm, mn, m32);
+        done = true;
+      }
+    }
+    if (!done)
       eval_octant<D, T, NB, RULE, COST, SLOW, 0, OctNb<D, T, NB>, AO3>(cell, first, s, os, fm,
                                                                        ncoef, nullptr, mn, best,
                                                                        bidx, al);
@@ -855,9 +862,14 @@ __device__ __forceinline__ int eval_sweep(const T* lt, bool prune_on, const Sten
 #endif
     cell.load(lt, O);
     if (prune && !__any_sync(0xffffffffu, octant_needed<D, T, NB>(cell, comp, mn))) continue;
-    if constexpr (SCREEN)
-      eval_octant_screened<D, NB, SLOW>(cell, O, s, os, fm, mn, m32);
-    else
+    bool done = false;
+    if constexpr (SCREEN) {
+      if (screen) {
+        eval_octant_screened<D, NB, SLOW>(cell, O, s, os, fm, mn, m32);
+        done = true;
+      }
+    }
+    if (!done)
       eval_octant<D, T, NB, RULE, COST, SLOW, 0, OctNb<D, T, NB>, AO3>(cell, O, s, os, fm, ncoef,
                                                                        nullptr, mn, best, bidx, al);
     n_ent += os[O + 1] - os[O];
@@ -1247,12 +1259,12 @@ __device__ __forceinline__ int sweep_block(const SolveParams& p, const StencilSm
       int n_ent, n_real;
       if (p.ao3_fb) {
         n_ent = eval_sweep<D, T, NB, RULE, COST, true, decltype(once), true>(
-            lt, p.prune != 0, s, os, fm, ncoef, comp, mn, best, bidx, once, n_real, &al, warm);
+            lt, p.prune, s, os, fm, ncoef, comp, mn, best, bidx, once, n_real, &al, warm);
       } else if (slow) {
-        n_ent = eval_sweep<D, T, NB, RULE, COST, true>(lt, p.prune != 0, s, os, fm, ncoef, comp,
+        n_ent = eval_sweep<D, T, NB, RULE, COST, true>(lt, p.prune, s, os, fm, ncoef, comp,
                                                        mn, best, bidx, once, n_real, nullptr, warm);
       } else {
-        n_ent = eval_sweep<D, T, NB, RULE, COST, false>(lt, p.prune != 0, s, os, fm, ncoef, comp,
+        n_ent = eval_sweep<D, T, NB, RULE, COST, false>(lt, p.prune, s, os, fm, ncoef, comp,
                                                         mn, best, bidx, once, n_real, nullptr,
                                                         warm);
       }
@@ -3408,7 +3420,8 @@ static int solve_impl(const phj_solve_args* a) {
   p.evals = a->evals;
   p.pcount = a->patch_counts;
   p.info = a->info;
-  p.prune = (a->options & PHJ_SOLVE_NO_PRUNE) ? 0 : 1;
+  p.prune = ((a->options & PHJ_SOLVE_NO_PRUNE) ? 0 : 1) |
+            ((a->options & PHJ_SOLVE_NO_SCREEN) ? 0 : 2);
   p.act = a->act_tol;
   p.inner = a->inner_sweeps < 1 ? 1 : a->inner_sweeps;
   p.ao3_fb = a->ao3_fb;
