@@ -175,10 +175,6 @@ typedef struct phj_solve_args {
  * in v0, patch_sweeps = equivalent sweeps (blocks swept / initial blocks),
  * maxch_hist untouched */
 #define PHJ_SOLVE_ASYNC 2
-/* phj_solve_args.options: evaluate every candidate in the working precision
- * (disable the fp32 screening of fp64 Kruzkov solves; for verification --
- * results are bit-identical either way) */
-#define PHJ_SOLVE_NO_SCREEN 4
 
 int64_t phj_solve_workspace_bytes(const phj_grid* g, int32_t n_patches, int32_t max_sweeps);
 /* PHJ_UNROLL(dim) this library was built with (octant-group padding) */

@@ -64,7 +64,6 @@ class SolveArgs(ctypes.Structure):
 
 SOLVE_NO_PRUNE = 1  # PHJ_SOLVE_NO_PRUNE
 SOLVE_ASYNC = 2  # PHJ_SOLVE_ASYNC
-SOLVE_NO_SCREEN = 4  # PHJ_SOLVE_NO_SCREEN
 TRANSPORT_ASYNC = 1  # PHJ_TRANSPORT_ASYNC
 
 

@@ -95,8 +95,7 @@ struct SolveParams {
   unsigned long long* evals;
   unsigned long long* pcount;  // [R][3] node relaxations, logical, executed evals (or NULL)
   int32_t* info;
-  int prune;  // bit 0: exact octant pruning (PHJ_SOLVE_NO_PRUNE clears it),
-              // bit 1: fp32 screening (PHJ_SOLVE_NO_SCREEN clears it)
+  int prune;  // exact octant pruning on (PHJ_SOLVE_NO_PRUNE clears it)
   double act;  // a node change marks the neighbour blocks only if > act (0 = exact)
   int inner;   // block-local relaxations per sweep (>= 1)
   // AO3 conical reduction (NULL ao3_fb = off)
@@ -124,14 +123,11 @@ struct StencilSmem {
   uint32_t* nz;  // [nent]
   int* oct;      // [ncls][2^D + 1]
   int* oreal;    // [ncls][2^D] real (non-padding) entries per octant (solve kernels)
-  float* wf;     // [nent][2^D] the weights rounded to fp32 (fp32 screening, T = double)
   static __host__ __device__ int64_t bytes(int ncls, int nc) {
     int64_t nent = (int64_t)ncls * nc;
     int64_t b = nent * (1 << D) * sizeof(T) + 2 * nent * sizeof(T);
     b = (b + 15) / 16 * 16;
     b += nent * 4 + (int64_t)ncls * ((1 << D) + 1) * 4 + (int64_t)ncls * (1 << D) * 4;
-    b = (b + 15) / 16 * 16;
-    b += nent * (1 << D) * 4;
     return (b + 15) / 16 * 16;
   }
 };
@@ -148,8 +144,6 @@ __device__ inline StencilSmem<D, T> carve_stencil(unsigned char* base, int ncls,
   s.nz = (uint32_t*)p;
   s.oct = (int*)(s.nz + nent);
   s.oreal = s.oct + (int64_t)ncls * ((1 << D) + 1);
-  unsigned char* q = (unsigned char*)(s.oreal + (int64_t)ncls * (1 << D));
-  s.wf = (float*)(base + ((q - base + 15) / 16 * 16));
   return s;
 }
 
@@ -173,10 +167,7 @@ __device__ inline void stage_entries(const StencilSmem<D, T>& s, int dst0, int s
     T sum = T(0);
     for (int k = 0; k < last; ++k) sum = sum + w[k];
     w[last] = T(1) - sum;
-    for (int k = 0; k < NC; ++k) {
-      s.w[(int64_t)dst * NC + k] = w[k];
-      s.wf[(int64_t)dst * NC + k] = (float)w[k];
-    }
+    for (int k = 0; k < NC; ++k) s.w[(int64_t)dst * NC + k] = w[k];
     s.nz[dst] = nzmask[src];
     const double c = cost ? cost[src] : 0.0;
     if (RULE == PHJ_RULE_KRUZKOV) {
@@ -669,96 +660,6 @@ struct OctNb {
   }
 };
 
-// ---- exact minimum with fp32 screening -------------------
-// Kruzkov workloads in fp64 are FP64-pipe bound, yet a node's minimum is
-// attained by one or two of its ~12 octant controls.  Every candidate of the
-// octant is first evaluated in fp32 (corner values and weights rounded to
-// fp32, the same FMA chain): |x32 - x64| <= e ~ 6e-7 for values in [0, 1].
-// Only entries whose fp32 value lies within kScreenDelta (>= 2e) of the
-// node's running fp32 minimum -- for some node of the warp -- are evaluated
-// in fp64, with exactly the arithmetic of eval_octant.  The true minimiser c*
-// is always among them: when it is screened the running minimum is either
-// the start value (an upper bound of the node's current minimum v* = x64(c*))
-// or an fp32 candidate value >= v* - e, so x32(c*) <= v* + e <= min + 2e.  The
-// fp64 minimum is therefore bit-identical to evaluating every entry in fp64.
-#ifndef PHJ_SCREEN
-#define PHJ_SCREEN 1
-#endif
-constexpr float kScreenDelta = 4.0e-6f;
-
-template <int D, int NB, bool SLOW>
-__device__ __forceinline__ void eval_octant_screened(const OctNb<D, double, NB>& cell, int O,
-                                                     const StencilSmem<D, double>& s,
-                                                     const int* os, const uint32_t (&fm)[NB],
-                                                     MinAcc<double> (&mn)[NB],
-                                                     float (&m32)[NB]) {
-  constexpr int NC = 1 << D;
-  constexpr int NR = 1 << (D - 1);
-  constexpr int U = (D == 2) ? PHJ_KUNROLL2 : PHJ_UNROLL(D);  // divides the host padding
-  const int e0 = os[O], e1 = os[O + 1];
-  if (e0 >= e1) return;
-  float cf[NR][NB + 1];
-#pragma unroll
-  for (int i = 0; i < NR; ++i)
-#pragma unroll
-    for (int j = 0; j <= NB; ++j) cf[i][j] = (float)cell.v[i][j];
-  auto c32 = [&](int K, int r) -> float {
-    if constexpr (D == 2) return cf[K & 1][r + ((K >> 1) & 1)];
-    else return cf[(K & 1) * 2 + ((K >> 1) & 1)][r + ((K >> 2) & 1)];
-  };
-  // fp32 pass: running fp32 minima, entries within the screening margin
-  uint32_t bits = 0u;
-  for (int e = e0; e < e1; e += U) {
-    float w[U][NC];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-#pragma unroll
-      for (int i = 0; i < NC / 4; ++i) {
-        const float4 q = reinterpret_cast<const float4*>(s.wf + (int64_t)(e + u) * NC)[i];
-        w[u][4 * i] = q.x;
-        w[u][4 * i + 1] = q.y;
-        w[u][4 * i + 2] = q.z;
-        w[u][4 * i + 3] = q.w;
-      }
-    }
-    uint32_t nz[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) nz[u] = SLOW ? s.nz[e + u] : 0u;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-#pragma unroll
-      for (int r = 0; r < NB; ++r) {
-        float x = w[u][0] * c32(0, r);
-#pragma unroll
-        for (int K = 1; K < NC; ++K) x = fmaf(w[u][K], c32(K, r), x);
-        if (SLOW && (fm[r] & nz[u])) x = __int_as_float(0x7f800000);  // rejected: +inf
-        m32[r] = fminf(m32[r], x);
-        if (x <= m32[r] + kScreenDelta) bits |= 1u << (e - e0 + u);
-      }
-    }
-  }
-  // fp64 pass over the screened entries of the warp (eval_octant arithmetic)
-  uint32_t wb = __reduce_or_sync(0xffffffffu, bits);
-  while (wb) {
-    const int b = __ffs(wb) - 1;
-    wb &= wb - 1u;
-    const int e = e0 + b;
-    double w[1][NC];
-    load_weights<double, NC>(s.w + (int64_t)e * NC, w[0]);
-    const uint32_t nz = SLOW ? s.nz[e] : 0u;
-    double acc[1][NB];
-#pragma unroll
-    for (int r = 0; r < NB; ++r) acc[0][r] = w[0][0] * cell.template corner<0>(r);
-    ChainStep<D, double, NB, 1, 1, OctNb<D, double, NB>>::run(cell, w, acc);
-#pragma unroll
-    for (int r = 0; r < NB; ++r) {
-      double x = acc[0][r];
-      if (SLOW && (fm[r] & nz)) x = big_value<double>();
-      mn[r].take(x);
-    }
-  }
-}
-
 // the octant of steepest descent at the lane's first node, majority over
 // the warp (warp-uniform)
 template <int D, typename T>
@@ -787,7 +688,7 @@ __device__ __forceinline__ int preferred_octant(const T* lt) {
 // gets the real (non-padding) ones among them.
 template <int D, typename T, int NB, int RULE, int COST, bool SLOW, typename Hook,
           bool AO3 = false>
-__device__ __forceinline__ int eval_sweep(const T* lt, int prune_on, const StencilSmem<D, T>& s,
+__device__ __forceinline__ int eval_sweep(const T* lt, bool prune_on, const StencilSmem<D, T>& s,
                                           const int* os, const uint32_t (&fm)[NB],
                                           const T (&ncoef)[NB], const bool (&comp)[NB],
                                           MinAcc<T> (&mn)[NB], T (&best)[NB], int (&bidx)[NB],
@@ -820,35 +721,19 @@ __device__ __forceinline__ int eval_sweep(const T* lt, int prune_on, const Stenc
   }
 #endif
   constexpr bool CAN_PRUNE = COST == PHJ_COST_NODE && PHJ_PRUNE;
-  constexpr bool SCREEN = PHJ_SCREEN && sizeof(T) == 8 && RULE == PHJ_RULE_KRUZKOV &&
-                          COST == PHJ_COST_NODE && !AO3;
-  const bool prune = CAN_PRUNE && (prune_on & 1);
-  const bool screen = SCREEN && (prune_on & 2);
+  const bool prune = CAN_PRUNE && prune_on;
   const int first = prune ? preferred_octant<D, T>(lt) : 0;
   OctNb<D, T, NB> cell;
   cell.load(lt, first);
   int n_ent = 0;
   n_real = 0;
-  // fp32 screening minima (non-computing nodes never select an entry)
-  float m32[NB];
-#pragma unroll
-  for (int r = 0; r < NB; ++r)
-    m32[r] = comp[r] ? __double2float_ru((double)mn[r].get()) : __int_as_float(0xff800000);
   // warm: the running minima start at the previous block-local relaxation's
   // minima (an upper bound of the new ones: values only decreased), so the
   // preferred octant is prunable too
   if (!(prune && warm) || __any_sync(0xffffffffu, octant_needed<D, T, NB>(cell, comp, mn))) {
-    bool done = false;
-    if constexpr (SCREEN) {
-      if (screen) {
-        eval_octant_screened<D, NB, SLOW>(cell, first, s, os, fm, mn, m32);
-        done = true;
-      }
-    }
-    if (!done)
-      eval_octant<D, T, NB, RULE, COST, SLOW, 0, OctNb<D, T, NB>, AO3>(cell, first, s, os, fm,
-                                                                       ncoef, nullptr, mn, best,
-                                                                       bidx, al);
+    eval_octant<D, T, NB, RULE, COST, SLOW, 0, OctNb<D, T, NB>, AO3>(cell, first, s, os, fm,
+                                                                     ncoef, nullptr, mn, best,
+                                                                     bidx, al);
     n_ent = os[first + 1] - os[first];
     n_real = s.oreal[first];
   }
@@ -862,16 +747,8 @@ __device__ __forceinline__ int eval_sweep(const T* lt, int prune_on, const Stenc
 #endif
     cell.load(lt, O);
     if (prune && !__any_sync(0xffffffffu, octant_needed<D, T, NB>(cell, comp, mn))) continue;
-    bool done = false;
-    if constexpr (SCREEN) {
-      if (screen) {
-        eval_octant_screened<D, NB, SLOW>(cell, O, s, os, fm, mn, m32);
-        done = true;
-      }
-    }
-    if (!done)
-      eval_octant<D, T, NB, RULE, COST, SLOW, 0, OctNb<D, T, NB>, AO3>(cell, O, s, os, fm, ncoef,
-                                                                       nullptr, mn, best, bidx, al);
+    eval_octant<D, T, NB, RULE, COST, SLOW, 0, OctNb<D, T, NB>, AO3>(cell, O, s, os, fm, ncoef,
+                                                                     nullptr, mn, best, bidx, al);
     n_ent += os[O + 1] - os[O];
     n_real += s.oreal[O];
   }
@@ -1259,12 +1136,12 @@ __device__ __forceinline__ int sweep_block(const SolveParams& p, const StencilSm
       int n_ent, n_real;
       if (p.ao3_fb) {
         n_ent = eval_sweep<D, T, NB, RULE, COST, true, decltype(once), true>(
-            lt, p.prune, s, os, fm, ncoef, comp, mn, best, bidx, once, n_real, &al, warm);
+            lt, p.prune != 0, s, os, fm, ncoef, comp, mn, best, bidx, once, n_real, &al, warm);
       } else if (slow) {
-        n_ent = eval_sweep<D, T, NB, RULE, COST, true>(lt, p.prune, s, os, fm, ncoef, comp,
+        n_ent = eval_sweep<D, T, NB, RULE, COST, true>(lt, p.prune != 0, s, os, fm, ncoef, comp,
                                                        mn, best, bidx, once, n_real, nullptr, warm);
       } else {
-        n_ent = eval_sweep<D, T, NB, RULE, COST, false>(lt, p.prune, s, os, fm, ncoef, comp,
+        n_ent = eval_sweep<D, T, NB, RULE, COST, false>(lt, p.prune != 0, s, os, fm, ncoef, comp,
                                                         mn, best, bidx, once, n_real, nullptr,
                                                         warm);
       }
@@ -3420,8 +3297,7 @@ static int solve_impl(const phj_solve_args* a) {
   p.evals = a->evals;
   p.pcount = a->patch_counts;
   p.info = a->info;
-  p.prune = ((a->options & PHJ_SOLVE_NO_PRUNE) ? 0 : 1) |
-            ((a->options & PHJ_SOLVE_NO_SCREEN) ? 0 : 2);
+  p.prune = (a->options & PHJ_SOLVE_NO_PRUNE) ? 0 : 1;
   p.act = a->act_tol;
   p.inner = a->inner_sweeps < 1 ? 1 : a->inner_sweeps;
   p.ao3_fb = a->ao3_fb;

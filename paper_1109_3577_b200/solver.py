@@ -425,8 +425,7 @@ def device_solve(plan: StencilPlan, work: torch.Tensor, lab: torch.Tensor, fmask
                  n_patches: int, *, rule: str, dtype: str, tol: float, max_sweeps: int,
                  mine: Optional[torch.Tensor] = None, sync: bool = True,
                  prune: bool = True, ao3=None, act_tol: float = 0.0,
-                 schedule: str = "jacobi", inner: int = 1, bands=None,
-                 screen: bool = True) -> DeviceSolveResult:
+                 schedule: str = "jacobi", inner: int = 1, bands=None) -> DeviceSolveResult:
     """One phj_solve launch: all patches of `lab`, to per-patch convergence.
     ``bands`` (patchy.band_schedule) prepends the value-ordered pass."""
     lib = _lib.load()
@@ -462,9 +461,8 @@ def device_solve(plan: StencilPlan, work: torch.Tensor, lab: torch.Tensor, fmask
     a.maxch_hist = _lib.ptr(mc)
     a.evals = _lib.ptr(ev)
     a.info = _lib.ptr(info)
-    a.options = ((0 if prune else _lib.SOLVE_NO_PRUNE) |
-                 (_lib.SOLVE_ASYNC if schedule == "async" else 0) |
-                 (0 if screen else _lib.SOLVE_NO_SCREEN))
+    a.options = (0 if prune else _lib.SOLVE_NO_PRUNE) | (
+        _lib.SOLVE_ASYNC if schedule == "async" else 0)
     a.act_tol = float(act_tol)
     a.inner_sweeps = int(inner)
     a.patch_counts = _lib.ptr(pc)

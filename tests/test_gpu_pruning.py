@@ -61,28 +61,3 @@ def test_pruning_is_bit_exact(name, kw):
     assert a.executed < b.executed, (a.executed, b.executed)
     print(f"{name}: executed {a.executed} of {b.executed} entries "
           f"({a.executed / b.executed:.2f}), sweeps {list(a.patch_sweeps)[:4]}")
-
-
-@pytest.mark.parametrize("name,kw,dtype", [
-    ("c2", dict(n=257), "float64"),
-    ("c3", dict(n=65), "float64"),
-    ("c5", dict(n=65), "float64"),
-    ("c5", dict(n=65), "float32"),   # fp32 workloads never screen: trivially equal
-])
-def test_fp32_screening_is_bit_exact(name, kw, dtype):
-    # the fp32-screened exact minimum against evaluating
-    # every candidate in fp64: identical fields and sweep counts (Jacobi
-    # schedule, deterministic), same logical work
-    w = configs.CONFIGS[name](dtype=dtype, **kw)
-    fplan, vf, lab, R = _patch_inputs(w)
-    fmask = fplan.fmask_from_labels(lab)
-    cfg = w.cfg
-    runs = []
-    for screen in (True, False):
-        res = device_solve(fplan, vf.clone(), lab, fmask, R, rule=cfg.rule, dtype=cfg.dtype,
-                           tol=cfg.tol, max_sweeps=cfg.sweep_limit(fplan.grid), screen=screen)
-        runs.append(res)
-    a, b = runs
-    assert torch.equal(a.values, b.values), "screened sweep differs from the fp64 sweep"
-    assert (a.patch_sweeps == b.patch_sweeps).all()
-    assert a.evals == b.evals
