@@ -2108,7 +2108,27 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
         }
       }
       unsigned long long changed = 0;
-      if (__any_sync(FULL, any)) {
+      if (copy_only && __any_sync(FULL, any)) {
+        // banded pass, last visit of the block: its movers' values into the
+        // other buffer (no gathers; the values did not change in this sweep)
+        unsigned long long todo = cm;
+        while (todo) {
+          const int j = __ffsll((long long)todo) - 1;
+          todo &= todo - 1;
+          const PT* pj = pin + (int64_t)j * p.plane;
+          PT* qj = pout + (int64_t)j * p.plane;
+#pragma unroll
+          for (int r = 0; r < NB; ++r) {
+            if (e[r] < 0) continue;
+            const PT v = pj[f0 + r];
+            qj[f0 + r] = v;
+            if (per0) {
+              if (c[0] == 0) qj[f0 + r + ghost_shift] = v;
+              else if (c[0] == M0 - 1) qj[f0 + r - ghost_shift] = v;
+            }
+          }
+        }
+      } else if (__any_sync(FULL, any)) {
         // the node itself is corner kself of its foot cell (feet lie in one of
         // the 2^D cells around the node): its old value comes with the corners
         int kself[NB];

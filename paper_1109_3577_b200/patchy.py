@@ -78,6 +78,8 @@ BAND_CAP_PER_NODE = 1.5
 BAND_SCALE = float(os.environ.get("PHJ_BAND_SCALE", "1"))
 #: fp32 workloads store the colour fields in fp32
 TRANSPORT_PHI_FP32 = True
+#: A/B knob: fp32 colour storage for fp64 workloads too (off: fp64 semantics)
+TRANSPORT_PHI_FP32_ALWAYS = os.environ.get("PHJ_PHI_FP32", "0") != "0"
 
 
 @dataclass
@@ -411,7 +413,8 @@ def _transport_and_argmax(fplan: StencilPlan, fb: torch.Tensor, parts, color_tol
         tsched = schedule if (fplan.grid.dim == 2 or TRANSPORT_ASYNC_3D) else "jacobi"
         # fp32 workloads keep their colour fields in fp32 too (half the
         # footprint: 35 GB instead of 70 GB at config 5)
-        pdt = torch.float32 if (dtype == "float32" and TRANSPORT_PHI_FP32) else torch.float64
+        pdt = torch.float32 if ((dtype == "float32" and TRANSPORT_PHI_FP32) or
+                                TRANSPORT_PHI_FP32_ALWAYS) else torch.float64
         bands = None
         if (TRANSPORT_BANDED and tsched == "jacobi" and banded_applies(fplan) and
                 key_work is not None):
