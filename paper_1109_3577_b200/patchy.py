@@ -73,8 +73,12 @@ SOLVE_BAND_WINDOW = tuple(int(x) for x in os.environ.get("PHJ_SOLVE_BAND_WINDOW"
 #: profiles/r2_band_ab.jsonl: 1 -> 2.7 s, 2 -> 341 ms, 3 -> 401 ms)
 SOLVE_BAND_INNER = int(os.environ.get("PHJ_BAND_INNER", "2"))
 BAND_CAP_PER_NODE = 1.5
-#: the solve's pass without grid barriers (rows claimed in order, in place)
-SOLVE_BAND_ASYNC = os.environ.get("PHJ_BAND_ASYNC", "1") != "0"
+#: the solve's pass without grid barriers (rows claimed in order, in place).
+#: Off: without the barrier warps run ahead of the front, later rows are
+#: relaxed before their upstream values arrive and the cleanup does most of
+#: the work (C5 patch solve 341 -> 613 ms, C3 39 -> 219 ms,
+#: profiles/r2r_band_async_ab.jsonl)
+SOLVE_BAND_ASYNC = os.environ.get("PHJ_BAND_ASYNC", "0") != "0"
 #: band width in units of the smallest SL time step (coarser bands: fewer,
 #: thicker sweeps)
 BAND_SCALE = float(os.environ.get("PHJ_BAND_SCALE", "1"))
