@@ -164,12 +164,6 @@ typedef struct phj_solve_args {
   int32_t n_band;
   int32_t band_inner;        /* block-local relaxations per visit in the pass
                                 (0 = inner_sweeps) */
-  int32_t band_entries;      /* PHJ_SOLVE_ASYNC only, > 0: run the pass without
-                                grid barriers -- the first band_entries entries
-                                (rows 0 .. n_band - 1) claimed in order by every
-                                warp, improvements published in place with an
-                                atomic minimum; 0 = the
-                                cooperative Jacobi pass */
   void* stream;               /* cudaStream_t */
 } phj_solve_args;
 

@@ -59,7 +59,7 @@ class SolveArgs(ctypes.Structure):
                 ("info", P), ("ao3_fb", P), ("ao3_mask", P), ("ao3_count", P),
                 ("ao3_words", I32), ("options", I32), ("act_tol", D), ("inner_sweeps", I32),
                 ("patch_counts", P), ("band_list", P), ("band_off", P), ("n_band", I32),
-                ("band_inner", I32), ("band_entries", I32), ("stream", P)]
+                ("band_inner", I32), ("stream", P)]
 
 
 SOLVE_NO_PRUNE = 1  # PHJ_SOLVE_NO_PRUNE

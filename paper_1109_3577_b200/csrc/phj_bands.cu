@@ -48,51 +48,63 @@ inline int64_t band_scratch_bytes(const phj_grid& g, int64_t rows) {
          256 + 2 * align_up(rows * 4, 256);
 }
 
-// warp block of internal serial s (Blk<D> geometry, axis 0 slowest)
-template <int D>
-__device__ __forceinline__ int block_of(const phj_grid& g, const TileGrid& tg, int64_t s) {
-  using B = Blk<D>;
-  if (D == 3) {
-    const int64_t i2 = s % g.shape[2], r = s / g.shape[2];
-    const int64_t i1 = r % g.shape[1], i0 = r / g.shape[1];
-    return (int)((i0 * tg.n[1] + i1 / B::BY) * tg.n[2] + i2 / B::BX);
-  } else {
-    const int64_t i1 = s % g.shape[1], i0 = s / g.shape[1];
-    return (int)((i0 / B::BY) * tg.n[1] + i1 / B::BX);
-  }
-}
-
+// One warp per warp block (the Blk<D> lane -> node map of the sweeps): the
+// smallest / largest key of its scheduled nodes by a warp reduction, the
+// time transform (monotone) applied to the two extremes only.
 template <int D, typename T>
 __global__ void band_times_kernel(phj_grid g, TileGrid tg, const T* __restrict__ key, int kruzkov,
                                   const uint8_t* __restrict__ nodes, BandScratch s) {
-  const int64_t n = g.shape[0] * g.shape[1] * (D == 3 ? g.shape[2] : 1);
+  using B = Blk<D>;
+  constexpr int last = D - 1;
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int gw = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int nw = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
   unsigned long long lmax = 0ull;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    if (!nodes[i]) continue;
+  for (int b = gw; b < tg.total; b += nw) {
     int c[3];
-    int64_t r = i;
-    for (int ax = D - 1; ax >= 0; --ax) {
-      c[ax] = (int)(r % g.shape[ax]);
-      r /= g.shape[ax];
+    const bool ok = lane_nodes<D>(g, tg, b, lane, c);
+    int64_t ser = 0, f = 0;
+#pragma unroll
+    for (int ax = 0; ax < D; ++ax) {
+      ser = ser * g.shape[ax] + c[ax];
+      f += (int64_t)(c[ax] + 1) * g.strides[ax];
     }
-    int64_t f = 0;
-    for (int ax = 0; ax < D; ++ax) f += (int64_t)(c[ax] + 1) * g.strides[ax];
-    double t = (double)key[f];
-    if (kruzkov) t = -log1p(-fmin(t, 1.0 - 1e-16));
-    t = fmax(t, 0.0);
-    const unsigned long long bits = (unsigned long long)__double_as_longlong(t);
-    const int b = block_of<D>(g, tg, i);
-    atomicMin(&s.tmin[b], bits);
-    atomicMax(&s.tmax[b], bits);
-    lmax = max(lmax, bits);
+    double vmin = 1.0e300, vmax = -1.0;
+#pragma unroll
+    for (int r = 0; r < B::NB; ++r) {
+      if (!(ok && c[last] + r < g.shape[last]) || !nodes[ser + r]) continue;
+      const double v = (double)key[f + r];
+      vmin = fmin(vmin, v);
+      vmax = fmax(vmax, v);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      vmin = fmin(vmin, __shfl_xor_sync(FULL, vmin, off));
+      vmax = fmax(vmax, __shfl_xor_sync(FULL, vmax, off));
+    }
+    if (lane == 0) {
+      unsigned long long b0 = ~0ull, b1 = 0ull;
+      if (vmin < 1.0e300) {  // the block holds a scheduled node
+        double t0 = vmin, t1 = vmax;
+        if (kruzkov) {
+          t0 = -log1p(-fmin(t0, 1.0 - 1e-16));
+          t1 = -log1p(-fmin(t1, 1.0 - 1e-16));
+        }
+        b0 = (unsigned long long)__double_as_longlong(fmax(t0, 0.0));
+        b1 = (unsigned long long)__double_as_longlong(fmax(t1, 0.0));
+        lmax = max(lmax, b1);
+      }
+      s.tmin[b] = b0;
+      s.tmax[b] = b1;
+    }
   }
-  for (int off = 16; off > 0; off >>= 1) lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, off));
-  if ((threadIdx.x & 31) == 0 && lmax) atomicMax(&s.glob[0], lmax);
+  if (lane == 0 && lmax) atomicMax(&s.glob[0], lmax);
 }
 
 __global__ void band_ranges_kernel(int total, double delta, int lo_w, int hi_w, int max_row,
                                    BandScratch s) {
+  unsigned long long entries = 0ull, blocks = 0ull, top = 0ull;
   for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < total; b += gridDim.x * blockDim.x) {
     s.lo[b] = -1;
     if (s.tmin[b] == ~0ull) continue;
@@ -103,11 +115,22 @@ __global__ void band_ranges_kernel(int total, double delta, int lo_w, int hi_w, 
     const int lo = max(0, k0 - hi_w), hi = k1 + lo_w;
     s.lo[b] = lo;
     s.hi[b] = hi;
-    atomicAdd(&s.glob[1], (unsigned long long)(hi - lo + 2));
-    atomicMax(&s.glob[2], (unsigned long long)(hi + 2));
-    atomicAdd(&s.glob[3], 1ull);
+    entries += (unsigned long long)(hi - lo + 2);
+    top = max(top, (unsigned long long)(hi + 2));
+    blocks += 1ull;
     atomicAdd(&s.diff[lo], 1);
     atomicSub(&s.diff[hi + 2], 1);
+  }
+  // totals: one atomic per warp instead of three per block on one address
+  for (int off = 16; off > 0; off >>= 1) {
+    entries += __shfl_xor_sync(0xffffffffu, entries, off);
+    blocks += __shfl_xor_sync(0xffffffffu, blocks, off);
+    top = max(top, __shfl_xor_sync(0xffffffffu, top, off));
+  }
+  if ((threadIdx.x & 31) == 0 && blocks) {
+    atomicAdd(&s.glob[1], entries);
+    atomicMax(&s.glob[2], top);
+    atomicAdd(&s.glob[3], blocks);
   }
 }
 
@@ -127,15 +150,89 @@ __global__ void band_offsets_kernel(int n_band, int final_row, int n_blocks, Ban
   for (int r = threadIdx.x; r <= n_band; r += blockDim.x) s.cursor[r] = 0;
 }
 
-__global__ void band_fill_kernel(int total, int n_band, int final_row, BandScratch s,
-                                 const int32_t* __restrict__ off, int32_t* __restrict__ list) {
-  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < total; b += gridDim.x * blockDim.x) {
-    const int lo = s.lo[b];
-    if (lo < 0) continue;
-    const int hi = s.hi[b];
-    for (int r = lo; r <= hi; ++r) list[off[r] + atomicAdd(&s.cursor[r], 1)] = b;
-    list[off[hi + 1] + atomicAdd(&s.cursor[hi + 1], 1)] = -b - 1;  // copy visit
-    if (final_row) list[off[n_band] + atomicAdd(&s.cursor[n_band], 1)] = b;
+// Append block id `val` to row r; the lanes of the warp appending to the same
+// row in this step share one cursor atomic (neighbouring blocks have nearly
+// the same rows, so a step touches a handful of rows).  All lanes call;
+// inactive ones pass r < 0.
+__device__ __forceinline__ void band_append(int r, int val, const BandScratch& s,
+                                            const int32_t* __restrict__ off,
+                                            int32_t* __restrict__ list) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const unsigned peers = __match_any_sync(FULL, r);
+  if (r < 0) return;
+  const int leader = __ffs(peers) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(&s.cursor[r], __popc(peers));
+  base = __shfl_sync(peers, base, leader);
+  list[off[r] + base + __popc(peers & ((1u << lane) - 1u))] = val;
+}
+
+// every third bit of x (Morton decode of one coordinate)
+__device__ __forceinline__ unsigned compact3(unsigned long long x) {
+  x &= 0x1249249249249249ull;
+  x = (x ^ (x >> 2)) & 0x10c30c30c30c30c3ull;
+  x = (x ^ (x >> 4)) & 0x100f00f00f00f00full;
+  x = (x ^ (x >> 8)) & 0x1f0000ff0000ffull;
+  x = (x ^ (x >> 16)) & 0x1f00000000ffffull;
+  x = (x ^ (x >> 32)) & 0x1fffffull;
+  return (unsigned)x;
+}
+__device__ __forceinline__ unsigned compact2(unsigned long long x) {
+  x &= 0x5555555555555555ull;
+  x = (x ^ (x >> 1)) & 0x3333333333333333ull;
+  x = (x ^ (x >> 2)) & 0x0f0f0f0f0f0f0f0full;
+  x = (x ^ (x >> 4)) & 0x00ff00ff00ff00ffull;
+  x = (x ^ (x >> 8)) & 0x0000ffff0000ffffull;
+  x = (x ^ (x >> 16)) & 0xffffffffull;
+  return (unsigned)x;
+}
+
+// Block id of position i of the fill order, or -1: blocks are appended in
+// Morton order of their coordinates (3D: cubes of kZ planes x 1 x 1 blocks
+// along a Morton curve over (plane / kZ, row block, column block)), so the
+// blocks a sweep's warps hold at the same time are neighbours in all
+// directions and share their halo rows through L1/L2 instead of DRAM.
+constexpr int kZ = 8;
+template <int D>
+__device__ __forceinline__ int fill_order_block(const TileGrid& tg, long long i) {
+  if (D == 3) {
+    const unsigned long long code = (unsigned long long)(i / kZ);
+    const int z = (int)compact3(code >> 2) * kZ + (int)(i % kZ);
+    const int y = (int)compact3(code >> 1), x = (int)compact3(code);
+    if (z >= tg.n[0] || y >= tg.n[1] || x >= tg.n[2]) return -1;
+    return (z * tg.n[1] + y) * tg.n[2] + x;
+  } else {
+    const int y = (int)compact2((unsigned long long)i >> 1), x = (int)compact2((unsigned long long)i);
+    if (y >= tg.n[0] || x >= tg.n[1]) return -1;
+    return y * tg.n[1] + x;
+  }
+}
+
+template <int D>
+__global__ void band_fill_kernel(TileGrid tg, long long n_pos, int n_band, int final_row,
+                                 BandScratch s, const int32_t* __restrict__ off,
+                                 int32_t* __restrict__ list) {
+  const unsigned FULL = 0xffffffffu;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long rounds = (n_pos + stride - 1) / stride;
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (long long k = 0; k < rounds; ++k, i += stride) {
+    const int b = i < n_pos ? fill_order_block<D>(tg, i) : -1;
+    const int lo = b >= 0 ? s.lo[b] : -1;
+    const int hi = lo < 0 ? -2 : s.hi[b];
+    // the warp walks rows from its smallest lo to its largest hi + 1
+    int wlo = lo < 0 ? 0x7fffffff : lo, whi = hi + 1;
+    for (int o = 16; o > 0; o >>= 1) {
+      wlo = min(wlo, __shfl_xor_sync(FULL, wlo, o));
+      whi = max(whi, __shfl_xor_sync(FULL, whi, o));
+    }
+    for (int r = wlo; r <= whi; ++r) {
+      const bool in = lo >= 0 && r >= lo && r <= hi + 1;
+      band_append(in ? r : -1, r <= hi ? b : -b - 1, s, off, list);  // hi + 1: the copy visit
+    }
+    if (final_row && __any_sync(FULL, lo >= 0))
+      band_append(lo >= 0 ? n_band : -1, b, s, off, list);
   }
 }
 
@@ -160,12 +257,9 @@ static int band_count_impl(const phj_grid* g, int32_t dtype, int32_t rule, const
   const TileGrid tg = make_tile_grid<D>(*g);
   const int64_t rows = band_rows(max_bands, lo_w, hi_w);
   BandScratch s = carve_bands<D>(*g, scratch, rows);
-  PHJ_CUDA(cudaMemsetAsync(s.tmin, 0xff, 8 * (size_t)tg.total, st));
-  PHJ_CUDA(cudaMemsetAsync(s.tmax, 0, 8 * (size_t)tg.total, st));
   PHJ_CUDA(cudaMemsetAsync(s.glob, 0, 32, st));
   PHJ_CUDA(cudaMemsetAsync(s.diff, 0, 4 * (size_t)rows, st));
-  const int64_t n = g->shape[0] * g->shape[1] * (D == 3 ? g->shape[2] : 1);
-  const int nb = (int)std::min<int64_t>((n + 255) / 256, 8 * phj_num_sms());
+  const int nb = (int)std::min<int64_t>(((int64_t)tg.total + 7) / 8, 8 * phj_num_sms());
   const int kr = rule == PHJ_RULE_KRUZKOV;
   if (dtype == PHJ_F32)
     band_times_kernel<D, float><<<std::max(nb, 1), 256, 0, st>>>(*g, tg, (const float*)key, kr,
@@ -223,12 +317,24 @@ extern "C" int phj_band_fill(const phj_grid* g, int32_t max_bands, int32_t lo_w,
   const int64_t rows = band_rows(max_bands, lo_w, hi_w);
   const bool d3 = g->dim == 3;
   BandScratch s = d3 ? carve_bands<3>(*g, scratch, rows) : carve_bands<2>(*g, scratch, rows);
-  const int total = d3 ? make_tile_grid<3>(*g).total : make_tile_grid<2>(*g).total;
+  const TileGrid tg = d3 ? make_tile_grid<3>(*g) : make_tile_grid<2>(*g);
   band_offsets_kernel<<<1, 256, 0, st>>>(n_band, final_row, n_blocks, s, band_off);
   phj_count_launch(1);
-  const int nbb = (int)std::min<int64_t>((total + 255) / 256, 8 * phj_num_sms());
-  band_fill_kernel<<<std::max(nbb, 1), 256, 0, st>>>(total, n_band, final_row, s, band_off,
-                                                      band_list);
+  // positions of the Morton fill order (power-of-two cube around the block grid)
+  int bits = 0;
+  const int ext0 = d3 ? (tg.n[0] + kZ - 1) / kZ : tg.n[0];
+  const int ext_max = std::max(ext0, std::max(tg.n[1], d3 ? tg.n[2] : 1));
+  while ((1 << bits) < ext_max) ++bits;
+  const long long n_pos = d3 ? ((long long)kZ << (3 * bits)) : (1ll << (2 * bits));
+  // few threads per round: a round appends a compact piece of the curve (the
+  // order inside a round is the arrival order of its warps)
+  const int nbb = (int)std::min<long long>((n_pos + 255) / 256, 2 * phj_num_sms());
+  if (d3)
+    band_fill_kernel<3><<<std::max(nbb, 1), 256, 0, st>>>(tg, n_pos, n_band, final_row, s,
+                                                           band_off, band_list);
+  else
+    band_fill_kernel<2><<<std::max(nbb, 1), 256, 0, st>>>(tg, n_pos, n_band, final_row, s,
+                                                           band_off, band_list);
   phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   return PHJ_OK;

@@ -994,15 +994,6 @@ __device__ __forceinline__ void add_patch_counts(const SolveParams& p, unsigned 
   }
 }
 
-// Atomic minimum of a non-negative value (the order of the bit patterns as
-// unsigned integers is the value order for x >= 0).
-__device__ __forceinline__ void atomic_min_value(double* a, double v) {
-  atomicMin(reinterpret_cast<unsigned long long*>(a), (unsigned long long)__double_as_longlong(v));
-}
-__device__ __forceinline__ void atomic_min_value(float* a, float v) {
-  atomicMin(reinterpret_cast<unsigned int*>(a), __float_as_uint(v));
-}
-
 // One block of the value sweep, processed by one warp from its staged halo
 // tile and node inputs.  `hook` (the next block's loads, deferred marks)
 // runs exactly once.  Returns (warp-uniform) whether any node changed.
@@ -1014,7 +1005,7 @@ __device__ __forceinline__ int sweep_block(const SolveParams& p, const StencilSm
                                             unsigned long long& evals, unsigned long long& exec,
                                             unsigned long long& xreal, unsigned long long* s_pc,
                                             PatchMax& pm, PhaseTimer& tm, const Hook& hook,
-                                            bool force_copy = false, bool inplace = false) {
+                                            bool force_copy = false) {
   using B = Blk<D>;
   using S = TileShape<D>;
   using NS = NodeStage<D, T>;
@@ -1200,18 +1191,6 @@ __device__ __forceinline__ int sweep_block(const SolveParams& p, const StencilSm
         if constexpr (RULE == PHJ_RULE_KRUZKOV) big |= mych[r] > T(p.act) * (T(1) - nv);
         else big |= mych[r] > T(p.act) * max(T(1), nv);
       }
-      if (inplace) {
-        // one buffer shared with concurrent visits of the same block: only
-        // improvements, as an atomic minimum (values never rise)
-        if (comp[r] && cur[r] < old[r]) {
-          atomic_min_value(&vout[f0 + r], nv);
-          if (per0) {
-            if (c[0] == 0) atomic_min_value(&vout[f0 + r + ghost_shift], nv);
-            else if (c[0] == M0 - 1) atomic_min_value(&vout[f0 + r - ghost_shift], nv);
-          }
-        }
-        continue;
-      }
       vout[f0 + r] = nv;
       if (per0) {
         if (c[0] == 0) vout[f0 + r + ghost_shift] = nv;
@@ -1220,7 +1199,7 @@ __device__ __forceinline__ int sweep_block(const SolveParams& p, const StencilSm
     }
   } else {
     hook();
-    if (any_copy && !inplace) {
+    if (any_copy) {
 #pragma unroll
       for (int r = 0; r < NB; ++r) {
         if (!copy[r]) continue;
@@ -1798,132 +1777,6 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   if (lane == 0)
     for (int i = 0; i < 12; ++i) atomicAdd(&g_phase_cycles[i], tm.acc[i]);
 #endif
-  __shared__ unsigned long long s_ev, s_ex, s_xr;
-  __shared__ int s_blk;
-  if (threadIdx.x == 0) {
-    s_ev = 0;
-    s_ex = 0;
-    s_xr = 0;
-    s_blk = 0;
-  }
-  __syncthreads();
-  atomicAdd(&s_ev, evals);
-  atomicAdd(&s_ex, exec);
-  atomicAdd(&s_xr, xreal);
-  if (lane == 0) atomicAdd(&s_blk, blocks_done);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    atomicAdd(&p.evals[0], s_ev);
-    atomicAdd(&p.evals[1], s_ex);
-    atomicAdd(&p.evals[2], s_xr);
-    atomicAdd(&p.info[2], s_blk);
-  }
-  if (p.pcount && p.R <= kSmemPatchReduce)
-    for (int i = threadIdx.x; i < p.R * 3; i += blockDim.x)
-      if (s_pc[i]) atomicAdd(&p.pcount[i], s_pc[i]);
-}
-
-// Barrier-free value-ordered pass (PHJ_BAND_ASYNC): the band
-// schedule's rows concatenated in sweep order and claimed one entry at a time
-// by every warp of a persistent launch -- no grid barrier between rows, so a
-// row's tail overlaps the next row.  One value buffer: a visit stages its
-// tile, relaxes as in the Jacobi pass and publishes improvements with an
-// atomic minimum (two warps may hold visits of the same block from
-// consecutive rows; values never rise, the map is monotone, so every mixture
-// of older and newer neighbour values stays an upper bound of the fixed
-// point -- the same argument as the asynchronous schedule).  Copy entries
-// are skipped (no second buffer).  The asynchronous relaxation continues
-// from its result.
-template <int D, typename T, int RULE, int COST, bool WCLS>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm)
-    band_async_kernel(const __grid_constant__ SolveParams p, int n_entries, int* take) {
-  using S = TileShape<D>;
-  extern __shared__ __align__(16) unsigned char smem[];
-  constexpr bool warp_cls = WCLS;
-  const int64_t sbytes = solve_stencil_bytes<D, T>(WCLS ? 2 : 1, p.nc);
-  StencilSmem<D, T> s =
-      WCLS ? carve_stencil<D, T>(smem + (threadIdx.x >> 5) * solve_stencil_slot<D, T>(p.nc), 1,
-                                 p.nc)
-           : carve_stencil<D, T>(smem, 1, p.nc);
-  int* s_done = (int*)(smem + sbytes);
-  unsigned long long* s_max = (unsigned long long*)(s_done + ((p.R + 1) / 2 * 2));
-  unsigned long long* s_pc = s_max + min(p.R, kSmemPatchReduce);
-  T* tiles = (T*)(smem + align_up(sbytes + (int64_t)((p.R + 1) / 2 * 2) * 4 +
-                                      (int64_t)min(p.R, kSmemPatchReduce) * 8 * 4,
-                                  16));
-  T* wtile = tiles + (threadIdx.x >> 5) * 2 * S::N;
-  NodeStage<D, T>* wnodes =
-      (NodeStage<D, T>*)(tiles + kWarps * 2 * S::N) + (threadIdx.x >> 5) * 2;
-  if (!warp_cls)
-    stage_stencil<D, T, RULE>(s, p.n_classes, p.nc, p.oct_start, p.nzmask, p.weights, p.cost,
-                              p.ctrl);
-  int wcls = -1;
-  for (int i = threadIdx.x; i < p.R; i += blockDim.x)
-    s_done[i] = (p.mine == nullptr || p.mine[i]) ? 0x7fffffff : 0;
-  for (int i = threadIdx.x; i < min(p.R, kSmemPatchReduce); i += blockDim.x) s_max[i] = 0ull;
-  for (int i = threadIdx.x; i < min(p.R, kSmemPatchReduce) * 3; i += blockDim.x) s_pc[i] = 0ull;
-  __syncthreads();
-  const unsigned FULL = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  unsigned long long* gmax_row = sweep_max_slots(p.ws, 0);
-  unsigned long long evals = 0, exec = 0, xreal = 0;
-  int blocks_done = 0;
-  PatchMax pm{-1, 0.0};
-  PhaseTimer tm;
-  tm.start();
-  T* v = (T*)p.v[0];
-  // entries claimed one ahead: the next entry's id is known while the
-  // current block is relaxed, and its tile is staged into the other buffer
-  int ticket = 0;
-  if (lane == 0) ticket = atomicAdd(take, 1);
-  int t = __shfl_sync(FULL, ticket, 0);
-  struct Ent {
-    int t, e;
-  };
-  auto next_entry = [&](int from) {
-    Ent r{from, -1};
-    while (r.t < n_entries) {
-      r.e = __ldg(&p.band_list[r.t]);
-      if (r.e >= 0) break;
-      if (lane == 0) ticket = atomicAdd(take, 1);
-      r.t = __shfl_sync(FULL, ticket, 0);
-      r.e = -1;
-    }
-    return r;
-  };
-  Ent cur = next_entry(t);
-  int stage = 0;
-  if (cur.t < n_entries) stage_block<D, T, COST>(p, v, cur.e, wtile, wnodes, lane);
-  while (cur.t < n_entries) {
-    const int blk = cur.e;
-    if (lane == 0) ticket = atomicAdd(take, 1);
-    const Ent nxt = next_entry(__shfl_sync(FULL, ticket, 0));
-    if (warp_cls) {
-      int bc[3];
-      decode_block<D>(p.tg, blk, bc);
-      if (bc[0] != wcls) {
-        __syncwarp();
-        stage_class<D, T, RULE>(s, bc[0], p.nc, lane, p.oct_start, p.nzmask, p.weights, p.cost,
-                                p.ctrl);
-        wcls = bc[0];
-      }
-    }
-    cp_async_wait_all();
-    __syncwarp();
-    auto hook = [&]() {
-      if (nxt.t < n_entries)
-        stage_block<D, T, COST>(p, v, nxt.e, wtile + (stage ^ 1) * S::N, wnodes + (stage ^ 1),
-                                lane);
-    };
-    sweep_block<D, T, RULE, COST>(p, s, blk, wtile + stage * S::N, wnodes + stage, v, s_done,
-                                  s_max, gmax_row, evals, exec, xreal, s_pc, pm, tm, hook,
-                                  false, true);
-    ++blocks_done;
-    __syncwarp();
-    cur = nxt;
-    stage ^= 1;
-  }
-  flush_patch_max(p, pm, s_max, gmax_row);
   __shared__ unsigned long long s_ev, s_ex, s_xr;
   __shared__ int s_blk;
   if (threadIdx.x == 0) {
@@ -3503,30 +3356,12 @@ static int solve_impl(const phj_solve_args* a) {
     pb.band_only = 1;
     // block-local relaxations per visit in the pass (0: the schedule's)
     if (a->band_inner > 0) pb.inner = a->band_inner;
-    int rc = PHJ_OK;
-    if (a->band_entries > 0) {
-      // barrier-free pass over the rows' entries (PHJ_BAND_ASYNC)
-      int n_entries = a->band_entries;
-      int* take = p.ws.take;
-      void* bargs[] = {(void*)&pb, (void*)&n_entries, (void*)&take};
-      int blocks = 0;
-      auto launch = [&](auto kernel) -> int {
-        if (int r = persistent_blocks(kernel, smem, &blocks)) return r;
-        PHJ_CUDA(cudaLaunchKernel((void*)kernel, dim3(blocks), dim3(kThreads), bargs, smem,
-                                  stream));
-        phj_count_launch(1);
-        return PHJ_OK;
-      };
-      rc = (D == 3 && p.n_classes > 1) ? launch(band_async_kernel<D, T, RULE, COST, D == 3>)
-                                       : launch(band_async_kernel<D, T, RULE, COST, false>);
-    } else {
-      void* bargs[] = {(void*)&pb};
-      rc = (D == 3 && p.n_classes > 1)
-               ? coop_launch(solve_kernel<D, T, RULE, COST, D == 3>,
-                             (p.tg.total + kWarps - 1) / kWarps, smem, bargs, stream, nullptr)
-               : coop_launch(solve_kernel<D, T, RULE, COST, false>,
-                             (p.tg.total + kWarps - 1) / kWarps, smem, bargs, stream, nullptr);
-    }
+    void* bargs[] = {(void*)&pb};
+    int rc = (D == 3 && p.n_classes > 1)
+                 ? coop_launch(solve_kernel<D, T, RULE, COST, D == 3>,
+                               (p.tg.total + kWarps - 1) / kWarps, smem, bargs, stream, nullptr)
+                 : coop_launch(solve_kernel<D, T, RULE, COST, false>,
+                               (p.tg.total + kWarps - 1) / kWarps, smem, bargs, stream, nullptr);
     if (rc) return rc;
     PHJ_CUDA(cudaMemsetAsync(a->workspace, 0, ws_bytes, stream));
     p.n_band = 0;

@@ -73,12 +73,6 @@ SOLVE_BAND_WINDOW = tuple(int(x) for x in os.environ.get("PHJ_SOLVE_BAND_WINDOW"
 #: profiles/r2_band_ab.jsonl: 1 -> 2.7 s, 2 -> 341 ms, 3 -> 401 ms)
 SOLVE_BAND_INNER = int(os.environ.get("PHJ_BAND_INNER", "2"))
 BAND_CAP_PER_NODE = 1.5
-#: the solve's pass without grid barriers (rows claimed in order, in place).
-#: Off: without the barrier warps run ahead of the front, later rows are
-#: relaxed before their upstream values arrive and the cleanup does most of
-#: the work (C5 patch solve 341 -> 613 ms, C3 39 -> 219 ms,
-#: profiles/r2r_band_async_ab.jsonl)
-SOLVE_BAND_ASYNC = os.environ.get("PHJ_BAND_ASYNC", "0") != "0"
 #: band width in units of the smallest SL time step (coarser bands: fewer,
 #: thicker sweeps)
 BAND_SCALE = float(os.environ.get("PHJ_BAND_SCALE", "1"))
@@ -295,7 +289,6 @@ def band_schedule(plan: StencilPlan, key_work: torch.Tensor, nodes: torch.Tensor
     _lib.check(lib.phj_band_fill(ctypes_ref(plan.gs), max_bands, lo_w, hi_w, n_band, n_blocks,
                                  int(final_row), _lib.ptr(scratch), _lib.ptr(band_list),
                                  _lib.ptr(band_off), _lib.stream_handle()), "band_fill")
-    band_list.n_entries = entries  # rows 0 .. n_band - 1 (without the final row)
     return band_list, band_off, n_band
 
 
@@ -611,8 +604,7 @@ def solve_patches_internal(plan: StencilPlan, color: torch.Tensor, lab: torch.Te
             bands = band_schedule(plan, lifted_work, nodes, rule, SOLVE_BAND_WINDOW,
                                   final_row=True)
             if bands is not None:
-                bands = (*bands, SOLVE_BAND_INNER,
-                         bands[0].n_entries if SOLVE_BAND_ASYNC else 0)
+                bands = (*bands, SOLVE_BAND_INNER)
         res = device_solve(plan, work, lab, fmask, n_patches, rule=rule, dtype=dtype, tol=cfg.tol,
                            ao3=ao3, bands=bands,
                            max_sweeps=cfg.sweep_limit(plan.grid), mine=mine,

@@ -471,8 +471,6 @@ def device_solve(plan: StencilPlan, work: torch.Tensor, lab: torch.Tensor, fmask
         a.band_off = _lib.ptr(bands[1])
         a.n_band = n_band
         a.band_inner = int(bands[3]) if len(bands) > 3 else 0
-        # barrier-free pass (asynchronous schedule): rows 0 .. n_band - 1
-        a.band_entries = int(bands[4]) if (len(bands) > 4 and schedule == "async") else 0
     if ao3 is not None:
         fbx, amask, acount, words = ao3
         a.ao3_fb = _lib.ptr(fbx)

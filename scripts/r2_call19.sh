@@ -1,4 +1,6 @@
 #!/bin/bash
-timeout 900 python scripts/scaling_projection.py c5 float64 work > gpurun_out/r2s_scaling_work.json 2> gpurun_out/r2s_scaling.err; echo "work rc=$?"
-timeout 900 python scripts/scaling_projection.py c5 float64 nodes > gpurun_out/r2s_scaling_nodes.json 2>> gpurun_out/r2s_scaling.err; echo "nodes rc=$?"
-timeout 600 python bench.py > gpurun_out/r2s_bench.json 2> gpurun_out/r2s_bench.err; echo "bench rc=$?"
+mkdir -p gpurun_out
+timeout 600 python scripts/step_breakdown.py c5 float64 > gpurun_out/r2s_step_breakdown.jsonl 2> gpurun_out/r2s_step_breakdown.err; echo "breakdown rc=$?"
+cat gpurun_out/r2s_step_breakdown.jsonl
+timeout 600 python scripts/profile_step.py c5 float64 1 > gpurun_out/r2s_plain.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2s_c5f64_launches.csv python scripts/profile_step.py c5 float64 1 > gpurun_out/r2s_ncu_list.log 2>&1; echo "launches rc=$?"

@@ -1,5 +1,10 @@
 #!/bin/bash
-for c in c5 c3 c4; do timeout 600 python scripts/profile_step.py $c float64 3 2>&1 | tail -1 | python -c "
-import sys,json; d=json.loads(sys.stdin.read()); print(json.dumps({'config':d['config'],'transport_ms':d['transport_kernel']['kernel_ms'],'phases':d['phases_ms']}))" >> gpurun_out/r2t_tiled_transport.jsonl; done
-timeout 1200 python -m pytest tests/test_gpu_async.py tests/test_gpu_configs.py tests/test_gpu_parity.py -q -x > gpurun_out/r2t_tests.log 2>&1; echo "tests rc=$?"
-PHJ_CERT_LOG=gpurun_out/r2t_cert.jsonl timeout 1500 python -m pytest tests/test_gpu_fullsize.py -q -k "c3 or c4 or c5_fp64" > gpurun_out/r2t_cert.log 2>&1; echo "cert rc=$?"
+# A/B of the conical pre-pass (PHJ_BAND_CONE = r: controls within pi/r of the lifted feedback in the value-ordered pass)
+mkdir -p gpurun_out
+for r in 0 4 3 6 8; do
+  for c in c5 c3; do
+    PHJ_BAND_CONE=$r timeout 400 python scripts/band_ab.py $c >> gpurun_out/r2t_cone_ab.jsonl 2>> gpurun_out/r2t_cone_ab.err
+  done
+done
+cat gpurun_out/r2t_cone_ab.jsonl
+tail -5 gpurun_out/r2t_cone_ab.err
