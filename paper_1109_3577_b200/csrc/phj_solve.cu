@@ -1290,10 +1290,13 @@ struct MarkQueue {
     if (bits != 0ull && lane < (D == 2 ? 9 : 27)) {
       const int nt = neighbour_block<D>(tg, g, blk, lane);
       if (nt >= 0) {
-        const bool first = atomicOr(&masks[nt], bits) == 0ull;
         if (append) {
+          const bool first = atomicOr(&masks[nt], bits) == 0ull;
           a_nt = nt;
           a_old = !first;
+        } else {
+          // sticky masks: a reduction (no value returned, nothing to wait for)
+          atomicOr(&masks[nt], bits);
         }
       }
     }
@@ -2129,11 +2132,19 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
           }
         }
       } else if (__any_sync(FULL, any)) {
-        // the node itself is corner kself of its foot cell (feet lie in one of
-        // the 2^D cells around the node): its old value comes with the corners
-        int kself[NB];
+        // corner pairs along the last axis are adjacent elements: one offset
+        // per pair (NC / 2 per node), the partner is the next element.  Nodes
+        // without an entry read their own cell (values unused).
+        constexpr int NP = NC / 2;
+        constexpr int KL = 1 << last;  // corner bit of the last axis
+        // (lanes of a partial block at the far grid edge lie outside the
+        // array: they read a clamped in-plane location)
+        const int64_t fsafe = min(f0, p.plane - (NB + 1));
+        int64_t poff[NB][NP];
 #pragma unroll
-        for (int r = 0; r < NB; ++r) kself[r] = e[r] >= 0 ? (~s_oct[e[r]]) & (NC - 1) : 0;
+        for (int r = 0; r < NB; ++r)
+#pragma unroll
+          for (int m = 0; m < NP; ++m) poff[r][m] = e[r] >= 0 ? base[r] + coff[m] : fsafe + r;
         // colours in batches of CB: all corner loads of a batch are in flight
         // together (the sweep is latency-bound on these gathers)
 #ifndef PHJ_TCB2
@@ -2158,15 +2169,23 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
             anyj |= js[q] >= 0;
           }
           if (!anyj) break;
-          double cv[CB][NB][NC];
+          // an empty slot of the last batch re-reads slot 0's colour (unused)
+          PT cv[CB][NB][NC], ov[CB][NB];
 #pragma unroll
           for (int q = 0; q < CB; ++q) {
-            const PT* pj = pin + (int64_t)max(js[q], 0) * p.plane;
+            const PT* pj = pin + (int64_t)(js[q] >= 0 ? js[q] : js[0]) * p.plane;
 #pragma unroll
-            for (int r = 0; r < NB; ++r)
+            for (int r = 0; r < NB; ++r) {
 #pragma unroll
-              for (int k = 0; k < NC; ++k)
-                cv[q][r][k] = (js[q] >= 0 && e[r] >= 0) ? (double)pj[base[r] + coff[k]] : 0.0;
+              for (int m = 0; m < NP; ++m) {
+                const PT* pr = pj + poff[r][m];
+                cv[q][r][m] = pr[0];
+                cv[q][r][m + KL] = pr[1];
+              }
+              // the node's old value (it is also a corner of its foot cell:
+              // an L1 hit)
+              ov[q][r] = pj[fsafe + r];
+            }
           }
           double lmax[CB];
 #pragma unroll
@@ -2179,13 +2198,12 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
 #pragma unroll
             for (int r = 0; r < NB; ++r) {
               if (e[r] < 0) continue;
-              double acc = 0.0, old = cv[q][r][0];
+              double acc = 0.0;
+              const double old = (double)ov[q][r];
 #pragma unroll
-              for (int k = 0; k < NC; ++k) {
-                acc = fma(s_w[k * wpitch + e[r]], cv[q][r][k], acc);
-                if (k > 0 && k == kself[r]) old = cv[q][r][k];
-              }
-              const PT nv = (PT)(live ? acc : old);  // changes measured on the stored value
+              for (int k = 0; k < NC; ++k)
+                acc = fma(s_w[k * wpitch + e[r]], (double)cv[q][r][k], acc);
+              const PT nv = live ? (PT)acc : ov[q][r];  // changes measured on the stored value
               lmax[q] = fmax(lmax[q], fabs(old - (double)nv));
               qj[f0 + r] = nv;
               if (per0) {
@@ -2194,10 +2212,16 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
               }
             }
           }
+          // warp maximum on the bit patterns (values >= 0: the integer order
+          // of (high, low) words is the value order) -- two REDUX per colour
 #pragma unroll
-          for (int off = 16; off > 0; off >>= 1)
-#pragma unroll
-            for (int q = 0; q < CB; ++q) lmax[q] = fmax(lmax[q], __shfl_xor_sync(FULL, lmax[q], off));
+          for (int q = 0; q < CB; ++q) {
+            const int hi = __double2hiint(lmax[q]);
+            const int mh = __reduce_max_sync(FULL, hi);
+            const unsigned lo = hi == mh ? (unsigned)__double2loint(lmax[q]) : 0u;
+            const unsigned ml = __reduce_max_sync(FULL, lo);
+            lmax[q] = __hiloint2double(mh, (int)ml);
+          }
 #pragma unroll
           for (int q = 0; q < CB; ++q) {
             if (js[q] < 0 || !(lmax[q] > 0.0)) continue;
