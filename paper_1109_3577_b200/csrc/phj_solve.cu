@@ -2146,11 +2146,16 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
 #pragma unroll
           for (int m = 0; m < NP; ++m) poff[r][m] = e[r] >= 0 ? base[r] + coff[m] : fsafe + r;
         // colours in batches of CB: all corner loads of a batch are in flight
-        // together (the sweep is latency-bound on these gathers)
+        // together.  3D: one colour per batch -- a block holds 3.6 colours on
+        // average at config 5, so pairs waste a slot on odd counts (C5 151 ->
+        // 141 ms, profiles/r2y_transport_variants.jsonl)
 #ifndef PHJ_TCB2
 #define PHJ_TCB2 1
 #endif
-        constexpr int CB = (D == 2) ? PHJ_TCB2 : 2;
+#ifndef PHJ_TCB3
+#define PHJ_TCB3 1
+#endif
+        constexpr int CB = (D == 2) ? PHJ_TCB2 : PHJ_TCB3;
         const bool masked = R <= 64;
         unsigned long long todo = masked ? cm : 0ull;
         int jnext = 0;  // unmasked (R > 64): every colour in order

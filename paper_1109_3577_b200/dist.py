@@ -15,7 +15,7 @@ split by colour: colours are independent linear fixed points with their own
 stopping rule, so each rank transports a disjoint colour set and the
 per-node argmax is merged exactly with two all-reduces (MAX of the fp64
 value bits -- phi >= 0, so the bit order is the value order -- then MIN of
-the colour index among the ranks holding that maximum: the lowest colour
+the colour index, as uint8, among the ranks holding that maximum: the lowest colour
 wins ties, as in the single-device running argmax, src/patchy.py:251-256).
 """
 
@@ -104,8 +104,11 @@ def merge_argmax(best_val: torch.Tensor, best_idx: torch.Tensor, n_colors: int):
     bits = best_val.view(torch.int64)
     gbits = bits.clone()
     td.all_reduce(gbits, op=td.ReduceOp.MAX)
-    cand = torch.where(bits == gbits, best_idx.to(torch.int64),
-                       torch.full_like(bits, n_colors))
+    # the index reduction in the narrowest type NCCL reduces (uint8 up to 254
+    # colours: 1/8 of the bytes of the value reduction)
+    idt = torch.uint8 if n_colors < 255 else torch.int32
+    cand = torch.where(bits == gbits, best_idx.to(idt),
+                       torch.full(bits.shape, n_colors, dtype=idt, device=bits.device))
     td.all_reduce(cand, op=td.ReduceOp.MIN)
     best_val.copy_(gbits.view(torch.float64))
     best_idx.copy_(torch.clamp(cand, max=n_colors - 1).to(best_idx.dtype))

@@ -76,6 +76,8 @@ BAND_CAP_PER_NODE = 1.5
 #: band width in units of the smallest SL time step (coarser bands: fewer,
 #: thicker sweeps)
 BAND_SCALE = float(os.environ.get("PHJ_BAND_SCALE", "1"))
+#: the same for the transport's pass alone
+TRANSPORT_BAND_SCALE = float(os.environ.get("PHJ_TBAND_SCALE", str(BAND_SCALE)))
 #: fp32 workloads store the colour fields in fp32
 TRANSPORT_PHI_FP32 = True
 #: A/B knob: fp32 colour storage for fp64 workloads too (off: fp64 semantics)
@@ -250,7 +252,7 @@ def banded_applies(plan: StencilPlan) -> bool:
 
 
 def band_schedule(plan: StencilPlan, key_work: torch.Tensor, nodes: torch.Tensor, rule: str,
-                  window, final_row: bool = False):
+                  window, final_row: bool = False, scale: Optional[float] = None):
     """Block schedule of a value-ordered pass on the device (phj_band_count /
     phj_band_fill): CSR (band_list, band_off, n_band) of the warp blocks each
     sweep visits (phj_transport_args / phj_solve_args band fields).
@@ -268,7 +270,7 @@ def band_schedule(plan: StencilPlan, key_work: torch.Tensor, nodes: torch.Tensor
     dev = plan.device
     lib = _lib.load()
     fmax = plan.eps_speed / 1.0e-12
-    delta_min = BAND_SCALE * plan.grid.k_step / fmax
+    delta_min = (BAND_SCALE if scale is None else scale) * plan.grid.k_step / fmax
     max_bands = int(BAND_CAP_PER_NODE * max(plan.int_shape))
     nb = nodes.view(-1).to(torch.uint8).contiguous()
     scratch = torch.empty(int(lib.phj_band_scratch_bytes(ctypes_ref(plan.gs), max_bands, lo_w,
@@ -296,7 +298,8 @@ def transport_bands(plan: StencilPlan, key_work: torch.Tensor, fb_int: torch.Ten
                     window=None):
     """band_schedule over the transport's movers (feedback >= 0, free)."""
     mover = (fb_int.view(-1) >= 0) & (plan.kind.view(-1) == KIND_FREE)
-    return band_schedule(plan, key_work, mover, rule, window or TRANSPORT_BAND_WINDOW)
+    return band_schedule(plan, key_work, mover, rule, window or TRANSPORT_BAND_WINDOW,
+                         scale=TRANSPORT_BAND_SCALE)
 
 
 def transport_internal(plan: StencilPlan, fb_int: torch.Tensor, parts_flat: Sequence,

@@ -28,7 +28,23 @@ mask = patchy.plan_interior_serial(fplan, vf) >= 1.0
 color, _, _, lab = patchy.assemble_internal(fplan.gs, bv, bi, len(parts), mask, fplan.kind,
                                             fplan.grid.n_interior, fplan.device)
 out = {"config": name, "scale": patchy.BAND_SCALE, "window": patchy.SOLVE_BAND_WINDOW,
-       "inner": patchy.SOLVE_BAND_INNER, "twindow": patchy.TRANSPORT_BAND_WINDOW}
+       "inner": patchy.SOLVE_BAND_INNER, "twindow": patchy.TRANSPORT_BAND_WINDOW,
+       "tscale": patchy.TRANSPORT_BAND_SCALE, "lib": os.path.basename(os.environ.get("PHJ_LIB_PATH", "default"))}
+if os.environ.get("PHJ_AB_TRANSPORT_ONLY"):
+    real = dist.world
+    for G in (1, 8):
+        dist.world = lambda G=G: (0, G)
+        try:
+            for rep in range(2):
+                bv, bi, csw, _ = patchy._transport_and_argmax(fplan, fb, parts, pcfg.color_tol,
+                                                              10 * max(fplan.grid.shape), cfg.schedule,
+                                                              cfg.dtype, key_work=vf, rule=cfg.rule)
+        finally:
+            dist.world = real
+        out[f"G{G}_transport_ms"] = patchy.TRANSPORT_DIAG["kernel_ms"]
+        out[f"G{G}_tsweeps"] = [min(map(abs, csw)), max(map(abs, csw))]
+    print(json.dumps(out), flush=True)
+    sys.exit(0)
 real = dist.world
 for G in (1, 8):
     dist.world = lambda G=G: (0, G)
