@@ -2048,12 +2048,45 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
       for (int i = threadIdx.x; i < R; i += blockDim.x) z[i * kMaxPad] = 0ull;
     }
     __syncthreads();
+    // Lane -> node map of this kernel.  3D (8 x 8 plane blocks): node r of a
+    // lane is row (lane / 8) + 4 r, column lane % 8, so a warp-wide gather of
+    // one corner covers 4 rows of 8 consecutive elements (the shared Blk<3>
+    // map -- 2 consecutive nodes per lane -- makes it 8 rows of 4 elements
+    // 16 bytes apart: twice the L1 wavefronts, and the two nodes' requests
+    // hit the same sectors).  2D: the Blk<2> map.
+    constexpr bool kRowSplit = D == 3 && B::BY == 8 && B::BX == 8 && NB == 2;
+    auto locate = [&](int b, bool (&in)[NB], int64_t (&ff)[NB], int64_t (&ss)[NB], int& c0) {
+      if constexpr (kRowSplit) {
+        int bb[3];
+        decode_block<D>(p.tg, b, bb);
+        c0 = bb[0];
+#pragma unroll
+        for (int r = 0; r < NB; ++r) {
+          int cc[3] = {bb[0], bb[1] * 8 + (lane >> 3) + 4 * r, bb[2] * 8 + (lane & 7)};
+          in[r] = cc[1] < g.shape[1] && cc[2] < g.shape[2];
+          ff[r] = ext_flat<D>(g, cc);
+          ss[r] = serial_of<D>(g, cc);
+        }
+      } else {
+        int cc[3];
+        const bool rok = lane_nodes<D>(g, p.tg, b, lane, cc);
+        c0 = cc[0];
+        const int64_t f0 = ext_flat<D>(g, cc), s0 = serial_of<D>(g, cc);
+#pragma unroll
+        for (int r = 0; r < NB; ++r) {
+          in[r] = rok && cc[last] + r < g.shape[last];
+          ff[r] = f0 + r;
+          ss[r] = s0 + r;
+        }
+      }
+    };
     // prefetch of one item: its colour mask (lane 0) and mover entries
     auto prefetch = [&](int b, unsigned long long& pcm, int (&pe)[NB]) {
       b = b < 0 ? -b - 1 : b;  // banded copy entries
-      int cc[3];
-      const bool rok = lane_nodes<D>(g, p.tg, b, lane, cc);
-      const int64_t ss = serial_of<D>(g, cc);
+      bool in[NB];
+      int64_t ff[NB], ss[NB];
+      int c0;
+      locate(b, in, ff, ss, c0);
       pcm = 0ull;
       if (lane == 0) {
         pcm = __ldcg(&cur_mask[b]);
@@ -2061,10 +2094,7 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
         cur_flags[b] = 0;
       }
 #pragma unroll
-      for (int r = 0; r < NB; ++r) {
-        const bool in = rok && cc[last] + r < g.shape[last];
-        pe[r] = in ? __ldg(&p.ent[ss + r]) : -1;
-      }
+      for (int r = 0; r < NB; ++r) pe[r] = in[r] ? __ldg(&p.ent[ss[r]]) : -1;
     };
     int item = gwarp;
     int blk = item < cnt ? __ldcg(&list[item]) : 0;
@@ -2092,15 +2122,15 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
       const unsigned long long cm = __shfl_sync(FULL, cm_l0, 0);
       const bool copy_only = blk < 0;  // banded: last visit, copy to the other buffer
       const int bid = copy_only ? -blk - 1 : blk;
-      int c[3];
-      const bool row_ok = lane_nodes<D>(g, p.tg, bid, lane, c);
-      const int64_t f0 = ext_flat<D>(g, c);
+      bool in_grid[NB];
+      int64_t fr[NB], sr_unused[NB];  // ext flat index of the lane's nodes
+      int c0;                         // their index along internal axis 0
+      locate(bid, in_grid, fr, sr_unused, c0);
       int64_t base[NB];
       bool any = false;
-      (void)row_ok;
 #pragma unroll
       for (int r = 0; r < NB; ++r) {
-        base[r] = f0 + r;
+        base[r] = fr[r];
         if (e[r] >= 0) {
           const int oc = s_oct[e[r]];
 #pragma unroll
@@ -2123,11 +2153,11 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
 #pragma unroll
           for (int r = 0; r < NB; ++r) {
             if (e[r] < 0) continue;
-            const PT v = pj[f0 + r];
-            qj[f0 + r] = v;
+            const PT v = pj[fr[r]];
+            qj[fr[r]] = v;
             if (per0) {
-              if (c[0] == 0) qj[f0 + r + ghost_shift] = v;
-              else if (c[0] == M0 - 1) qj[f0 + r - ghost_shift] = v;
+              if (c0 == 0) qj[fr[r] + ghost_shift] = v;
+              else if (c0 == M0 - 1) qj[fr[r] - ghost_shift] = v;
             }
           }
         }
@@ -2139,12 +2169,14 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
         constexpr int KL = 1 << last;  // corner bit of the last axis
         // (lanes of a partial block at the far grid edge lie outside the
         // array: they read a clamped in-plane location)
-        const int64_t fsafe = min(f0, p.plane - (NB + 1));
+        int64_t fsafe[NB];
+#pragma unroll
+        for (int r = 0; r < NB; ++r) fsafe[r] = min(fr[r], p.plane - 2);
         int64_t poff[NB][NP];
 #pragma unroll
         for (int r = 0; r < NB; ++r)
 #pragma unroll
-          for (int m = 0; m < NP; ++m) poff[r][m] = e[r] >= 0 ? base[r] + coff[m] : fsafe + r;
+          for (int m = 0; m < NP; ++m) poff[r][m] = e[r] >= 0 ? base[r] + coff[m] : fsafe[r];
         // colours in batches of CB: all corner loads of a batch are in flight
         // together.  3D: one colour per batch -- a block holds 3.6 colours on
         // average at config 5, so pairs waste a slot on odd counts (C5 151 ->
@@ -2189,7 +2221,7 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
               }
               // the node's old value (it is also a corner of its foot cell:
               // an L1 hit)
-              ov[q][r] = pj[fsafe + r];
+              ov[q][r] = pj[fsafe[r]];
             }
           }
           double lmax[CB];
@@ -2210,10 +2242,10 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
                 acc = fma(s_w[k * wpitch + e[r]], (double)cv[q][r][k], acc);
               const PT nv = live ? (PT)acc : ov[q][r];  // changes measured on the stored value
               lmax[q] = fmax(lmax[q], fabs(old - (double)nv));
-              qj[f0 + r] = nv;
+              qj[fr[r]] = nv;
               if (per0) {
-                if (c[0] == 0) qj[f0 + r + ghost_shift] = nv;
-                else if (c[0] == M0 - 1) qj[f0 + r - ghost_shift] = nv;
+                if (c0 == 0) qj[fr[r] + ghost_shift] = nv;
+                else if (c0 == M0 - 1) qj[fr[r] - ghost_shift] = nv;
               }
             }
           }
