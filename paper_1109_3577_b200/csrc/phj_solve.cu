@@ -609,8 +609,25 @@ struct TileShape {
   static constexpr int RB = B::BY + 2;                    // rows per plane
   static constexpr int R = (D == 2) ? RB : 3 * RB;        // rows (x 3 planes in 3D)
   static constexpr int C = B::BX + 2 + ((B::BX + 2) % 2 == 0);  // columns (odd pitch: banks)
-  static constexpr int N = R * C;
+  // 3D solve tiles (8-wide blocks, 2 nodes per lane): rows alternate between
+  // pitch 11 and 13 (row r starts at 12 r - (r & 1)).  A half-warp's 16 lanes
+  // (4 consecutive rows x 4 lanes 2 elements apart) then read 16 distinct
+  // 8-byte banks for every row / column / plane shift of the octant loads;
+  // with the constant odd pitch 11 two of them collided and every LDS.64 of
+  // the cell loads took 4 wavefronts instead of 2 (ncu: 13.7 G excess
+  // wavefronts per config-5 pass, the shared-memory pipe at 76 % of peak).
+  static constexpr bool SWZ = D == 3 && B::BX == 8 && B::NB == 2 && RB % 2 == 0;
+  static constexpr int P = 12;  // mean pitch of the swizzled layout
+  __host__ __device__ static constexpr int row(int r) { return SWZ ? P * r - (r & 1) : r * C; }
+  static constexpr int N = SWZ ? R * P : R * C;
 };
+
+// +1 / -1 for lanes on odd / even block rows: the offset between a lane's
+// row and the next one is P + sg in the swizzled layout (two rows: 2 P).
+template <int D>
+__device__ __forceinline__ int lane_sg(int lane) {
+  return ((lane / Blk<D>::LX) & 1) ? 1 : -1;
+}
 
 // The lane's origin in the tile (its first node's 3^D neighbourhood starts
 // here) and the element of that node displaced by (d0, d1[, d2]).
@@ -618,13 +635,20 @@ template <int D, typename T>
 __device__ __forceinline__ const T* lane_tile(const T* tile, int lane) {
   using B = Blk<D>;
   using S = TileShape<D>;
-  return tile + (lane / B::LX) * S::C + (lane % B::LX) * B::NB;
+  return tile + S::row(lane / B::LX) + (lane % B::LX) * B::NB;
+}
+// offset from the lane origin to (plane dp, row dy) of its neighbourhood
+template <int D>
+__device__ __forceinline__ int tile_rel(int sg, int dp, int dy) {
+  using S = TileShape<D>;
+  if constexpr (S::SWZ) return S::P * (dp * S::RB + dy) + ((dy & 1) ? sg : 0);
+  else return (dp * S::RB + dy) * S::C;
 }
 template <int D, typename T>
-__device__ __forceinline__ T tile_at(const T* lt, int d0, int d1, int d2 = 0) {
+__device__ __forceinline__ T tile_at(const T* lt, int sg, int d0, int d1, int d2 = 0) {
   using S = TileShape<D>;
   if constexpr (D == 2) return lt[(1 + d0) * S::C + 1 + d1];
-  else return lt[((1 + d0) * S::RB + 1 + d1) * S::C + 1 + d2];
+  else return lt[tile_rel<D>(sg, 1 + d0, 1 + d1) + 1 + d2];
 }
 
 // The 2^D-corner cells of one octant (runtime O) for the lane's NB nodes;
@@ -639,7 +663,7 @@ struct OctNb {
     if constexpr (D == 2) return v[K & 1][r + ((K >> 1) & 1)];
     else return v[(K & 1) * 2 + ((K >> 1) & 1)][r + ((K >> 2) & 1)];
   }
-  __device__ __forceinline__ void load(const T* lt, int O) {
+  __device__ __forceinline__ void load(const T* lt, int O, int sg) {
     using S = TileShape<D>;
     const int b0 = O & 1, b1 = (O >> 1) & 1, b2 = (O >> 2) & 1;
     if constexpr (D == 2) {
@@ -649,13 +673,18 @@ struct OctNb {
 #pragma unroll
         for (int j = 0; j <= NB; ++j) v[k0][j] = t0[k0 * S::C + j];
     } else {
-      const T* t0 = lt + (b0 * S::RB + b1) * S::C + b2;
+      // rows b1 and b1 + 1 of planes b0 and b0 + 1 (two row bases: the row
+      // pitch depends on the row parity in the swizzled layout)
+      const T* ta = lt + tile_rel<D>(sg, b0, b1) + b2;
+      const T* tb = lt + tile_rel<D>(sg, b0, b1 + 1) + b2;
+      constexpr int PS = S::SWZ ? S::P * S::RB : S::RB * S::C;  // plane stride
 #pragma unroll
       for (int k0 = 0; k0 < 2; ++k0)
 #pragma unroll
-        for (int k1 = 0; k1 < 2; ++k1)
-#pragma unroll
-          for (int j = 0; j <= NB; ++j) v[k0 * 2 + k1][j] = t0[(k0 * S::RB + k1) * S::C + j];
+        for (int j = 0; j <= NB; ++j) {
+          v[k0 * 2][j] = ta[k0 * PS + j];
+          v[k0 * 2 + 1][j] = tb[k0 * PS + j];
+        }
     }
   }
 };
@@ -663,16 +692,16 @@ struct OctNb {
 // the octant of steepest descent at the lane's first node, majority over
 // the warp (warp-uniform)
 template <int D, typename T>
-__device__ __forceinline__ int preferred_octant(const T* lt) {
+__device__ __forceinline__ int preferred_octant(const T* lt, int sg) {
   const unsigned FULL = 0xffffffffu;
   bool down[D];
   if constexpr (D == 2) {
-    down[0] = tile_at<D>(lt, 1, 0) < tile_at<D>(lt, -1, 0);
-    down[1] = tile_at<D>(lt, 0, 1) < tile_at<D>(lt, 0, -1);
+    down[0] = tile_at<D>(lt, sg, 1, 0) < tile_at<D>(lt, sg, -1, 0);
+    down[1] = tile_at<D>(lt, sg, 0, 1) < tile_at<D>(lt, sg, 0, -1);
   } else {
-    down[0] = tile_at<D>(lt, 1, 0, 0) < tile_at<D>(lt, -1, 0, 0);
-    down[1] = tile_at<D>(lt, 0, 1, 0) < tile_at<D>(lt, 0, -1, 0);
-    down[2] = tile_at<D>(lt, 0, 0, 1) < tile_at<D>(lt, 0, 0, -1);
+    down[0] = tile_at<D>(lt, sg, 1, 0, 0) < tile_at<D>(lt, sg, -1, 0, 0);
+    down[1] = tile_at<D>(lt, sg, 0, 1, 0) < tile_at<D>(lt, sg, 0, -1, 0);
+    down[2] = tile_at<D>(lt, sg, 0, 0, 1) < tile_at<D>(lt, sg, 0, 0, -1);
   }
   int o = 0;
 #pragma unroll
@@ -700,6 +729,7 @@ __device__ __forceinline__ int eval_sweep(const T* lt, bool prune_on, const Sten
     // in registers, compile-time octants
     Nbhd<D, T, NB> nb;
     using S = TileShape<D>;
+    static_assert(!S::SWZ, "register-neighbourhood path assumes the constant tile pitch");
     if constexpr (D == 2) {
 #pragma unroll
       for (int dy = 0; dy < 3; ++dy)
@@ -722,9 +752,10 @@ __device__ __forceinline__ int eval_sweep(const T* lt, bool prune_on, const Sten
 #endif
   constexpr bool CAN_PRUNE = COST == PHJ_COST_NODE && PHJ_PRUNE;
   const bool prune = CAN_PRUNE && prune_on;
-  const int first = prune ? preferred_octant<D, T>(lt) : 0;
+  const int sg = lane_sg<D>(threadIdx.x & 31);
+  const int first = prune ? preferred_octant<D, T>(lt, sg) : 0;
   OctNb<D, T, NB> cell;
-  cell.load(lt, first);
+  cell.load(lt, first, sg);
   int n_ent = 0;
   n_real = 0;
   // warm: the running minima start at the previous block-local relaxation's
@@ -745,7 +776,7 @@ __device__ __forceinline__ int eval_sweep(const T* lt, bool prune_on, const Sten
 #else
     if (O == first) continue;
 #endif
-    cell.load(lt, O);
+    cell.load(lt, O, sg);
     if (prune && !__any_sync(0xffffffffu, octant_needed<D, T, NB>(cell, comp, mn))) continue;
     eval_octant<D, T, NB, RULE, COST, SLOW, 0, OctNb<D, T, NB>, AO3>(cell, O, s, os, fm, ncoef,
                                                                      nullptr, mn, best, bidx, al);
@@ -888,7 +919,7 @@ __device__ __forceinline__ void stage_block(const SolveParams& p, const T* __res
       rr = r - pl * S::RB;
     }
     const int c0 = sg * P::SW;
-    T* dst = tile + r * S::C + c0;
+    T* dst = tile + S::row(r) + c0;
     if (full) {
       const T* src = v + o + pl * s0x + (int64_t)rr * rs + c0;
 #pragma unroll
@@ -1025,6 +1056,7 @@ __device__ __forceinline__ int sweep_block(const SolveParams& p, const StencilSm
   const int lshift = (int)((f0 - lx * NB) & 1);  // label half-word offset of the row
   const bool stage_coef = COST == PHJ_COST_NODE && p.coef != nullptr;
   const T* lt = lane_tile<D>(tile, lane);
+  const int sg = lane_sg<D>(lane);
 
   int labv[NB];
   uint32_t fm[NB];
@@ -1106,7 +1138,7 @@ __device__ __forceinline__ int sweep_block(const SolveParams& p, const StencilSm
     T old[NB], cur[NB];
 #pragma unroll
     for (int r = 0; r < NB; ++r) {
-      old[r] = (D == 2) ? tile_at<D>(lt, 0, r) : tile_at<D>(lt, 0, 0, r);
+      old[r] = (D == 2) ? tile_at<D>(lt, sg, 0, r) : tile_at<D>(lt, sg, 0, 0, r);
       cur[r] = old[r];
     }
     bool hooked = false;
@@ -1173,7 +1205,7 @@ __device__ __forceinline__ int sweep_block(const SolveParams& p, const StencilSm
 #pragma unroll
       for (int r = 0; r < NB; ++r) {
         if (D == 2) ltw[S::C + 1 + r] = cur[r];
-        else ltw[(S::RB + 1) * S::C + 1 + r] = cur[r];
+        else ltw[tile_rel<D>(sg, 1, 1) + 1 + r] = cur[r];
       }
       __syncwarp();
     }
@@ -1203,7 +1235,7 @@ __device__ __forceinline__ int sweep_block(const SolveParams& p, const StencilSm
 #pragma unroll
       for (int r = 0; r < NB; ++r) {
         if (!copy[r]) continue;
-        const T old = (D == 2) ? tile_at<D>(lt, 0, r) : tile_at<D>(lt, 0, 0, r);
+        const T old = (D == 2) ? tile_at<D>(lt, sg, 0, r) : tile_at<D>(lt, sg, 0, 0, r);
         vout[f0 + r] = old;
         if (per0) {
           if (c[0] == 0) vout[f0 + r + ghost_shift] = old;
