@@ -233,6 +233,20 @@ int phj_feedback_allowed(const phj_grid* g, const phj_stencil* st, int32_t dtype
                          const int32_t* allow_count, int32_t allow_words, int32_t* out,
                          unsigned long long* evals, void* stream);
 
+/* phj_feedback_allowed on a slab of the grid: block rows [slab_begin,
+ * slab_end) along internal axis 0 (phj_block_dims[0] node layers each;
+ * slab_end < 0 = the whole grid).  Only the nodes of the slab are written
+ * to `out` and counted in `evals` (accumulated, not reset).  The ranks of a
+ * multi-GPU run split the feedback stage by slabs and all-gather `out`
+ * (paper_1109_3577_b200/dist.py; the reference's feedback loop over all
+ * serials, solver.py:413-443, has no such split). */
+int phj_feedback_slab(const phj_grid* g, const phj_stencil* st, int32_t dtype, int32_t rule,
+                      const void* v, const int8_t* kind, const uint32_t* fmask, const void* coef,
+                      double coef0, double unreach, const int32_t* allow_row,
+                      const unsigned long long* allow_mask, const int32_t* allow_count,
+                      int32_t allow_words, int32_t* out, unsigned long long* evals,
+                      int32_t slab_begin, int32_t slab_end, void* stream);
+
 /* Colour transport of all target parts at once, each to its own
  * max|change| <= tol (Jacobi, whole loop on device, one launch).  phi0/phi1
  * are colour-major [n_colors][ext nodes] doubles holding the start fields

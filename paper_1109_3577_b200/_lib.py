@@ -93,7 +93,7 @@ EXPORTS = (
     "phj_band_scratch_bytes", "phj_band_count", "phj_band_fill", "phj_solve",
     "phj_fmask_from_labels",
     "phj_fmask_from_hard",
-    "phj_feedback", "phj_feedback_allowed", "phj_transport", "phj_lift", "phj_argmax_update",
+    "phj_feedback", "phj_feedback_allowed", "phj_feedback_slab", "phj_transport", "phj_lift", "phj_argmax_update",
     "phj_argmax_colors", "phj_argmax_colors_t", "phj_count_labels",
     "phj_interpolate_points",
     "phj_assemble_codes",
@@ -134,6 +134,8 @@ def load() -> ctypes.CDLL:
         "phj_feedback": (ctypes.c_int, [P, P, I32, I32, P, P, P, P, D, D, P, P, P]),
         "phj_feedback_allowed": (ctypes.c_int, [P, P, I32, I32, P, P, P, P, D, D, P, P, P, I32,
                                                 P, P, P]),
+        "phj_feedback_slab": (ctypes.c_int, [P, P, I32, I32, P, P, P, P, D, D, P, P, P, I32,
+                                             P, P, I32, I32, P]),
         "phj_transport": (ctypes.c_int, [P]),
         "phj_lift": (ctypes.c_int, [P, P, I32, P, P, D, D, I32, P]),
         "phj_argmax_update": (ctypes.c_int, [P, P, I32, P, P, P]),

@@ -3142,6 +3142,9 @@ struct FeedbackParams {
   const unsigned long long* allow_mask;
   const int32_t* allow_count;
   int allow_words;
+  // blocks [blk_begin, blk_end): a slab of block rows along internal axis 0
+  // (ranks of a multi-GPU run split the stage by slabs)
+  int blk_begin, blk_end;
 };
 
 template <int D, typename T, int RULE, int COST>
@@ -3158,7 +3161,7 @@ __global__ void __launch_bounds__(kThreads) feedback_kernel(const __grid_constan
   const int lane = threadIdx.x & 31;
   unsigned long long ev = 0;
   const T* v = (const T*)p.v;
-  for (int blk = blockIdx.x * kWarps + (threadIdx.x >> 5); blk < p.tg.total;
+  for (int blk = p.blk_begin + blockIdx.x * kWarps + (threadIdx.x >> 5); blk < p.blk_end;
        blk += gridDim.x * kWarps) {
     int c[3];
     const bool row_ok = lane_nodes<D>(g, p.tg, blk, lane, c);
@@ -3725,10 +3728,18 @@ static int feedback_impl(const phj_grid* g, const phj_stencil* st, const void* v
                          double coef0, double unreach, const int32_t* allow_row,
                          const unsigned long long* allow_mask, const int32_t* allow_count,
                          int32_t allow_words, int32_t* out, unsigned long long* evals,
-                         cudaStream_t stream) {
+                         int32_t slab_begin, int32_t slab_end, cudaStream_t stream) {
   FeedbackParams p;
   p.g = *g;
   p.tg = make_tile_grid<D>(*g);
+  {
+    // slabs count block rows along internal axis 0 (slab_end < 0: all)
+    const int per_row = p.tg.total / p.tg.n[0];
+    const int r0 = slab_end < 0 ? 0 : std::max(0, std::min(slab_begin, p.tg.n[0]));
+    const int r1 = slab_end < 0 ? p.tg.n[0] : std::max(r0, std::min(slab_end, p.tg.n[0]));
+    p.blk_begin = r0 * per_row;
+    p.blk_end = r1 * per_row;
+  }
   p.n_classes = st->n_classes;
   p.nc = st->n_controls;
   p.n_real = st->n_real;
@@ -3753,20 +3764,22 @@ static int feedback_impl(const phj_grid* g, const phj_stencil* st, const void* v
                 (size_t)p.n_classes * p.nc * 4 + 16;
   auto k = feedback_kernel<D, T, RULE, COST>;
   PHJ_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int blocks = std::min((p.tg.total + kWarps - 1) / kWarps, 8 * phj_num_sms());
+  if (p.blk_end <= p.blk_begin) return PHJ_OK;
+  int blocks = std::min((p.blk_end - p.blk_begin + kWarps - 1) / kWarps, 8 * phj_num_sms());
   k<<<blocks, kThreads, smem, stream>>>(p);
   phj_count_launch(1);
   PHJ_CUDA(cudaGetLastError());
   return PHJ_OK;
 }
 
-extern "C" int phj_feedback_allowed(const phj_grid* g, const phj_stencil* st, int32_t dtype,
+extern "C" int phj_feedback_slab(const phj_grid* g, const phj_stencil* st, int32_t dtype,
                                     int32_t rule, const void* v, const int8_t* kind,
                                     const uint32_t* fmask, const void* coef, double coef0,
                                     double unreach, const int32_t* allow_row,
                                     const unsigned long long* allow_mask,
                                     const int32_t* allow_count, int32_t allow_words,
-                                    int32_t* out, unsigned long long* evals, void* stream) {
+                                    int32_t* out, unsigned long long* evals, int32_t slab_begin,
+                                    int32_t slab_end, void* stream) {
   if (!g || !st || !v || !kind || !fmask || !out) {
     phj_set_error("phj_feedback: missing argument");
     return PHJ_ERR_ARG;
@@ -3793,7 +3806,7 @@ extern "C" int phj_feedback_allowed(const phj_grid* g, const phj_stencil* st, in
       cc == (CC == PHJ_COST_CTRL))                                                         \
     return feedback_impl<DD, TT, RR, CC>(g, st, v, kind, fmask, coef, coef0, unreach,      \
                                          allow_row, allow_mask, allow_count, allow_words, out, \
-                                         evals, s);
+                                         evals, slab_begin, slab_end, s);
   PHJ_FB(2, double, PHJ_RULE_REF, PHJ_COST_NODE)
   PHJ_FB(2, double, PHJ_RULE_REF, PHJ_COST_CTRL)
   PHJ_FB(2, double, PHJ_RULE_KRUZKOV, PHJ_COST_NODE)
@@ -3809,6 +3822,17 @@ extern "C" int phj_feedback_allowed(const phj_grid* g, const phj_stencil* st, in
 #undef PHJ_FB
   phj_set_error("phj_feedback: unsupported combination");
   return PHJ_ERR_UNSUPPORTED;
+}
+
+extern "C" int phj_feedback_allowed(const phj_grid* g, const phj_stencil* st, int32_t dtype,
+                                    int32_t rule, const void* v, const int8_t* kind,
+                                    const uint32_t* fmask, const void* coef, double coef0,
+                                    double unreach, const int32_t* allow_row,
+                                    const unsigned long long* allow_mask,
+                                    const int32_t* allow_count, int32_t allow_words,
+                                    int32_t* out, unsigned long long* evals, void* stream) {
+  return phj_feedback_slab(g, st, dtype, rule, v, kind, fmask, coef, coef0, unreach, allow_row,
+                           allow_mask, allow_count, allow_words, out, evals, 0, -1, stream);
 }
 
 extern "C" int phj_feedback(const phj_grid* g, const phj_stencil* st, int32_t dtype, int32_t rule,

@@ -115,6 +115,33 @@ def merge_argmax(best_val: torch.Tensor, best_idx: torch.Tensor, n_colors: int):
     return best_val, best_idx
 
 
+def slab_bounds(n_rows: int, n_ranks: int) -> list:
+    """Block-row range [begin, end) per rank: equal slabs (the last ones may
+    be short or empty), so one all-gather of equal chunks assembles the field."""
+    per = (n_rows + n_ranks - 1) // n_ranks
+    return [(min(r * per, n_rows), min((r + 1) * per, n_rows)) for r in range(n_ranks)]
+
+
+def gather_slabs(compute, n_rows: int, row_elems: int, n_total: int, dtype, device):
+    """A per-serial field computed by slabs: rank r calls
+    ``compute(begin, end, chunk)`` for its block rows (``chunk`` = the
+    contiguous serials of that slab) and the chunks are all-gathered.
+    Returns the first ``n_total`` elements of the assembled field."""
+    import torch.distributed as td
+
+    rank, n_ranks = world()
+    bounds = slab_bounds(n_rows, n_ranks)
+    per = (n_rows + n_ranks - 1) // n_ranks
+    full = torch.empty(n_ranks * per * row_elems, dtype=dtype, device=device)
+    b, e = bounds[rank]
+    mine = full[rank * per * row_elems:(rank + 1) * per * row_elems]
+    if e > b:
+        compute(b, e, mine)
+    if n_ranks > 1:
+        td.all_gather_into_tensor(full, mine.clone())
+    return full[:n_total]
+
+
 def sum_over_ranks(t: torch.Tensor) -> torch.Tensor:
     import torch.distributed as td
 

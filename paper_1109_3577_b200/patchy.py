@@ -32,7 +32,7 @@ from .problems import (ProblemSpec, TargetSpec, _check_parts, device_partition_c
 from .runtime import ExecutionStrategy, RunStats
 from .solver import (_rule_id, DIRICHLET, KIND_FREE, KIND_OBSTACLE, KIND_TARGET, STATE_CONSTRAINT,
                      FeedbackField, SolverConfig, StencilPlan, SweepStats, ctypes_ref,
-                     device_solve, feedback_internal, stats_for_patch, unreach_threshold,
+                     device_solve, feedback_internal, feedback_sharded, stats_for_patch, unreach_threshold,
                      unreached_value, _dtype_id)
 
 UNREACHABLE = -1
@@ -838,7 +838,7 @@ def run_patchy(spec: ProblemSpec, pcfg: PatchyConfig, cfg: Optional[SolverConfig
             stats.warnings.append(cst.warning)
     with stats.phase("lift"):
         vf = lift_internal(cplan, vc, fplan, rule, dtype)
-        fb, ev = feedback_internal(fplan, vf, rule=rule, dtype=dtype)
+        fb, ev = feedback_sharded(fplan, vf, rule=rule, dtype=dtype)
     transport_sweeps = []
     with stats.phase("transport"):
         ut = pcfg.unreachable_threshold

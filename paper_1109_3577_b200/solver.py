@@ -819,20 +819,66 @@ def extract_feedback(field: NodeField, spec: ProblemSpec, table: Optional[Stenci
 
 
 def feedback_internal(plan: StencilPlan, work: torch.Tensor, *, rule: str, dtype: str,
-                      allowed=None):
+                      allowed=None, slab=None, out=None, ev=None):
+    """Optimal control per internal serial (solver.py:413-443).  ``slab`` =
+    (begin, end) restricts the launch to those block rows along internal axis
+    0 (phj_feedback_slab; the other entries of ``out`` are left untouched)."""
     lib = _lib.load()
-    out = torch.empty(plan.grid.n_interior, dtype=torch.int32, device=plan.device)
-    ev = torch.zeros(1, dtype=torch.int64, device=plan.device)
+    if out is None:
+        out = torch.empty(plan.grid.n_interior, dtype=torch.int32, device=plan.device)
+    if ev is None:
+        ev = torch.zeros(1, dtype=torch.int64, device=plan.device)
     coef, coef0 = plan.coef(rule, dtype)
     st = plan.stencil_struct()
     rows, mask, count, words = allowed if allowed is not None else (None, None, None, 0)
-    _lib.check(lib.phj_feedback_allowed(ctypes_ref(plan.gs), ctypes_ref(st), _dtype_id(dtype),
-                                        _rule_id(rule), _lib.ptr(work), _lib.ptr(plan.kind),
-                                        _lib.ptr(plan.fmask_hard), _lib.ptr(coef), coef0,
-                                        unreach_threshold(rule), _lib.ptr(rows), _lib.ptr(mask),
-                                        _lib.ptr(count), int(words), _lib.ptr(out),
-                                        _lib.ptr(ev), _lib.stream_handle()), "phj_feedback")
+    s0, s1 = (0, -1) if slab is None else (int(slab[0]), int(slab[1]))
+    _lib.check(lib.phj_feedback_slab(ctypes_ref(plan.gs), ctypes_ref(st), _dtype_id(dtype),
+                                     _rule_id(rule), _lib.ptr(work), _lib.ptr(plan.kind),
+                                     _lib.ptr(plan.fmask_hard), _lib.ptr(coef), coef0,
+                                     unreach_threshold(rule), _lib.ptr(rows), _lib.ptr(mask),
+                                     _lib.ptr(count), int(words), _lib.ptr(out),
+                                     _lib.ptr(ev), s0, s1, _lib.stream_handle()), "phj_feedback")
     return out, ev
+
+
+def feedback_sharded(plan: StencilPlan, work: torch.Tensor, *, rule: str, dtype: str):
+    """feedback_internal split over the ranks by slabs of block rows along
+    internal axis 0 and all-gathered (dist.gather_slabs); one rank: the plain
+    launch.  Every rank needs the whole field: the colour transport is split
+    by colour, not by space."""
+    from . import dist
+
+    rank, world = dist.world()
+    if world <= 1:
+        return feedback_internal(plan, work, rule=rule, dtype=dtype)
+    dims = (ctypes.c_int32 * 3)()
+    _lib.load().phj_block_dims(plan.grid.dim, dims)
+    layers = int(dims[0])                       # node layers of axis 0 per block row
+    n0 = int(plan.int_shape[0])
+    row_elems = int(np.prod(plan.int_shape[1:]))
+    ev = torch.zeros(1, dtype=torch.int64, device=plan.device)
+
+    def compute(r0, r1, chunk):
+        # chunk: the contiguous serials of block rows [r0, r1)
+        base = r0 * layers * row_elems
+        feedback_internal(plan, work, rule=rule, dtype=dtype, slab=(r0, r1),
+                          out=_OffsetView(chunk, base), ev=ev)
+
+    out = dist.gather_slabs(compute, (n0 + layers - 1) // layers, layers * row_elems,
+                            plan.grid.n_interior, torch.int32, plan.device)
+    dist.sum_over_ranks(ev)
+    return out, ev
+
+
+class _OffsetView:
+    """A tensor chunk addressed as if it started ``base`` elements earlier
+    (the kernel writes out[serial]; the chunk holds serials base ...)."""
+
+    def __init__(self, chunk: torch.Tensor, base: int):
+        self.chunk, self.base = chunk, base
+
+    def data_ptr(self) -> int:
+        return self.chunk.data_ptr() - self.base * self.chunk.element_size()
 
 
 def reduce_controls(control_set, a_star: np.ndarray, r: float) -> np.ndarray:

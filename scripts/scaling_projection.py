@@ -5,12 +5,13 @@ these ranks never wait: patches and colours are independent).
 For G in (1, 2, 4, 8) and each rank r, the rank's own work is run alone on
 the full GPU exactly as that rank would run it (dist.world() patched to
 (r, G)): its colour subset of the transport (dist.my_colours) and its patch
-subset of the patch solve (dist.mine_mask, LPT).  Replicated stages (coarse,
-lift, feedback, assembly) are timed once.  Collectives are estimated from
-their byte counts at an NVLink-5 all-reduce bus bandwidth (argmax merge:
-2 x N x 8 B, value gather: N x 8 B MIN).  Projected step time of G GPUs =
-replicated + max_r (transport_r) + merge + max_r (patch_r) + gather;
-efficiency = T(1) / (G * T(G)).
+subset of the patch solve (dist.mine_mask, LPT), its slab of the feedback
+stage (phj_feedback_slab).  Replicated stages (coarse, lift, assembly) are
+timed once.  Collectives are estimated from their byte counts at an NVLink-5
+bus bandwidth (feedback all-gather: N x 4 B; argmax merge: N x 8 B MAX +
+N x 1 B MIN; value gather: N x 8 B MIN).  Projected step time of G GPUs =
+replicated + max_r (feedback_r) + all-gather + max_r (transport_r) + merge +
+max_r (patch_r) + gather; efficiency = T(1) / (G * T(G)).
 
     python scripts/scaling_projection.py [c5] [float64] [weights]
 weights: "work" (default: the per-patch executed evaluations of a previous
@@ -28,7 +29,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-from paper_1109_3577_b200 import configs, dist, patchy  # noqa: E402
+from paper_1109_3577_b200 import _lib, configs, dist, patchy  # noqa: E402
 from paper_1109_3577_b200.solver import feedback_internal, unreach_threshold  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c5"
@@ -100,19 +101,36 @@ for G in (1, 2, 4, 8):
                 execd_all = execd.copy()
         finally:
             dist.world = real_world
-    rep = sum(res["replicated_ms"].values())
+    # the feedback stage is split by slabs of block rows (solver.feedback_sharded):
+    # the slowest rank's slab + an all-gather of the int32 field
+    fb_ms = [t_fb]
+    if G > 1:
+        import ctypes as _ct
+        dims = (_ct.c_int32 * 3)()
+        _lib.load().phj_block_dims(fplan.grid.dim, dims)
+        n_rows = (fplan.int_shape[0] + int(dims[0]) - 1) // int(dims[0])
+        fb_ms = []
+        for b0, b1 in dist.slab_bounds(n_rows, G):
+            _, t = timed(lambda: feedback_internal(fplan, vf, rule=cfg.rule, dtype=cfg.dtype,
+                                                   slab=(b0, b1)))
+            fb_ms.append(t)
+    rep = sum(v for k, v in res["replicated_ms"].items() if k != "feedback")
     nbytes = n * 8
     allreduce_ms = lambda b: 0.0 if G == 1 else 2.0 * (G - 1) / G * b / (BUS_GBS * 1e9) * 1e3
-    merge = 2 * allreduce_ms(nbytes)
+    allgather_ms = lambda b: 0.0 if G == 1 else (G - 1) / G * b / (BUS_GBS * 1e9) * 1e3
+    fb_stage = max(fb_ms) + allgather_ms(n * 4)
+    # argmax merge: MAX of the fp64 bits + MIN of the uint8 colour index
+    merge = allreduce_ms(nbytes) + allreduce_ms(n)
     gather = allreduce_ms(nbytes)
-    step = rep + max(tr_ms) + merge + max(pa_ms) + gather
+    step = rep + fb_stage + max(tr_ms) + merge + max(pa_ms) + gather
     if G == 1:
         base = step
         owner = np.zeros(R, dtype=int)
     else:
         owner = dist.lpt_assign(sizes, G, execd_all if WEIGHTS == "work" else None)
     work_bins = np.bincount(owner, weights=execd, minlength=G)
-    res[f"G{G}"] = {"step_ms": step, "transport_ms_per_rank": tr_ms,
+    res[f"G{G}"] = {"step_ms": step, "feedback_ms_per_rank": fb_ms, "feedback_stage_ms": fb_stage,
+                    "transport_ms_per_rank": tr_ms,
                     "patch_ms_per_rank": pa_ms, "merge_ms_est": merge, "gather_ms_est": gather,
                     "efficiency": base / (G * step),
                     "patch_work_balance": float(execd.sum() / (G * work_bins.max())),

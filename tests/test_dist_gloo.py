@@ -138,3 +138,47 @@ def test_lpt_weights_change_the_assignment():
     m0 = dist.mine_mask(sizes, 0, 2, "cpu", work).numpy()
     m1 = dist.mine_mask(sizes, 1, 2, "cpu", work).numpy()
     assert np.array_equal(m0 + m1, np.ones(4, dtype=np.uint8))
+
+
+def _slab_worker(rank, world, port, n_rows, row_elems, n_total, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    td.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        calls = []
+
+        def compute(b, e, chunk):
+            # the slab's serials hold their own global index
+            calls.append((b, e))
+            n = (e - b) * row_elems
+            chunk[:n] = torch.arange(b * row_elems, e * row_elems, dtype=torch.int32)
+
+        out = dist.gather_slabs(compute, n_rows, row_elems, n_total, torch.int32, "cpu")
+        q.put((rank, calls, out.numpy().tolist()))
+    finally:
+        td.destroy_process_group()
+
+
+def test_slab_split_and_all_gather_world2():
+    """The feedback stage split by slabs of block rows (dist.gather_slabs,
+    solver.feedback_sharded): disjoint slabs covering every row, the
+    all-gathered field complete on both ranks -- also when the rows do not
+    divide evenly and the last block row is partial."""
+    n_rows, row_elems, n_total = 7, 5, 33  # 7 block rows of 5 serials, the last one partial
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_slab_worker, args=(r, 2, port, n_rows, row_elems, n_total, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    out.sort()
+    assert out[0][1] == [(0, 4)] and out[1][1] == [(4, 7)]
+    for _, _, field in out:
+        assert field == list(range(n_total))
+    assert dist.slab_bounds(5, 8) == [(0, 1), (1, 2), (2, 3), (3, 4), (4, 5), (5, 5), (5, 5),
+                                      (5, 5)]

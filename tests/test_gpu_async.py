@@ -46,3 +46,30 @@ def test_async_transport_matches_jacobi(name, kw, inner, monkeypatch):
           f"{csj[:4]} async {csa[:4]}")
     assert all(c > 0 for c in csj) and all(c > 0 for c in csa)
     assert err <= 1e-9
+
+
+@pytest.mark.parametrize("name,kw", CASES)
+def test_feedback_by_slabs_equals_the_full_launch(name, kw):
+    """phj_feedback_slab (the multi-GPU split of the feedback stage,
+    solver.feedback_sharded): uneven slabs of block rows fill exactly the
+    entries of the full launch, and the evaluation counts add up."""
+    import ctypes
+
+    from paper_1109_3577_b200 import _lib, solver
+
+    w = configs.CONFIGS[name](**kw)
+    fplan, cplan = patchy.make_plans(w.spec, w.pcfg)
+    vc, _ = patchy.solve_full_internal(cplan, patchy.coarse_cfg(w.cfg))
+    vf = patchy.lift_internal(cplan, vc, fplan, w.cfg.rule, w.cfg.dtype)
+    full, ev_full = solver.feedback_internal(fplan, vf, rule=w.cfg.rule, dtype=w.cfg.dtype)
+    dims = (ctypes.c_int32 * 3)()
+    _lib.load().phj_block_dims(fplan.grid.dim, dims)
+    n_rows = (fplan.int_shape[0] + int(dims[0]) - 1) // int(dims[0])
+    out = torch.full_like(full, -7)
+    ev = torch.zeros(1, dtype=torch.int64, device=full.device)
+    cuts = [0, n_rows // 3, n_rows // 3, n_rows - 1, n_rows]  # one empty slab
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        solver.feedback_internal(fplan, vf, rule=w.cfg.rule, dtype=w.cfg.dtype, slab=(a, b),
+                                 out=out, ev=ev)
+    assert torch.equal(out, full)
+    assert int(ev.item()) == int(ev_full.item())
