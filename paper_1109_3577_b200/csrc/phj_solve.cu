@@ -1486,6 +1486,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) solve_kernel(const __gri
                                                     vout, s_done, s_max, gmax_row, evals, exec,
                                                     xreal, s_pc, pm, tm, hook, copy_visit);
       ++blocks_done;
+#ifdef PHJ_TIMING
+      if (lane == 0 && banded) atomicAdd(&g_visit_kind[copy_visit ? 3 : ch], 1ull);
+#endif
       // the band schedule, not the activity, drives the pass
       mq.issue(p.tg, p.g, bid, banded ? 0 : ch, lane, nxt_flags);
       tm.mark(6);

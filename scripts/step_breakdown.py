@@ -48,6 +48,11 @@ for fn in ("device_solve", "feedback_internal"):
     if hasattr(patchy, fn):
         wrap(patchy, fn)
 plans = patchy.make_plans(w.spec, w.pcfg)
+fake = os.environ.get("PHJ_FAKE_WORLD")  # "rank,world": this rank's share, no collectives
+if fake:
+    from paper_1109_3577_b200 import dist
+    fr, fw = (int(x) for x in fake.split(","))
+    dist.world = lambda: (fr, fw)
 for step in range(3):
     acc.clear()
     torch.cuda.synchronize()
@@ -55,7 +60,7 @@ for step in range(3):
     patchy.run_patchy(w.spec, w.pcfg, w.cfg, plans=plans, outputs=False)
     torch.cuda.synchronize()
     total = 1000 * (time.perf_counter() - t0)
-    out = {"config": name, "dtype": dtype, "step": step, "total_ms": round(total, 2),
+    out = {"config": name, "dtype": dtype, "step": step, "fake_world": fake, "total_ms": round(total, 2),
            "transport_kernel_ms": round(patchy.TRANSPORT_DIAG.get("kernel_ms", 0.0), 2),
            "split_ms": {k: round(v, 2) for k, v in acc.items()}}
     print(json.dumps(out), flush=True)
