@@ -132,13 +132,15 @@ def gather_slabs(compute, n_rows: int, row_elems: int, n_total: int, dtype, devi
     rank, n_ranks = world()
     bounds = slab_bounds(n_rows, n_ranks)
     per = (n_rows + n_ranks - 1) // n_ranks
-    full = torch.empty(n_ranks * per * row_elems, dtype=dtype, device=device)
+    full = torch.full((n_ranks * per * row_elems,), -1, dtype=dtype, device=device)
     b, e = bounds[rank]
     mine = full[rank * per * row_elems:(rank + 1) * per * row_elems]
     if e > b:
         compute(b, e, mine)
-    if n_ranks > 1:
+    if n_ranks > 1 and td.is_available() and td.is_initialized():
         td.all_gather_into_tensor(full, mine.clone())
+    # (a patched world() without a process group -- the one-GPU projection of
+    # a rank's share -- leaves the other ranks' slabs unfilled)
     return full[:n_total]
 
 

@@ -18,6 +18,7 @@ Two switches the reference lacks (``SolverConfig``):
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass, field as _field
 from typing import Optional
 

@@ -60,6 +60,12 @@ for G in (1, 8):
     dist.world = lambda G=G: (0, G)
     try:
         for rep in range(2):
+            # node-count LPT on every repetition: a solve stores the work it
+            # measured on the plan, and without a process group that is this
+            # rank's patches only (weights of the others 0 -> a different,
+            # lighter assignment: the G8 figures of earlier A/B files taken
+            # with this script are too low for that reason)
+            fplan._patch_work = None
             _, pst, _, pinfo = patchy.solve_patches_internal(fplan, color, lab, len(parts), pcfg,
                                                              cfg, vf)
     finally:

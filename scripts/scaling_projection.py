@@ -43,14 +43,22 @@ dev = fplan.device
 n = fplan.grid.n_interior
 
 
+REPS = int(os.environ.get("PHJ_PROJ_REPS", "2"))
+
+
 def timed(fn):
-    a = torch.cuda.Event(enable_timing=True)
-    b = torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    a.record()
-    out = fn()
-    b.record()
-    torch.cuda.synchronize()
+    """Device time of fn(): the last of REPS calls -- a rank repeats the same
+    shapes every step, so its steady state has the allocator pools and the
+    band-list sizes of its own share warm (a single cold call of a rank's
+    share measured ~23 ms more at G = 8)."""
+    for _ in range(REPS):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record()
+        out = fn()
+        b.record()
+        torch.cuda.synchronize()
     return out, a.elapsed_time(b)
 
 
@@ -86,14 +94,18 @@ for G in (1, 2, 4, 8):
                     fplan.gs, bv, bi, R, mask, fplan.kind, n, dev))
                 res["replicated_ms"]["assembly"] = t_as
                 sizes = patchy.count_labels(color, R).cpu().numpy()
-            if G > 1 and WEIGHTS == "work":
-                # the per-patch work every rank would hold after a first solve
-                # of this patch map (measured at G = 1, all patches)
-                fplan._patch_work = ((tuple(int(x) for x in sizes), G), execd_all)
-            else:
-                fplan._patch_work = None
-            (out, pst, warns, pinfo), t_pa = timed(lambda: patchy.solve_patches_internal(
-                fplan, color, lab, R, pcfg, cfg, vf))
+            def patch_share():
+                # LPT weights: the per-patch work every rank would hold after a
+                # first solve of this patch map (measured at G = 1, all
+                # patches), or node counts; reset before every repetition (a
+                # solve stores its own measured work on the plan)
+                if G > 1 and WEIGHTS == "work":
+                    fplan._patch_work = ((tuple(int(x) for x in sizes), G), execd_all)
+                else:
+                    fplan._patch_work = None
+                return patchy.solve_patches_internal(fplan, color, lab, R, pcfg, cfg, vf)
+
+            (out, pst, warns, pinfo), t_pa = timed(patch_share)
             pa_ms.append(t_pa)
             if G == 1:
                 relax = np.array([s.node_relaxations for s in pst], dtype=float)

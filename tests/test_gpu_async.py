@@ -73,3 +73,29 @@ def test_feedback_by_slabs_equals_the_full_launch(name, kw):
                                  out=out, ev=ev)
     assert torch.equal(out, full)
     assert int(ev.item()) == int(ev_full.item())
+
+
+def test_sharded_feedback_of_two_ranks_assembles_the_full_field(monkeypatch):
+    """solver.feedback_sharded as ranks 0 and 1 of 2 (world patched, no
+    process group: each call fills its own slab only): the two slabs are
+    disjoint, cover every node and equal the single-rank feedback."""
+    from paper_1109_3577_b200 import dist, solver
+
+    w = configs.CONFIGS["c5"](n=65, dtype="float64")
+    fplan, cplan = patchy.make_plans(w.spec, w.pcfg)
+    vc, _ = patchy.solve_full_internal(cplan, patchy.coarse_cfg(w.cfg))
+    vf = patchy.lift_internal(cplan, vc, fplan, w.cfg.rule, w.cfg.dtype)
+    full, ev_full = solver.feedback_internal(fplan, vf, rule=w.cfg.rule, dtype=w.cfg.dtype)
+    parts, evs = [], 0
+    for r in range(2):
+        monkeypatch.setattr(dist, "world", lambda r=r: (r, 2))
+        out, ev = solver.feedback_sharded(fplan, vf, rule=w.cfg.rule, dtype=w.cfg.dtype)
+        parts.append(out.clone())
+        evs += int(ev.item())
+    # kind-free nodes without any admissible control also hold -1: compare by slab
+    n0 = fplan.int_shape[0]
+    row = full.numel() // n0
+    cut = ((n0 + 1) // 2) * row
+    assert torch.equal(parts[0][:cut], full[:cut]) and torch.equal(parts[1][cut:], full[cut:])
+    assert bool((parts[0][cut:] == -1).all()) and bool((parts[1][:cut] == -1).all())
+    assert evs == int(ev_full.item())
