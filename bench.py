@@ -457,9 +457,13 @@ def run_ours(args):
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps,
                 "ms_per_step": 1000.0 * e_dt / e2e_steps},
         "roofline": {"bound": "fp64" if args.dtype == "float64" else "fp32",
-                     "kernel": ("solve_async_kernel (fine patch solve, one persistent launch)"
+                     "kernel": ("fine patch solve: value-ordered pass (solve_kernel) + asynchronous "
+                                "relaxation (solve_async_kernel), one phj_solve call"
                                 if cfg.schedule == "async" else
                                 "solve_kernel (fine patch solve, one cooperative launch)"),
+                     "limiter": "shared-memory (LSU) wavefronts + latency, not the FP64 pipe: ncu of "
+                                "the C5 fp64 pass: LSU data pipe 65 % of peak, FP64 pipe 38 %, DRAM "
+                                "0.44 TB/s (profiles/r2ae_c5f64_solve_banded_ncu.txt, DESIGN.md §5)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak if peak else None, "traffic": traffic,
                      "flops_per_candidate": fl,
