@@ -19,6 +19,7 @@ from .dynamics import Dubins, ScaledSpeed, SinProduct
 from .patchy import PatchyConfig
 from .problems import (ControlSet, ProblemSpec, TargetSpec, discretize_circle, fibonacci_sphere,
                        partition_balls_halves, partition_octants, partition_random_directions,
+                       RandomDirections,
                        partition_target, target_nodes)
 from .solver import SolverConfig
 
@@ -136,8 +137,7 @@ def c5(rule: str = "kruzkov", dtype: str = "float32", schedule: str = "async", n
                        dynamics=ScaledSpeed(speed).dynamics(), control_set=fibonacci_sphere(96),
                        target=TargetSpec.ball((0.0, 0.0, 0.0), 0.15), model=ScaledSpeed(speed))
     pcfg = PatchyConfig(n_patches=32, coarse_nodes=nc_, fine_nodes=n,
-                        parts=lambda t, g, serials=None: partition_random_directions(
-                            t, g, 32, seed, serials=serials))
+                        parts=RandomDirections(32, seed))
     return Workload("c5", f"3D variable speed {n}^3, 96 controls, 32 patches", spec, pcfg,
                     SolverConfig(schedule=schedule, tol=1e-8 if dtype == "float64" else 1e-6, rule=rule,
                                  dtype=dtype), (n,) * 3, (nc_,) * 3)

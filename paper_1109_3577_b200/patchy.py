@@ -914,8 +914,13 @@ def _resolve_parts(pcfg: PatchyConfig, spec: ProblemSpec, grid: Grid, plan=None)
         if dev is not None:
             # built-in partitions on the device: one copy of (serials, codes)
             n_parts, code = dev
-            both = torch.stack([ser_t.to(torch.int64), code]).cpu().numpy()
-            parts = [both[0][both[1] == j] for j in range(n_parts)]
+            # grouped on the device (stable sort by part keeps the serial
+            # order inside a part), one copy of (serials, part sizes)
+            _, perm = torch.sort(code, stable=True)
+            packed = torch.cat([ser_t.to(torch.int64)[perm],
+                                torch.bincount(code, minlength=n_parts)]).cpu().numpy()
+            bounds = np.cumsum(packed[ser_t.numel():])[:-1]
+            parts = np.split(packed[:ser_t.numel()], bounds)
             _check_parts(parts, n_parts)
             if cache is None:
                 plan._parts_cache = cache = {}

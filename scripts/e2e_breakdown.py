@@ -13,7 +13,7 @@ import paper_1109_3577_b200 as phj  # noqa: E402
 from paper_1109_3577_b200 import configs, patchy  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
-w = configs.CONFIGS[name]()
+w = configs.CONFIGS[name](dtype="float64") if name == "c5" else configs.CONFIGS[name]()
 r = phj.run_patchy(w.spec, w.pcfg, w.cfg)
 host = torch.empty(r.value.values.shape, dtype=r.value.values.dtype, pin_memory=True)
 

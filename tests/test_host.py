@@ -253,7 +253,7 @@ def test_device_partition_codes_match_numpy_partitions():
     # patchy._resolve_parts; run here on CPU tensors) equal the numpy forms
     import torch
 
-    for w in (configs.c2(n=257), configs.c3(n=65)):
+    for w in (configs.c2(n=257), configs.c3(n=65), configs.c5(n=65), configs.c5(n=129)):
         g = w.spec.make_grid(w.pcfg.fine_nodes)
         ser = np.nonzero(w.spec.target.contains(g.interior_points()))[0]
         want = w.pcfg.parts(w.spec.target, g, serials=ser)
