@@ -124,9 +124,11 @@ def slab_bounds(n_rows: int, n_ranks: int) -> list:
 
 def gather_slabs(compute, n_rows: int, row_elems: int, n_total: int, dtype, device):
     """A per-serial field computed by slabs: rank r calls
-    ``compute(begin, end, chunk)`` for its block rows (``chunk`` = the
-    contiguous serials of that slab) and the chunks are all-gathered.
-    Returns the first ``n_total`` elements of the assembled field."""
+    ``compute(begin, end, field)`` for its block rows -- it fills
+    ``field[begin * row_elems : end * row_elems]`` of the whole (padded) field
+    with values >= -1 -- and the slabs are all-gathered in place.  Returns the first
+    ``n_total`` elements (entries of other ranks are -1 when there is no
+    process group: a patched world() in the one-GPU projection of a share)."""
     import torch.distributed as td
 
     rank, n_ranks = world()
@@ -134,13 +136,17 @@ def gather_slabs(compute, n_rows: int, row_elems: int, n_total: int, dtype, devi
     per = (n_rows + n_ranks - 1) // n_ranks
     full = torch.full((n_ranks * per * row_elems,), -1, dtype=dtype, device=device)
     b, e = bounds[rank]
-    mine = full[rank * per * row_elems:(rank + 1) * per * row_elems]
     if e > b:
-        compute(b, e, mine)
+        compute(b, e, full)
     if n_ranks > 1 and td.is_available() and td.is_initialized():
-        td.all_gather_into_tensor(full, mine.clone())
-    # (a patched world() without a process group -- the one-GPU projection of
-    # a rank's share -- leaves the other ranks' slabs unfilled)
+        if full.is_cuda and td.get_backend() != "nccl":
+            # gloo has no all-gather of device tensors (the functional
+            # two-ranks-on-one-GPU check): the other ranks' entries are -1, the
+            # field's values are >= -1, so an element-wise MAX assembles it
+            td.all_reduce(full, op=td.ReduceOp.MAX)
+        else:
+            mine = full[rank * per * row_elems:(rank + 1) * per * row_elems]
+            td.all_gather_into_tensor(full, mine.clone())
     return full[:n_total]
 
 

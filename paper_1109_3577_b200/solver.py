@@ -859,27 +859,14 @@ def feedback_sharded(plan: StencilPlan, work: torch.Tensor, *, rule: str, dtype:
     row_elems = int(np.prod(plan.int_shape[1:]))
     ev = torch.zeros(1, dtype=torch.int64, device=plan.device)
 
-    def compute(r0, r1, chunk):
-        # chunk: the contiguous serials of block rows [r0, r1)
-        base = r0 * layers * row_elems
-        feedback_internal(plan, work, rule=rule, dtype=dtype, slab=(r0, r1),
-                          out=_OffsetView(chunk, base), ev=ev)
+    def compute(r0, r1, field):
+        # the kernel writes field[serial] for the serials of block rows [r0, r1)
+        feedback_internal(plan, work, rule=rule, dtype=dtype, slab=(r0, r1), out=field, ev=ev)
 
     out = dist.gather_slabs(compute, (n0 + layers - 1) // layers, layers * row_elems,
                             plan.grid.n_interior, torch.int32, plan.device)
     dist.sum_over_ranks(ev)
     return out, ev
-
-
-class _OffsetView:
-    """A tensor chunk addressed as if it started ``base`` elements earlier
-    (the kernel writes out[serial]; the chunk holds serials base ...)."""
-
-    def __init__(self, chunk: torch.Tensor, base: int):
-        self.chunk, self.base = chunk, base
-
-    def data_ptr(self) -> int:
-        return self.chunk.data_ptr() - self.base * self.chunk.element_size()
 
 
 def reduce_controls(control_set, a_star: np.ndarray, r: float) -> np.ndarray:

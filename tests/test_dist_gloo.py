@@ -147,11 +147,11 @@ def _slab_worker(rank, world, port, n_rows, row_elems, n_total, q):
     try:
         calls = []
 
-        def compute(b, e, chunk):
+        def compute(b, e, field):
             # the slab's serials hold their own global index
             calls.append((b, e))
-            n = (e - b) * row_elems
-            chunk[:n] = torch.arange(b * row_elems, e * row_elems, dtype=torch.int32)
+            field[b * row_elems:e * row_elems] = torch.arange(b * row_elems, e * row_elems,
+                                                              dtype=torch.int32)
 
         out = dist.gather_slabs(compute, n_rows, row_elems, n_total, torch.int32, "cpu")
         q.put((rank, calls, out.numpy().tolist()))
