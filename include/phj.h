@@ -301,6 +301,10 @@ typedef struct phj_transport_args {
  * no node changes by more than act_eps; color_sweeps = equivalent sweeps
  * */
 #define PHJ_TRANSPORT_ASYNC 1
+/* Jacobi transport: a work ticket buys two consecutive list entries instead
+ * of one (half the same-address claims per sweep; for launches that own few
+ * of the colours -- a rank of a multi-GPU run -- and find most entries empty) */
+#define PHJ_TRANSPORT_PAIRS 2
 
 /* argmax over the colours of a [n_colors][ext] colour field (strict >,
  * lowest colour on ties, patchy.py:251-256) */

@@ -65,6 +65,7 @@ class SolveArgs(ctypes.Structure):
 SOLVE_NO_PRUNE = 1  # PHJ_SOLVE_NO_PRUNE
 SOLVE_ASYNC = 2  # PHJ_SOLVE_ASYNC
 TRANSPORT_ASYNC = 1  # PHJ_TRANSPORT_ASYNC
+TRANSPORT_PAIRS = 2  # PHJ_TRANSPORT_PAIRS
 
 
 class TransportArgs(ctypes.Structure):

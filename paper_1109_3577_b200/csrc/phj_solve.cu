@@ -1988,6 +1988,7 @@ struct TransportParams {
   const int32_t* band_list;
   const int32_t* band_off;
   int n_band;
+  int chunk;  // list entries per work ticket (1 or 2; transport_kernel)
 };
 
 #ifndef PHJ_TRANSPORT_CTAS
@@ -2131,19 +2132,39 @@ __global__ void __launch_bounds__(kThreads, PHJ_TRANSPORT_CTAS) transport_kernel
 #pragma unroll
       for (int r = 0; r < NB; ++r) pe[r] = in[r] ? __ldg(&p.ent[ss[r]]) : -1;
     };
+    // A ticket buys kChunk consecutive list entries: the claims of a sweep all
+    // hit one counter, and same-address atomics serialise in L2 (54 k tickets
+    // of a config-5 sweep: 38 us, scripts/atomic_ticket_probe.cu), a floor
+    // every rank of a multi-GPU run pays in full.  Dynamic item q >= 1 of the
+    // warp is entry nwarps + kChunk * T[(q - 1) / kChunk + 1] + (q - 1) % kChunk.
+    // One entry per ticket keeps a single GPU best balanced (C5 transport
+    // 127 vs 130 ms with pairs); a rank that owns few colours finds most
+    // entries empty and is bound by the claims: pairs (PHJ_TRANSPORT_PAIRS)
+    // take rank 0 of 8 from 47.8 to 36.5 ms.
+    const int kChunk = p.chunk;
     int item = gwarp;
     int blk = item < cnt ? __ldcg(&list[item]) : 0;
-    int nxt = nwarps + __shfl_sync(FULL, ticket, 0);
+    int nxt = nwarps + kChunk * __shfl_sync(FULL, ticket, 0);  // q = 1: first entry of ticket 1
+    int qn = 1;                                                // stream position of nxt
     int nblk = (item < cnt && nxt < cnt) ? __ldcg(&list[nxt]) : 0;
-    if (lane == 0) ticket = ticket2;
     unsigned long long cm_l0 = 0ull;
     int e[NB];
     if (item < cnt) prefetch(blk, cm_l0, e);
     while (item < cnt) {
-      // lookahead: ticket of the item after next, next block's inputs
-      const int nn = nwarps + __shfl_sync(FULL, ticket, 0);
+      // lookahead: the item after next (a new ticket every kChunk items: the
+      // one claimed kChunk iterations ago), next block's inputs
+      int nn;
+      if ((qn & (kChunk - 1)) == 0) {
+        nn = nwarps + kChunk * __shfl_sync(FULL, ticket2, 0);
+        if (lane == 0) {
+          ticket = ticket2;
+          if (nxt < cnt && nn < cnt) ticket2 = atomicAdd(take, 1);
+        }
+      } else {
+        nn = nxt + 1;
+      }
+      ++qn;
       const int nnblk = (nxt < cnt && nn < cnt) ? __ldcg(&list[nn]) : 0;
-      if (lane == 0 && nxt < cnt && nn < cnt) ticket = atomicAdd(take, 1);
       unsigned long long ncm_l0 = 0ull;
       int ne[NB];
 #pragma unroll
@@ -3620,6 +3641,7 @@ static int transport_impl(const phj_transport_args* a) {
   p.band_list = banded ? a->band_list : nullptr;
   p.band_off = banded ? a->band_off : nullptr;
   p.n_band = banded ? a->n_band : 0;
+  p.chunk = (a->options & PHJ_TRANSPORT_PAIRS) ? 2 : 1;
   if (banded && (a->n_band >= a->max_sweeps || p.R > 64)) {
     phj_set_error("phj_transport: the banded pass needs n_band < max_sweeps and <= 64 colours");
     return PHJ_ERR_ARG;
