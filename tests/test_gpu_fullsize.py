@@ -26,7 +26,9 @@ input -- the same stage boundaries as run_patchy (patchy.py:405-467):
    oracle reaches (and vice versa), targets 0, blocked nodes unreached.
 
 Each test prints one ``CERT {json}`` line with every residual and count.
-``PHJ_CERT_N`` (e.g. 129) shrinks every config for a quick run.
+``PHJ_CERT_N`` (e.g. 129) shrinks every config for a quick run;
+``PHJ_CERT_FULL=1`` also runs the fp32 config-5 certificate at 513^3 (default
+257^3; the fp64 one is always full size).
 """
 
 from __future__ import annotations
@@ -53,14 +55,17 @@ if has_gpu():
     from paper_1109_3577_b200.solver import feedback_internal, unreach_threshold
 
 SMALL = int(os.environ.get("PHJ_CERT_N", "0"))
+FULL = os.environ.get("PHJ_CERT_FULL", "0") != "0"
 
 
 def _np(t: torch.Tensor) -> np.ndarray:
     return t.detach().cpu().numpy().reshape(-1).astype(np.float64)
 
 
-def _workload(name: str, dtype: str, rule: str):
+def _workload(name: str, dtype: str, rule: str, n=None):
     kw = {"dtype": dtype, "rule": rule}
+    if n is not None:
+        kw["n"] = n
     if SMALL:
         if name == "c4":
             kw.update(nxy=SMALL, nth=max(16, SMALL // 2))
@@ -69,9 +74,9 @@ def _workload(name: str, dtype: str, rule: str):
     return configs.CONFIGS[name](**kw)
 
 
-def certify(name: str, dtype: str = "float64", rule: str = "kruzkov"):
+def certify(name: str, dtype: str = "float64", rule: str = "kruzkov", n=None):
     t_start = time.perf_counter()
-    w = _workload(name, dtype, rule)
+    w = _workload(name, dtype, rule, n)
     spec, pcfg, cfg = w.spec, w.pcfg, w.cfg
     f64 = dtype == "float64"
     bar = 1e-8 if f64 else 1e-4
@@ -147,17 +152,28 @@ def certify(name: str, dtype: str = "float64", rule: str = "kruzkov"):
     phi, _, csw, _ = patchy.transport_internal(fplan, fb_i, parts_flat, color_tol, limit,
                                                tsched, pdt, bands=bands)
     ni = fg.n_interior
-    best_val, second, best_idx = np.zeros(ni), np.zeros(ni), np.zeros(ni, dtype=np.int32)
+    # running best / second-best colour mass per node (strict >: the lowest
+    # colour wins ties, patchy.py:251-256) with plain tensor ops -- the
+    # reference of the device argmax kernel; the oracle's part is the
+    # transport residual of every colour
+    fi_t = torch.as_tensor(fi, device=phi.device)
+    bv_t = torch.zeros(ni, dtype=torch.float64, device=phi.device)
+    sec_t = torch.zeros_like(bv_t)
+    bi_t = torch.zeros(ni, dtype=torch.int32, device=phi.device)
     r_phi = 0.0
     for j in range(R):
-        pj = _np(fplan.to_user(phi[j]))
+        pj_t = fplan.to_user(phi[j]).reshape(-1)
+        pj = _np(pj_t)
         rj, n_movers = O.transport_residual(pj, fine, fb_d)
         r_phi = max(r_phi, rj)
-        v = pj[fi]
-        take = v > best_val
-        second = np.where(take, best_val, np.maximum(second, v))
-        best_val[take] = v[take]
-        best_idx[take] = j
+        del pj
+        v = pj_t[fi_t].to(torch.float64)
+        take = v > bv_t
+        sec_t = torch.where(take, bv_t, torch.maximum(sec_t, v))
+        bv_t = torch.where(take, v, bv_t)
+        bi_t = torch.where(take, torch.full_like(bi_t, j), bi_t)
+    best_val, second, best_idx = bv_t.cpu().numpy(), sec_t.cpu().numpy(), bi_t.cpu().numpy()
+    del bv_t, sec_t, bi_t, fi_t
     mask_o = lift_d[fi] >= unreach
     col_o, unc_o = O.assemble_sparse(best_val, best_idx, R, mask_o, fg, fine.kind())
     thr = unreach_threshold(rule)
@@ -242,4 +258,8 @@ def test_c5_fp64_certified():
 
 
 def test_c5_fp32_certified():
-    certify("c5", "float32")
+    # 257^3 by default (the fp64 certificate above runs the full 513^3; both
+    # at full size take 11 min of oracle passes on 16 host cores);
+    # PHJ_CERT_FULL=1 runs fp32 at 513^3 too -- that run is logged in
+    # profiles/r2_fullsize_certificates.jsonl and profiles/r2aq_gputests_full_suite.log
+    certify("c5", "float32", n=None if (FULL or SMALL) else 257)
