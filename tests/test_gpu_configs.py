@@ -30,6 +30,12 @@ def _to_v(T):
     return np.where(T >= 0.5e9, 1.0, -np.expm1(-T))
 
 
+def _working(T, rule):
+    """The oracle's working variable from the API's T field: v (Kruzkov) or
+    u = T itself with the sentinel (reference rule)."""
+    return _to_v(T) if rule == "kruzkov" else np.asarray(T, dtype=float)
+
+
 def _run_both(w, color_tol=1e-12):
     """Device pipeline vs the oracle's.  Jacobi on both sides stops at the
     same tol; the asynchronous device schedule converges to within
@@ -59,13 +65,13 @@ def _values_on_oracle_labels(w, ores, fine):
     pm = phj.PatchMap(g, R, ores.color)
     lifted = phj.NodeField(g)  # not read by cold state-constrained solves
     val, _, _ = phj.solve_patches(w.spec, g, pm, lifted, w.pcfg, w.cfg)
-    return _to_v(val.numpy().reshape(-1))[fine.grid.interior_flat()]
+    return _working(val.numpy().reshape(-1), w.cfg.rule)[fine.grid.interior_flat()]
 
 
 def _compare(res, ores, fine, bar, name, w, tie_gap=1e-12, phi_gap=1e-9):
     g = fine.grid
     inner = g.interior_flat()
-    got_v = _to_v(res.value.numpy().reshape(-1))[inner]
+    got_v = _working(res.value.numpy().reshape(-1), w.cfg.rule)[inner]
     want_v = ores.value[inner]
     fb = res.feedback.indices.cpu().numpy()
     ties = ores.gaps < tie_gap
@@ -140,6 +146,17 @@ def test_c5_reduced_kruzkov_fp32():
     w = configs.c5(n=65, dtype="float32")
     res, ores, fine = _run_both(w)
     _compare(res, ores, fine, 1e-4, "c5@65 fp32", w, tie_gap=1e-5, phi_gap=1e-6)
+
+
+@pytest.mark.parametrize("name,kw", [("c2", {"n": 129}), ("c3", {"n": 65}),
+                                     ("c5", {"n": 65, "dtype": "float64"})])
+def test_reduced_reference_rule(name, kw):
+    # the API's default update rule (the reference's own: u <- min I[u] + h,
+    # sentinel 1e9) through the whole pipeline in 2D and 3D, Jacobi on both
+    # sides (same start, same stop): values, feedback, labels
+    w = configs.CONFIGS[name](rule="reference", schedule="jacobi", **kw)
+    res, ores, fine = _run_both(w)
+    _compare(res, ores, fine, 1e-8, f"{name} reference rule", w)
 
 
 def test_c1_reference_rule_full_pipeline_matches_oracle_gs():
