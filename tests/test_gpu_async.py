@@ -99,3 +99,38 @@ def test_sharded_feedback_of_two_ranks_assembles_the_full_field(monkeypatch):
     assert torch.equal(parts[0][:cut], full[:cut]) and torch.equal(parts[1][cut:], full[cut:])
     assert bool((parts[0][cut:] == -1).all()) and bool((parts[1][:cut] == -1).all())
     assert evs == int(ev_full.item())
+
+
+def test_async_transport_matches_the_reference_golden_colours():
+    """The asynchronous (in-place) 2D transport against the colour fields the
+    REAL reference produced (tests/golden/c1_patchy.npz, converged at 1e-12)
+    -- not only against the device's own Jacobi transport."""
+    import os
+
+    import numpy as np
+
+    import paper_1109_3577_b200 as phj
+    from paper_1109_3577_b200 import solver as S
+
+    c = np.load(os.path.join(os.path.dirname(__file__), "golden", "c1_patchy.npz"))
+    spec = phj.ProblemSpec(name="c1", dim=2, box_lo=(-2.0, -2.0), box_hi=(2.0, 2.0),
+                           dynamics=lambda X, a: np.tile(np.asarray(a, float), (len(X), 1)),
+                           control_set=phj.discretize_circle(32),
+                           target=phj.TargetSpec.ball((0.0, 0.0), 0.1),
+                           model=phj.ScaledSpeed(1.0))
+    g = phj.Grid(spec.box_lo, spec.box_hi, (101, 101))
+    plan = S.StencilPlan(g, spec)
+    fb = plan.serial_to_internal(torch.as_tensor(c["feedback"], device=plan.device,
+                                                 dtype=torch.int32)).contiguous()
+    parts = np.split(c["parts"], np.cumsum(c["part_sizes"])[:-1])
+    flat = [plan.user_serials_to_internal_flat(np.asarray(p, dtype=np.int64)) for p in parts]
+    for inner in (1, 8):
+        patchy.TRANSPORT_INNER[2] = inner
+        try:
+            phi, R, csw, _ = patchy.transport_internal(plan, fb, flat, 1e-12, 10 * 101, "async")
+        finally:
+            patchy.TRANSPORT_INNER[2] = 8
+        assert all(x > 0 for x in csw)
+        for j in range(R):
+            got = plan.to_user(phi[j]).cpu().numpy()
+            assert np.abs(got - c["phi"][j]).max() <= 1e-9, (inner, j)
